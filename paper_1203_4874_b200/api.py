@@ -1,0 +1,320 @@
+"""Python host API mirroring the reference ``cbp::`` decoder interface.
+
+Same function names, argument meaning and error behaviour as
+/root/reference/proj/core/include/cbp/decoder.hpp (decode_frame, spectral_deblur,
+estimate_kernel_width, sample_cofactors, complete_to_spectrum, resolve_scales,
+assemble_kernel, validate_pair) and encoder.hpp (encode_frame). All compute runs in
+libcbp_cuda.so through the C ABI of include/cbp_cuda.h; torch only supplies device
+memory and the current CUDA stream. Errors raise ``CbpError`` whose ``code`` is the
+reference ``Errc`` name and whose message carries the reference's
+"<Name>: <stage>: <detail>" text.
+
+Frames are numpy arrays or torch tensors shaped (rows, cols) or (channels, rows, cols);
+row index m is the z1 power (types.hpp:15-17).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import CbpError, DecodeCfg, DecodeInfo, KernelSlot  # noqa: F401
+
+AXIS_Z1, AXIS_Z2 = 0, 1
+
+_tls = threading.local()
+
+
+def context(device: int | None = None) -> N.Context:
+    """Per-thread, per-device context (decode_frame is reentrant)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = N.Context(device)
+    return ctxs[device]
+
+
+def _stream_ptr(device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dev_planes(x, device=None) -> torch.Tensor:
+    """float32, contiguous, on the GPU, shaped (..., channels, rows, cols)."""
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(x)
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    x = x.to(device=device, dtype=torch.float32)
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    return x.contiguous()
+
+
+def make_cfg(search_min=9, search_max=25, tau=1e-6, epsilon=None, gap_threshold=1e-9,
+             trust_hint=False, max_imag_energy=0.01, negative_weight_tol=0.01,
+             validate=True) -> DecodeCfg:
+    """DecodeConfig with the reference defaults (decoder.hpp:10-20)."""
+    return DecodeCfg(int(search_min), int(search_max), float(tau), int(epsilon is not None),
+                     0.0 if epsilon is None else float(epsilon), float(gap_threshold),
+                     int(bool(trust_hint)), float(max_imag_energy), float(negative_weight_tol),
+                     int(bool(validate)))
+
+
+def friendly_size(n: int) -> int:
+    return int(N.lib().cbp_friendly_size(int(n)))
+
+
+# ------------------------------------------------------------------ deconvolution
+def spectral_deblur(blurred, kernel, epsilon: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    """cbp::spectral_deblur (decoder.hpp:63, decoder.cpp:273-278).
+
+    ``blurred``: (rows, cols), (channels, rows, cols) or (batch, channels, rows, cols);
+    ``kernel``: t x t nonnegative weights summing to 1. Returns the latent on the GPU,
+    shaped like the input with rows-t+1 x cols-t+1 planes.
+    """
+    ndim = blurred.dim() if isinstance(blurred, torch.Tensor) else np.ndim(blurred)
+    x = _dev_planes(blurred)
+    x4 = x.unsqueeze(0) if x.dim() == 3 else x
+    B, ch, rows, cols = x4.shape
+    k = np.ascontiguousarray(np.asarray(kernel, dtype=np.float64))
+    if k.ndim != 2 or k.shape[0] != k.shape[1]:
+        raise CbpError(13, "DimMismatch: kernel weights must be width x width")
+    t = k.shape[0]
+    ctx = context(x4.device.index)
+    M, Nc = rows - t + 1, cols - t + 1
+    if out is None:  # output planes keep the input geometry; the top-left M x N is written
+        out = torch.empty((B, ch, rows, cols), dtype=torch.float32, device=x4.device)
+    ctx.check(N.lib().cbp_spectral_deblur(ctx.ptr, C.c_void_p(x4.data_ptr()), B, ch, rows, cols, cols,
+                                          k.ctypes.data_as(C.c_void_p), t, float(epsilon),
+                                          C.c_void_p(out.data_ptr()), out.shape[-1],
+                                          _stream_ptr(x4.device)))
+    out = out[..., :M, :Nc]
+    if ndim == 2:
+        return out[0, 0]
+    if ndim == 3:
+        return out[0]
+    return out
+
+
+# ----------------------------------------------------------------------- decode
+@dataclass
+class StageTimings:
+    """decoder.hpp:65-71 (CUDA-event milliseconds of the batch the frame was in)."""
+    polynomial_evaluation_ms: float = 0.0
+    kernel_degree_estimation_ms: float = 0.0
+    kernel_estimation_1d_ms: float = 0.0
+    kernel_estimation_2d_fft_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+@dataclass
+class DecodedFrame:
+    """decoder.hpp:73-80. ``latent`` is a GPU tensor (channels, M, N)."""
+    latent: torch.Tensor
+    kernel_estimate: np.ndarray
+    width_used: int
+    width_clamped: bool
+    stage_timings: StageTimings = field(default_factory=StageTimings)
+    validation_residual: float = 0.0
+    epsilon_used: float = 0.0
+
+
+def _as_batch(x) -> tuple[torch.Tensor, int]:
+    ndim = x.dim() if isinstance(x, torch.Tensor) else np.ndim(x)
+    t = _dev_planes(x)
+    if t.dim() == 3:
+        t = t.unsqueeze(0)
+    return t.contiguous(), ndim
+
+
+def decode_frames(pub, prv, hints=None, cfg: DecodeCfg | None = None) -> list[DecodedFrame]:
+    """Batched cbp::decode_frame: pub/prv shaped (batch, channels, rows, cols)."""
+    P, _ = _as_batch(pub)
+    Q, _ = _as_batch(prv)
+    if P.shape != Q.shape:
+        raise CbpError(13, "DimMismatch: pair frames disagree on dimensions")
+    B, ch, rows, cols = P.shape
+    cfg = cfg or make_cfg()
+    ctx = context(P.device.index)
+    out = torch.empty((B, ch, rows, cols), dtype=torch.float32, device=P.device)
+    hint_arr = None
+    if hints is not None:
+        hs = [hints] * B if np.isscalar(hints) else list(hints)
+        hint_arr = (C.c_int * B)(*[int(h) if h is not None else 0 for h in hs])
+    infos = (DecodeInfo * max(B, 1))()
+    ctx.check(N.lib().cbp_decode_frames(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), B, ch,
+                                        rows, cols, cols, hint_arr, C.byref(cfg), C.c_void_p(out.data_ptr()),
+                                        cols, infos, _stream_ptr(P.device)))
+    res = []
+    for b in range(B):
+        inf = infos[b]
+        t = inf.width_used
+        k = np.array(inf.kernel[: t * t]).reshape(t, t)
+        res.append(DecodedFrame(out[b, :, : rows - t + 1, : cols - t + 1], k, t, bool(inf.width_clamped),
+                                StageTimings(*list(inf.stage_ms)), inf.validation_residual, inf.epsilon_used))
+    return res
+
+
+def decode_frame(pub, prv, hint: int | None = None, cfg: DecodeCfg | None = None) -> DecodedFrame:
+    """cbp::decode_frame (decoder.hpp:82, decoder.cpp:280-378)."""
+    return decode_frames(pub, prv, None if hint is None else [hint], cfg)[0]
+
+
+def estimate_kernel_width(pub, prv, search_min: int, search_max: int, tau: float) -> tuple[int, bool]:
+    """cbp::estimate_kernel_width (decoder.hpp:29-30) -> (width, clamped)."""
+    P, _ = _as_batch(pub)
+    Q, _ = _as_batch(prv)
+    _, ch, rows, cols = P.shape
+    ctx = context(P.device.index)
+    w = C.c_int(); c = C.c_int()
+    ctx.check(N.lib().cbp_estimate_kernel_width(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), ch,
+                                                rows, cols, cols, search_min, search_max, tau, C.byref(w),
+                                                C.byref(c), _stream_ptr(P.device)))
+    return w.value, bool(c.value)
+
+
+def sample_slices(pub, prv, t: int, axis: int) -> tuple[np.ndarray, np.ndarray]:
+    """axis_roots_dft of luma(pub) / luma(prv) (fft.hpp:15-18): (t, L) complex each."""
+    P, _ = _as_batch(pub)
+    Q, _ = _as_batch(prv)
+    _, ch, rows, cols = P.shape
+    L = cols if axis == AXIS_Z1 else rows
+    sp = np.empty((t, L), np.complex128); sq = np.empty((t, L), np.complex128)
+    ctx = context(P.device.index)
+    ctx.check(N.lib().cbp_sample_slices(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), ch, rows,
+                                        cols, cols, t, axis, sp.ctypes.data_as(C.c_void_p),
+                                        sq.ctypes.data_as(C.c_void_p), _stream_ptr(P.device)))
+    return sp, sq
+
+
+def sample_cofactors(pub, prv, width: int, axis: int, gap_threshold: float = 1e-9):
+    """cbp::sample_cofactors (decoder.hpp:40-41) -> (values t x t complex, gaps)."""
+    P, _ = _as_batch(pub)
+    Q, _ = _as_batch(prv)
+    _, ch, rows, cols = P.shape
+    vals = np.empty((width, width), np.complex128); gaps = np.empty(width)
+    ctx = context(P.device.index)
+    ctx.check(N.lib().cbp_sample_cofactors(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), ch,
+                                           rows, cols, cols, width, axis, gap_threshold,
+                                           vals.ctypes.data_as(C.c_void_p), gaps.ctypes.data_as(C.c_void_p),
+                                           _stream_ptr(P.device)))
+    return vals, gaps
+
+
+def cofactor_solve_batch(p, q, t: int, gap_threshold: float = 1e-9):
+    """Batched cbp::cofactor_null_solve (poly.hpp:51-52): p, q (batch, len) complex."""
+    p = np.ascontiguousarray(np.atleast_2d(p), np.complex128)
+    q = np.ascontiguousarray(np.atleast_2d(q), np.complex128)
+    B, L = p.shape
+    k1 = np.empty((B, t), np.complex128); k2 = np.empty((B, t), np.complex128)
+    gaps = np.empty(B); st = np.zeros(B, np.int32)
+    ctx = context()
+    ctx.check(N.lib().cbp_cofactor_solve_batch(ctx.ptr, p.ctypes.data_as(C.c_void_p), q.ctypes.data_as(C.c_void_p),
+                                               B, L, t, gap_threshold, k1.ctypes.data_as(C.c_void_p),
+                                               k2.ctypes.data_as(C.c_void_p), gaps.ctypes.data_as(C.c_void_p),
+                                               st.ctypes.data_as(C.c_void_p), _stream_ptr(None)))
+    return k1, k2, gaps
+
+
+def cofactor_null_solve(p, q, t: int, gap_threshold: float = 1e-9):
+    """cbp::cofactor_null_solve for one pair -> (k1, k2, gap); p and q may differ in length."""
+    p = np.asarray(p, np.complex128).ravel(); q = np.asarray(q, np.complex128).ravel()
+    if len(p) < t or len(q) < t:
+        raise CbpError(1, "InvalidArgument: slice degree below cofactor degree")
+    L = max(len(p), len(q))  # zero padding leaves the stacked convolution system unchanged
+    pp = np.zeros(L, np.complex128); pp[: len(p)] = p
+    qq = np.zeros(L, np.complex128); qq[: len(q)] = q
+    k1, k2, g = cofactor_solve_batch(pp[None], qq[None], t, gap_threshold)
+    return k1[0], k2[0], float(g[0])
+
+
+def complete_to_spectrum(values, axis: int) -> np.ndarray:
+    """cbp::complete_to_spectrum (decoder.hpp:45)."""
+    v = np.ascontiguousarray(values, np.complex128); t = v.shape[0]
+    out = np.empty_like(v)
+    ctx = context()
+    ctx.check(N.lib().cbp_complete_to_spectrum(ctx.ptr, v.ctypes.data_as(C.c_void_p), t, axis,
+                                               out.ctypes.data_as(C.c_void_p), _stream_ptr(None)))
+    return out
+
+
+def resolve_scales(a_values, b_values):
+    """cbp::resolve_scales (decoder.hpp:54) -> (lambda, mu, residual)."""
+    a = np.ascontiguousarray(a_values, np.complex128); b = np.ascontiguousarray(b_values, np.complex128)
+    t = a.shape[0]
+    lam = np.empty(t, np.complex128); mu = np.empty(t, np.complex128); res = C.c_double()
+    ctx = context()
+    ctx.check(N.lib().cbp_resolve_scales(ctx.ptr, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p), t,
+                                         lam.ctypes.data_as(C.c_void_p), mu.ctypes.data_as(C.c_void_p),
+                                         C.byref(res), _stream_ptr(None)))
+    return lam, mu, res.value
+
+
+def assemble_kernel(a_spectrum, b_spectrum, lam, mu, max_imag_energy=0.01, negative_weight_tol=0.01) -> np.ndarray:
+    """cbp::assemble_kernel (decoder.hpp:57-59) -> t x t weights."""
+    a = np.ascontiguousarray(a_spectrum, np.complex128); b = np.ascontiguousarray(b_spectrum, np.complex128)
+    lam = np.ascontiguousarray(lam, np.complex128); mu = np.ascontiguousarray(mu, np.complex128)
+    t = a.shape[0]
+    w = np.empty((t, t))
+    ctx = context()
+    ctx.check(N.lib().cbp_assemble_kernel(ctx.ptr, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                          lam.ctypes.data_as(C.c_void_p), mu.ctypes.data_as(C.c_void_p), t,
+                                          max_imag_energy, negative_weight_tol, w.ctypes.data_as(C.c_void_p),
+                                          _stream_ptr(None)))
+    return w
+
+
+def validate_pair(pub, prv, k1, k2) -> float:
+    """cbp::validate_pair (decoder.hpp:85-86)."""
+    P, _ = _as_batch(pub)
+    Q, _ = _as_batch(prv)
+    _, ch, rows, cols = P.shape
+    k1 = np.ascontiguousarray(k1, np.float64); k2 = np.ascontiguousarray(k2, np.float64)
+    if k1.shape != k2.shape:
+        raise CbpError(13, "DimMismatch: kernel widths differ")
+    r = C.c_double()
+    ctx = context(P.device.index)
+    ctx.check(N.lib().cbp_validate_pair(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), ch, rows, cols,
+                                        cols, k1.ctypes.data_as(C.c_void_p), k2.ctypes.data_as(C.c_void_p),
+                                        k1.shape[0], C.byref(r), _stream_ptr(P.device)))
+    return r.value
+
+
+def encode_frame(latent, k1, k2) -> tuple[torch.Tensor, torch.Tensor]:
+    """cbp::encode_frame on the device (encoder.cpp:83-103): (public, private) FP32 planes."""
+    X, ndim = _as_batch(latent)
+    B, ch, rows, cols = X.shape
+    k1 = np.ascontiguousarray(k1, np.float64); k2 = np.ascontiguousarray(k2, np.float64)
+    t = k1.shape[0]
+    ro, co = rows + t - 1, cols + t - 1
+    pub = torch.empty((B, ch, ro, co), dtype=torch.float32, device=X.device)
+    prv = torch.empty_like(pub)
+    ctx = context(X.device.index)
+    ctx.check(N.lib().cbp_encode_frames(ctx.ptr, C.c_void_p(X.data_ptr()), B, ch, rows, cols, cols,
+                                        k1.ctypes.data_as(C.c_void_p), k2.ctypes.data_as(C.c_void_p), t,
+                                        C.c_void_p(pub.data_ptr()), C.c_void_p(prv.data_ptr()), co,
+                                        _stream_ptr(X.device)))
+    if ndim == 2:
+        return pub[0, 0], prv[0, 0]
+    if ndim == 3:
+        return pub[0], prv[0]
+    return pub, prv
+
+
+def synth_frames(planes: int, rows: int, cols: int, seed: int, device=None) -> torch.Tensor:
+    """Device-generated U[0,1) planes for benchmarking (not the reference's mt19937_64 stream)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    out = torch.empty((planes, rows, cols), dtype=torch.float32, device=dev)
+    ctx = context(dev.index)
+    ctx.check(N.lib().cbp_synth_frames(ctx.ptr, C.c_void_p(out.data_ptr()), planes, rows, cols, cols,
+                                       C.c_uint64(seed), _stream_ptr(dev)))
+    return out

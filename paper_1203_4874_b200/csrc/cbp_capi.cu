@@ -1,0 +1,300 @@
+// C ABI: context, workspaces, FFT plans/tables and the fixed-kernel deconvolution
+// entry points (reference decoder.cpp:273-278 spectral_deblur).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "cbp_ctx.cuh"
+
+using namespace cbp_dev;
+
+namespace cbp_host {
+
+const char* errc_name(int status) {  // error.cpp:5-27, status = 1 + Errc
+  static const char* names[] = {
+      "InvalidArgument", "NonUnitSamplePoint", "DegenerateInput", "IllConditioned",
+      "CoprimalityFailure", "FrameTooSmall", "RangeExceeded", "NotQuantized",
+      "InconsistentAxes", "IllConditionedSlice", "DegenerateScales", "NonRealKernel",
+      "DimMismatch", "IoFailure", "CorruptManifest", "MissingFrame", "FormatViolation",
+      "PairMismatch"};
+  if (status >= 1 && status <= 18) return names[status - 1];
+  if (status == CBP_CUDA_ERROR) return "CudaError";
+  if (status == CBP_UNSUPPORTED) return "Unsupported";
+  return status == 0 ? "Ok" : "Error";
+}
+
+int set_error(cbp_ctx* ctx, int status, const std::string& msg) {
+  if (ctx) ctx->err = std::string(errc_name(status)) + ": " + msg;
+  return status;
+}
+
+int cuda_check(cbp_ctx* ctx, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  return set_error(ctx, CBP_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void* workspace(cbp_ctx* ctx, int id, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->ws_bytes[id] >= bytes) return ctx->ws[id];
+  if (ctx->ws[id]) {
+    cudaDeviceSynchronize();  // growth is rare: never inside a steady-state loop
+    cudaFree(ctx->ws[id]);
+  }
+  ctx->ws[id] = nullptr;
+  ctx->ws_bytes[id] = 0;
+  size_t want = bytes + bytes / 8;
+  if (cudaMalloc(&ctx->ws[id], want) != cudaSuccess) return nullptr;
+  ctx->ws_bytes[id] = want;
+  return ctx->ws[id];
+}
+
+const float2* twiddles(cbp_ctx* ctx, int n) {
+  auto it = ctx->tw.find(n);
+  if (it != ctx->tw.end()) return it->second;
+  std::vector<float2> h(size_t(std::max(n, 1)));
+  for (int k = 0; k < n; ++k) {
+    const double ang = -2.0 * M_PI * double(k) / double(n);
+    h[k] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+  }
+  float2* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(float2)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  ctx->tw[n] = d;
+  return d;
+}
+
+FftPlan make_plan(int n) {
+  FftPlan p{};
+  p.n = n;
+  p.nst = 0;
+  int r = n;
+  while (r % 8 == 0 && r != 16) p.radix[p.nst++] = 8, r /= 8;  // 16 -> 4 x 4
+  while (r % 4 == 0) p.radix[p.nst++] = 4, r /= 4;
+  while (r % 2 == 0) p.radix[p.nst++] = 2, r /= 2;
+  while (r % 9 == 0) p.radix[p.nst++] = 9, r /= 9;
+  while (r % 3 == 0) p.radix[p.nst++] = 3, r /= 3;
+  while (r % 5 == 0) p.radix[p.nst++] = 5, r /= 5;
+  while (r % 7 == 0) p.radix[p.nst++] = 7, r /= 7;
+  if (r != 1) p.nst = -1;  // not 2/3/5/7-smooth
+  return p;
+}
+
+int friendly_size(int n) {  // fft.cpp:272-280
+  if (n < 1) return -1;
+  for (int m = n;; ++m) {
+    int r = m;
+    for (int f : {2, 3, 5, 7})
+      while (r % f == 0) r /= f;
+    if (r == 1) return m;
+  }
+}
+
+int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
+  std::memset(&a, 0, sizeof(a));
+  a.Mb = Mb;
+  a.Nb = Nb;
+  a.Gr = friendly_size(Mb);
+  a.Gc = friendly_size(Nb);
+  a.Hc = a.Gc / 2 + 1;
+  a.even = (a.Gc % 2 == 0) ? 1 : 0;
+  const int L = a.even ? a.Gc / 2 : a.Gc;
+  a.plan_row = make_plan(L);
+  a.plan_col = make_plan(a.Gr);
+  if (a.plan_row.nst < 0 || a.plan_col.nst < 0)
+    return set_error(ctx, CBP_UNSUPPORTED, "transform grid is not 2/3/5/7-smooth");
+  a.xp = (a.Hc + 3) & ~3;
+  // rows per CTA for passes A/C: keep 2*rpc*L*8 bytes <= 64 KB, at most 8 rows
+  int rpc = 8;
+  while (rpc > 1 && size_t(2) * rpc * L * sizeof(float2) > 64 * 1024) rpc /= 2;
+  a.rows_per_cta = rpc;
+  a.col_width = deblur_col_width(a.Gr, CBP_MAX_WIDTH);
+  a.tw_row = twiddles(ctx, L);
+  a.tw_post = twiddles(ctx, a.Gc);
+  a.tw_col = twiddles(ctx, a.Gr);
+  if (!a.tw_row || !a.tw_post || !a.tw_col)
+    return set_error(ctx, CBP_CUDA_ERROR, "twiddle table allocation failed");
+  if (size_t(2) * rpc * L * sizeof(float2) > 200 * 1024)
+    return set_error(ctx, CBP_UNSUPPORTED, "frame too wide for the shared-memory row transform");
+  return 0;
+}
+
+int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
+               size_t out_plane_stride, cudaStream_t stream) {
+  // Group whole frames so the half spectrum of a group (written by pass A, read and
+  // rewritten by B, read by C) stays resident in the 126 MB L2.
+  const size_t plane_bytes = size_t(a.Mb) * a.xp * sizeof(float2);
+  const int ch = std::max(a.channels, 1);
+  const size_t budget = 40ull << 20;
+  int frames_per_group = int(std::max<size_t>(1, budget / (plane_bytes * ch)));
+  const int frames = planes / ch;
+  frames_per_group = std::min(frames_per_group, std::max(frames, 1));
+  const int group_planes = frames_per_group * ch;
+  float2* X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * group_planes));
+  if (!X) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  a.X = X;
+  a.x_plane = size_t(a.Mb) * a.xp;
+  a.in_plane = in_plane_stride;
+  a.out_plane = out_plane_stride;
+  const float* in0 = a.in;
+  float* out0 = a.out;
+  const cbp_kernel_slot* slot0 = a.slot;
+  for (int p0 = 0; p0 < planes; p0 += group_planes) {
+    const int np = std::min(group_planes, planes - p0);
+    a.in = in0 + size_t(p0) * in_plane_stride;
+    a.out = out0 + size_t(p0) * out_plane_stride;
+    a.slot = slot0 + (a.slot_per_frame ? p0 / ch : 0);
+    int st = cuda_check(ctx, launch_deblur(a, np, stream), "deconvolution launch");
+    if (st) return st;
+  }
+  return 0;
+}
+
+}  // namespace cbp_host
+
+using namespace cbp_host;
+
+extern "C" {
+
+void cbp_decode_cfg_default(cbp_decode_cfg* c) {  // decoder.hpp:10-20
+  c->search_min = 9;
+  c->search_max = 25;
+  c->tau = 1e-6;
+  c->has_epsilon = 0;
+  c->epsilon = 0.0;
+  c->gap_threshold = 1e-9;
+  c->trust_hint = 0;
+  c->max_imag_energy = 0.01;
+  c->negative_weight_tol = 0.01;
+  c->validate = 1;
+}
+
+const char* cbp_errc_name(int status) { return errc_name(status); }
+int cbp_friendly_size(int n) { return friendly_size(n); }
+
+int cbp_create(int device, cbp_ctx** out) {
+  if (!out) return CBP_INVALID_ARGUMENT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return CBP_CUDA_ERROR;
+  if (device < 0 || device >= n) return CBP_INVALID_ARGUMENT;
+  if (cudaSetDevice(device) != cudaSuccess) return CBP_CUDA_ERROR;
+  cbp_ctx* ctx = new cbp_ctx();
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMallocHost(&ctx->host_slot, sizeof(cbp_kernel_slot)) != cudaSuccess) {
+    delete ctx;
+    return CBP_CUDA_ERROR;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return 0;
+}
+
+void cbp_destroy(cbp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : ctx->tw) cudaFree(kv.second);
+  for (void* p : ctx->ws)
+    if (p) cudaFree(p);
+  if (ctx->host_slot) cudaFreeHost(ctx->host_slot);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+const char* cbp_last_error(const cbp_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+// validate_kernel (kernel.cpp:7-17)
+static int check_kernel(cbp_ctx* ctx, const double* w, int t) {
+  if (!(t >= 1 && t % 2 == 1 && t <= CBP_MAX_WIDTH))
+    return set_error(ctx, CBP_INVALID_ARGUMENT, "kernel width must be odd and >= 1");
+  double s = 0.0, mn = 1e300;
+  for (int i = 0; i < t * t; ++i) {
+    if (!std::isfinite(w[i])) return set_error(ctx, CBP_INVALID_ARGUMENT, "kernel weights must be finite");
+    mn = std::min(mn, w[i]);
+  }
+  if (mn < 0.0) return set_error(ctx, CBP_INVALID_ARGUMENT, "kernel weights must be nonnegative");
+  for (int n = 0; n < t; ++n)
+    for (int m = 0; m < t; ++m) s += w[m * t + n];
+  if (std::abs(s - 1.0) > 1e-9)
+    return set_error(ctx, CBP_INVALID_ARGUMENT, "kernel weights must sum to 1");
+  return 0;
+}
+
+static int check_geometry(cbp_ctx* ctx, int batch, int channels, int rows, int cols, int ld) {
+  if (batch < 0) return set_error(ctx, CBP_INVALID_ARGUMENT, "batch must be >= 0");
+  if (!(channels == 1 || channels == 3))
+    return set_error(ctx, CBP_DIM_MISMATCH, "frame must have 1 or 3 planes");
+  if (rows < 1 || cols < 1) return set_error(ctx, CBP_DIM_MISMATCH, "empty frame plane");
+  if (ld < cols) return set_error(ctx, CBP_INVALID_ARGUMENT, "row pitch smaller than the row");
+  return 0;
+}
+
+int cbp_spectral_deblur(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels, int rows,
+                        int cols, int ld, const double* kernel, int t, double epsilon,
+                        float* latent_dev, int ld_out, void* stream) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  int st = check_kernel(ctx, kernel, t);
+  if (st) return st;
+  if (!(epsilon >= 0.0)) return set_error(ctx, CBP_INVALID_ARGUMENT, "epsilon must be nonnegative");
+  if ((st = check_geometry(ctx, batch, channels, rows, cols, ld))) return st;
+  if (rows < t || cols < t)
+    return set_error(ctx, CBP_FRAME_TOO_SMALL, "blurred frame smaller than the kernel");
+  if (batch == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cbp_kernel_slot* slot = static_cast<cbp_kernel_slot*>(workspace(ctx, WS_SLOTS, sizeof(cbp_kernel_slot) * 64));
+  if (!slot) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  // stage the fixed kernel into a context-owned slot (pinned, stream-ordered)
+  if ((st = cuda_check(ctx, cudaStreamSynchronize(s), "stream sync"))) return st;
+  cbp_kernel_slot* h = ctx->host_slot;
+  std::memset(h, 0, offsetof(cbp_kernel_slot, weights));
+  h->width = t;
+  h->epsilon = epsilon;
+  std::memcpy(h->weights, kernel, sizeof(double) * t * t);
+  if ((st = cuda_check(ctx, cudaMemcpyAsync(slot, h, sizeof(cbp_kernel_slot), cudaMemcpyHostToDevice, s),
+                       "slot upload")))
+    return st;
+  DeblurArgs a;
+  if ((st = deblur_setup(ctx, rows, cols, a))) return st;
+  a.in = blurred_dev;
+  a.in_ld = ld;
+  a.out = latent_dev;
+  a.out_ld = ld_out;
+  a.slot = slot;
+  a.slot_per_frame = 0;
+  a.channels = channels;
+  return deblur_run(ctx, a, batch * channels, size_t(rows) * ld, size_t(rows) * ld_out, s);
+}
+
+int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,
+                             int rows, int cols, int ld, const cbp_kernel_slot* slot_dev,
+                             float* latent_dev, int ld_out, void* stream) {
+  if (!ctx || !slot_dev) return CBP_INVALID_ARGUMENT;
+  int st = check_geometry(ctx, batch, channels, rows, cols, ld);
+  if (st) return st;
+  if (batch == 0) return 0;
+  DeblurArgs a;
+  if ((st = deblur_setup(ctx, rows, cols, a))) return st;
+  a.in = blurred_dev;
+  a.in_ld = ld;
+  a.out = latent_dev;
+  a.out_ld = ld_out;
+  a.slot = slot_dev;
+  a.slot_per_frame = 0;
+  a.channels = channels;
+  return deblur_run(ctx, a, batch * channels, size_t(rows) * ld, size_t(rows) * ld_out,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int cbp_read_slots(cbp_ctx* ctx, const cbp_kernel_slot* slots_dev, int count,
+                   cbp_kernel_slot* slots_host, void* stream) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int st = cuda_check(ctx, cudaMemcpyAsync(slots_host, slots_dev, sizeof(cbp_kernel_slot) * count,
+                                           cudaMemcpyDeviceToHost, s), "slot read");
+  if (st) return st;
+  return cuda_check(ctx, cudaStreamSynchronize(s), "slot read sync");
+}
+
+}  // extern "C"

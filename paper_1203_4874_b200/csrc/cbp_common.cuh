@@ -1,0 +1,74 @@
+// Shared device helpers for the CBP sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/cbp_cuda.h"
+
+namespace cbp_dev {
+
+// ---------------------------------------------------------------- complex math
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__host__ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+__host__ __device__ __forceinline__ double2 zadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+__host__ __device__ __forceinline__ double2 zcmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__host__ __device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
+__host__ __device__ __forceinline__ double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ double zabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double zabs(double2 a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+// exp(-2*pi*i * k / n) in FP64
+__device__ __forceinline__ double2 zroot(long k, long n) {
+  double s, c;
+  sincospi(-2.0 * double(k % n) / double(n), &s, &c);
+  return make_double2(c, s);
+}
+
+// ------------------------------------------------------------- frame geometry
+struct FrameGeom {
+  int batch, channels, rows, cols, ld;
+  __host__ __device__ size_t plane_elems() const { return size_t(rows) * ld; }
+  __host__ __device__ const float* plane(const float* base, int b, int c) const {
+    return base + (size_t(b) * channels + c) * plane_elems();
+  }
+};
+
+// Rec.601 luma on the fly (image.cpp:41-45): identity for gray, same association
+// order as Eigen's 0.299*R + 0.587*G + 0.114*B.
+__device__ __forceinline__ double luma_at(const float* p0, size_t plane, int channels, size_t off) {
+  if (channels == 1) return double(__ldg(p0 + off));
+  double r = __ldg(p0 + off), g = __ldg(p0 + plane + off), b = __ldg(p0 + 2 * plane + off);
+  // unfused, like the reference's Eigen expression (bit-identical to the CPU restatement)
+  return __dadd_rn(__dadd_rn(__dmul_rn(0.299, r), __dmul_rn(0.587, g)), __dmul_rn(0.114, b));
+}
+
+// Record the first failure on a slot (status stays the first error).
+__device__ __forceinline__ void slot_fail(cbp_kernel_slot* s, int status, int stage, int axis,
+                                          int slice, double value, int reason) {
+  if (atomicCAS(&s->status, 0, status) == 0) {
+    s->fail_stage = stage;
+    s->fail_axis = axis;
+    s->fail_slice = slice;
+    s->fail_value = value;
+    s->fail_reason = reason;
+  }
+}
+
+}  // namespace cbp_dev

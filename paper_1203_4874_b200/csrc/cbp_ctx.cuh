@@ -1,0 +1,54 @@
+// Host-side context shared by the C-ABI translation units.
+#pragma once
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cbp_deblur.cuh"
+#include "cbp_fft.cuh"
+
+struct cbp_ctx {
+  int device = 0;
+  std::string err;
+  std::map<int, float2*> tw;  // n -> exp(-2 pi i k / n), k < n (device, FP64-rounded)
+  // device workspaces, grown on demand (never inside a launch sequence)
+  void* ws[16] = {};
+  size_t ws_bytes[16] = {};
+  cbp_kernel_slot* host_slot = nullptr;  // pinned staging
+  cudaEvent_t ev[8] = {};
+  int num_sms = 148;
+};
+
+namespace cbp_host {
+
+enum Workspace {
+  WS_X = 0,       // deconvolution half spectrum
+  WS_SLOTS = 1,   // kernel slots owned by the context
+  WS_PART = 2,    // fold partial sums
+  WS_FOLD = 3,    // folds
+  WS_SLICES = 4,  // unit-circle slices
+  WS_SOLVE = 5,   // cofactor solutions
+  WS_MISC = 6,
+  WS_PUB = 7,     // host-pipeline staging
+  WS_PRV = 8,
+  WS_OUT = 9,
+  WS_RED = 10,    // validation partial sums
+};
+
+const char* errc_name(int status);
+int set_error(cbp_ctx* ctx, int status, const std::string& msg);
+int cuda_check(cbp_ctx* ctx, cudaError_t e, const char* what);
+void* workspace(cbp_ctx* ctx, int id, size_t bytes);
+const float2* twiddles(cbp_ctx* ctx, int n);
+cbp_dev::FftPlan make_plan(int n);
+int friendly_size(int n);
+
+// Fills the deconvolution geometry (grid, plans, tables) for a Mb x Nb plane.
+int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, cbp_dev::DeblurArgs& a);
+// Runs passes A/B/C over `planes` planes of one batch in L2-sized groups.
+int deblur_run(cbp_ctx* ctx, cbp_dev::DeblurArgs a, int planes, size_t in_plane_stride,
+               size_t out_plane_stride, cudaStream_t stream);
+
+}  // namespace cbp_host

@@ -1,0 +1,36 @@
+// Launch interface of the three-pass deconvolution (see cbp_deblur.cu).
+#pragma once
+
+#include "cbp_fft.cuh"
+
+namespace cbp_dev {
+
+struct DeblurArgs {
+  const float* in;  // blurred planes: plane p at in + p*in_plane, rows of in_ld floats
+  size_t in_plane;
+  int in_ld;
+  float* out;  // latent planes
+  size_t out_plane;
+  int out_ld;
+  float2* X;  // half-spectrum workspace: plane p at X + p*x_plane, rows of xp
+  size_t x_plane;
+  int xp;
+  int Mb, Nb;       // blurred plane extent
+  int Gr, Gc, Hc;   // grid and half-spectrum width Gc/2+1
+  int even;         // Gc even: half-length complex row transform
+  int rows_per_cta; // pass A/C rows per CTA
+  int col_width;    // pass B columns per CTA
+  const cbp_kernel_slot* slot;
+  int slot_per_frame;  // 1: slot[p / channels]; 0: slot[0] for every plane
+  int channels;
+  FftPlan plan_row;  // length Gc/2 (even) or Gc
+  FftPlan plan_col;  // length Gr
+  const float2* tw_row;   // exp(-2 pi i k / plan_row.n)
+  const float2* tw_post;  // exp(-2 pi i k / Gc), k <= Gc/2
+  const float2* tw_col;   // exp(-2 pi i k / Gr)
+};
+
+int deblur_col_width(int Gr, int t_max);
+cudaError_t launch_deblur(DeblurArgs a, int planes, cudaStream_t stream);
+
+}  // namespace cbp_dev

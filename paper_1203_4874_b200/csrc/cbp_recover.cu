@@ -1,0 +1,1347 @@
+// Kernel recovery on the device: sampling, width search, per-slice cofactor solves,
+// scale resolution / kernel assembly, validation residual and CBP generation.
+// Every stage keeps the reference's FP64 arithmetic (decoder.cpp, poly.cpp, fft.cpp);
+// inputs are the FP32 frames as stored in HBM.
+#include "cbp_linalg.cuh"
+#include "cbp_recover.cuh"
+
+namespace cbp_dev {
+
+constexpr int kSolveMaxWidth = 31;  // 2t x 2t complex Gram + eigenvectors in shared memory
+
+// ----------------------------------------------------------------- slots
+__global__ void k_init_slots(RecoverArgs a, const int* hints) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.batch) return;
+  cbp_kernel_slot* s = a.slots + b;
+  s->status = 0;
+  s->fail_stage = 0;
+  s->fail_axis = -1;
+  s->fail_slice = -1;
+  s->fail_reason = 0;
+  s->fail_value = 0.0;
+  s->clamped = 0;
+  s->width_z1 = s->width_z2 = 0;
+  s->residual = 0.0;
+  s->scale_residual = 0.0;
+  s->epsilon = 0.0;
+  const int h = hints ? hints[b] : 0;
+  s->width = (a.trust_hint && h > 0) ? h : 0;  // decoder.cpp:302-306
+  a.flags[b] = 0;
+}
+
+cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_dev, cudaStream_t s) {
+  k_init_slots<<<(a.batch + 127) / 128, 128, 0, s>>>(a, hints_dev);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ int fold_width(const RecoverArgs& a, int b, int t_fixed) {
+  return t_fixed > 0 ? t_fixed : a.slots[b].width;
+}
+__device__ __forceinline__ int rows_per_block(int t) { return t * ((128 + t - 1) / t); }
+
+// ---------------------------------------------------- polynomial evaluation
+// Z1 fold (fft.cpp:206-208): fold[r][n] = sum_{m = r mod t} luma[m][n]. Partial sums
+// per block of rows_per_block(t) rows; grid (ceil(cols/256), nrb, batch*2).
+__global__ void __launch_bounds__(256) k_fold_z1_part(RecoverArgs a, int t_fixed) {
+  const int b = blockIdx.z >> 1, q = blockIdx.z & 1;
+  const cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = fold_width(a, b, t_fixed);
+  if (t <= 0) return;
+  const int RB = rows_per_block(t);
+  const int rb = blockIdx.y;
+  const int r0 = rb * RB;
+  if (r0 >= a.rows) return;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.cols) return;
+  const size_t plane = size_t(a.rows) * a.ld;
+  const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane;
+  const int r1 = min(r0 + RB, a.rows);
+  double* out = a.part + (((size_t(b) * 2 + q) * a.nrb + rb) * a.t_max) * a.cols + n;
+  for (int r = 0; r < t; ++r) {
+    double acc = 0.0;
+    for (int m = r0 + r; m < r1; m += t) acc += luma_at(base, plane, a.channels, size_t(m) * a.ld + n);
+    out[size_t(r) * a.cols] = acc;
+  }
+}
+
+// Sum the row-block partials in a fixed order, then the t x t DFT epilogue:
+// slice_i[n] = sum_r W(i, r) fold[r][n], W(i, r) = exp(-2 pi i ((i r) mod t) / t)
+// (fft.cpp:203-208). grid (ceil(cols/128), batch*2), smem t_max*128 doubles + roots.
+__global__ void __launch_bounds__(128) k_fold_z1_dft(RecoverArgs a, int t_fixed) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
+  const cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = fold_width(a, b, t_fixed);
+  if (t <= 0) return;
+  double2* root = reinterpret_cast<double2*>(sh);
+  double* fold = sh + 2 * a.t_max;
+  for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
+  __syncthreads();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.cols) return;
+  const int RB = rows_per_block(t);
+  const int nrb = (a.rows + RB - 1) / RB;
+  const double* part = a.part + ((size_t(b) * 2 + q) * a.nrb * a.t_max) * a.cols + n;
+  for (int r = 0; r < t; ++r) {
+    double acc = 0.0;
+    for (int rb = 0; rb < nrb; ++rb) acc += part[(size_t(rb) * a.t_max + r) * a.cols];
+    fold[r * blockDim.x + threadIdx.x] = acc;
+  }
+  double2* out = a.slices + slice_offset(a, b, 0, q, 0) + n;
+  for (int i = 0; i < t; ++i) {
+    double re = 0.0, im = 0.0;
+    int idx = 0;
+    for (int r = 0; r < t; ++r) {
+      const double f = fold[r * blockDim.x + threadIdx.x];
+      re = fma(root[idx].x, f, re);
+      im = fma(root[idx].y, f, im);
+      idx += i;
+      if (idx >= t) idx -= t;
+    }
+    out[size_t(i) * a.lmax] = make_double2(re, im);
+  }
+}
+
+// Z2 fold (fft.cpp:210-212) with one warp per row, then its DFT epilogue. Also flags
+// negative luma (decoder.cpp:52) and non-finite samples (image.cpp:33).
+// grid (ceil(rows/4), batch*2), block 128, smem 4 warps * t_max * 33 doubles + roots.
+__global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
+  cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = fold_width(a, b, t_fixed);
+  if (t <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* root = reinterpret_cast<double2*>(sh);
+  double* acc = sh + 2 * a.t_max + size_t(warp) * a.t_max * 33;
+  double* fold = acc + size_t(a.t_max) * 32;
+  for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
+  __syncthreads();
+  const int m = blockIdx.x * 4 + warp;
+  if (m >= a.rows) return;
+  for (int r = 0; r < t; ++r) acc[r * 32 + lane] = 0.0;
+  __syncwarp();
+  const size_t plane = size_t(a.rows) * a.ld;
+  const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane + size_t(m) * a.ld;
+  const int step = 32 % t;
+  int r = lane % t;
+  bool neg = false, bad = false;
+  for (int n = lane; n < a.cols; n += 32) {
+    const double x = luma_at(base, plane, a.channels, n);
+    neg |= x < 0.0;
+    bad |= !isfinite(x);
+    acc[r * 32 + lane] += x;
+    r += step;
+    if (r >= t) r -= t;
+  }
+  if (__any_sync(0xffffffffu, neg) && lane == 0) atomicOr(a.flags + b, 1);
+  if (__any_sync(0xffffffffu, bad) && lane == 0)
+    slot_fail(slot, CBP_RANGE_EXCEEDED, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_NONFINITE);
+  __syncwarp();
+  for (int rr = lane; rr < t; rr += 32) {
+    double s = 0.0;
+    for (int l = 0; l < 32; ++l) s += acc[rr * 32 + l];
+    fold[rr] = s;
+  }
+  __syncwarp();
+  double2* out = a.slices + slice_offset(a, b, 1, q, 0) + m;
+  for (int i = lane; i < t; i += 32) {
+    double re = 0.0, im = 0.0;
+    int idx = 0;
+    for (int rr = 0; rr < t; ++rr) {
+      re = fma(root[idx].x, fold[rr], re);
+      im = fma(root[idx].y, fold[rr], im);
+      idx += i;
+      if (idx >= t) idx -= t;
+    }
+    out[size_t(i) * a.lmax] = make_double2(re, im);
+  }
+}
+
+cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
+  const int tm = t_fixed > 0 ? t_fixed : a.t_max;
+  RecoverArgs b = a;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_fold_z1_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_fold_z2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cfg = true;
+  }
+  dim3 g1((a.cols + 255) / 256, a.nrb, a.batch * 2);
+  k_fold_z1_part<<<g1, 256, 0, s>>>(b, t_fixed);
+  dim3 g2((a.cols + 127) / 128, a.batch * 2);
+  size_t sm2 = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
+  k_fold_z1_dft<<<g2, 128, sm2, s>>>(b, t_fixed);
+  dim3 g3((a.rows + 3) / 4, a.batch * 2);
+  size_t sm3 = (2 * a.t_max + 4 * size_t(a.t_max) * 33) * sizeof(double);
+  k_fold_z2<<<g3, 128, sm3, s>>>(b, t_fixed);
+  (void)tm;
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------- kernel degree estimation
+// One CTA per (size s, axis, frame): s x s leading Bezout block of the DC slices
+// (poly.cpp:66-79), then sigma_min / sigma_max by one-sided Jacobi (poly.cpp:81-91).
+__global__ void __launch_bounds__(256) k_width_blocks(RecoverArgs a) {
+  extern __shared__ double2 shz[];
+  __shared__ int flag;
+  __shared__ double sv[CBP_MAX_WIDTH + 1];
+  const int si = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
+  const cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0 || slot->width > 0) return;  // failed or hinted
+  if (a.flags[b] & 1) return;                         // signed content: see k_width_pick
+  const int s = a.search_min + 2 * si;
+  if (s > a.search_max) return;
+  const int L = axis == 0 ? a.cols : a.rows;
+  const double2* p = a.slices + slice_offset(a, b, axis, 0, 0);
+  const double2* q = a.slices + slice_offset(a, b, axis, 1, 0);
+  double2* A = shz;  // column-major s x s
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) {
+    const int i = idx % s, j = idx / s;
+    double re = 0.0, im = 0.0;
+    const int kmax = min(i, j);
+    for (int k = 0; k <= kmax; ++k) {
+      const int hi = i + j + 1 - k;
+      const double2 ph = hi < L ? p[hi] : make_double2(0, 0);
+      const double2 qh = hi < L ? q[hi] : make_double2(0, 0);
+      const double2 pk = k < L ? p[k] : make_double2(0, 0);
+      const double2 qk = k < L ? q[k] : make_double2(0, 0);
+      const double2 u = zmul(ph, qk), v = zmul(qh, pk);
+      re += u.x - v.x;
+      im += u.y - v.y;
+    }
+    A[j * s + i] = make_double2(re, im);
+  }
+  __syncthreads();
+  onesided_sv(A, s, s, sv, &flag);
+  if (threadIdx.x == 0) {
+    double mx = 0.0, mn = 1e300;
+    for (int i = 0; i < s; ++i) mx = fmax(mx, sv[i]), mn = fmin(mn, sv[i]);
+    a.ratios[(size_t(b) * 2 + axis) * a.nsizes + si] = mx == 0.0 ? 0.0 : mn / mx;
+  }
+}
+
+// Per frame: all-zero check, first singular size per axis, axis agreement
+// (decoder.cpp:38-44, 83-89).
+__global__ void __launch_bounds__(128) k_width_pick(RecoverArgs a) {
+  const int b = blockIdx.x;
+  cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0 || slot->width > 0) return;
+  __shared__ int nz[4];
+  if (threadIdx.x < 4) nz[threadIdx.x] = 0;
+  __syncthreads();
+  for (int axis = 0; axis < 2; ++axis) {
+    const int L = axis == 0 ? a.cols : a.rows;
+    for (int q = 0; q < 2; ++q) {
+      const double2* v = a.slices + slice_offset(a, b, axis, q, 0);
+      bool any = false;
+      for (int i = threadIdx.x; i < L; i += blockDim.x) any |= (v[i].x != 0.0 || v[i].y != 0.0);
+      if (__syncthreads_or(any) && threadIdx.x == 0) nz[axis * 2 + q] = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (a.flags[b] & 1) {  // signed content -> axis_spectrum_half path (decoder.cpp:65-82)
+    slot_fail(slot, CBP_UNSUPPORTED, CBP_STAGE_KERNEL_DEGREE_ESTIMATION, -1, -1, 0.0, CBP_REASON_SIGNED);
+    return;
+  }
+  int w[2];
+  bool cl[2];
+  for (int axis = 0; axis < 2; ++axis) {
+    if (!nz[axis * 2] || !nz[axis * 2 + 1]) {
+      slot_fail(slot, CBP_DEGENERATE_INPUT, CBP_STAGE_KERNEL_DEGREE_ESTIMATION, -1, -1, 0.0,
+                CBP_REASON_ZERO_POLY);
+      return;
+    }
+    w[axis] = a.search_max;
+    cl[axis] = true;
+    for (int si = 0; si < a.nsizes; ++si) {
+      const double r = a.ratios[(size_t(b) * 2 + axis) * a.nsizes + si];
+      if (r < a.tau) {
+        w[axis] = a.search_min + 2 * si;
+        cl[axis] = false;
+        break;
+      }
+    }
+  }
+  slot->width_z1 = w[0];
+  slot->width_z2 = w[1];
+  if (w[0] != w[1]) {
+    slot_fail(slot, CBP_INCONSISTENT_AXES, CBP_STAGE_KERNEL_DEGREE_ESTIMATION, -1, -1, 0.0,
+              CBP_REASON_AXES_DISAGREE);
+    return;
+  }
+  slot->width = w[0];
+  slot->clamped = (cl[0] && cl[1]) ? 1 : 0;
+}
+
+cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
+  dim3 g(a.nsizes, 2, a.batch);
+  size_t sm = size_t(a.search_max) * a.search_max * sizeof(double2);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cfg = true;
+  }
+  k_width_blocks<<<g, 256, sm, s>>>(a);
+  k_width_pick<<<a.batch, 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------ kernel estimation 1D
+// cofactor_null_solve (poly.cpp:93-121) for one slice pair. A = [T_t(p) | -T_t(q)]
+// ((max(lp,lq)+t-1) x 2t); its Gram A^H A is block-Toeplitz and is filled from the
+// auto/cross correlations of p and q at lags -(t-1)..(t-1). Hermitian Jacobi gives the
+// eigenpairs; the null vector is then refined with residuals r = A x computed directly
+// from p, q (so its accuracy is not limited by the squared conditioning of the Gram),
+// and the gap sigma_{2t-2}/sigma_0 uses the direct residual norm |A v_2|.
+struct SolveSmem {
+  double2* G;     // n x n
+  double2* V;     // n x n
+  double2* corr;  // 4t-1 lags: pp[0..t-1], qq[0..t-1], pq[-(t-1)..t-1]
+  double2* x;     // n
+  double2* g;     // n
+  double2* coef;  // n
+  double* red;    // 32
+  JacobiScratch js;
+};
+
+__device__ __forceinline__ double2 ld_or0(const double2* v, int i, int len) {
+  return (i >= 0 && i < len) ? v[i] : make_double2(0.0, 0.0);
+}
+
+// r = A x for x (length 2t in smem); returns |r|^2 (block-reduced), r stored in scratch.
+__device__ double apply_A(const double2* p, int lp, const double2* q, int lq, int t, const double2* x,
+                          double2* r, int R, double* red) {
+  double loc = 0.0;
+  for (int nn = threadIdx.x; nn < R; nn += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    const int j0 = max(0, nn - max(lp, lq) + 1), j1 = min(t - 1, nn);
+    for (int j = j0; j <= j1; ++j) {
+      const double2 pv = ld_or0(p, nn - j, lp), qv = ld_or0(q, nn - j, lq);
+      const double2 a = zmul(pv, x[j]), c = zmul(qv, x[t + j]);
+      acc.x += a.x - c.x;
+      acc.y += a.y - c.y;
+    }
+    r[nn] = acc;
+    loc += zabs2(acc);
+  }
+  loc = warp_sum(loc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = loc;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) tot += red[w];
+  __syncthreads();
+  return tot;
+}
+
+// g = A^H r (length 2t) into smem.
+__device__ void apply_AH(const double2* p, int lp, const double2* q, int lq, int t, const double2* r,
+                         double2* g) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < 2 * t; j += nw) {
+    const bool isq = j >= t;
+    const int sh = isq ? j - t : j;
+    const double2* v = isq ? q : p;
+    const int len = isq ? lq : lp;
+    double re = 0.0, im = 0.0;
+    for (int m = lane; m < len; m += 32) {
+      const double2 c = zcmul(v[m], r[m + sh]);
+      re += c.x;
+      im += c.y;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) g[j] = isq ? make_double2(-re, -im) : make_double2(re, im);
+  }
+  __syncthreads();
+}
+
+struct SolveResult {
+  double gap;
+  int status;  // 0, CBP_REASON_GAP
+};
+
+// Whole CTA. On return x[0..2t) holds the unit-norm, phase-normalized null vector [k2; k1].
+__device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double2* q, int lq, int t,
+                                          double gap_threshold, double2* r, SolveSmem sm) {
+  const int n = 2 * t;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // correlations: c(x, y, d) = sum_m conj(x[m]) y[m + d]
+  const int nl = 4 * t - 1;
+  for (int l = warp; l < nl; l += nw) {
+    const double2 *xv, *yv;
+    int lx, ly, d;
+    if (l < t) {
+      xv = p, yv = p, lx = lp, ly = lp, d = l;
+    } else if (l < 2 * t) {
+      xv = q, yv = q, lx = lq, ly = lq, d = l - t;
+    } else {
+      xv = p, yv = q, lx = lp, ly = lq, d = l - 2 * t - (t - 1);
+    }
+    double re = 0.0, im = 0.0;
+    const int m0 = max(0, -d), m1 = min(lx, ly - d);
+    for (int m = m0 + lane; m < m1; m += 32) {
+      const double2 c = zcmul(xv[m], yv[m + d]);
+      re += c.x;
+      im += c.y;
+    }
+    re = warp_sum(re);
+    im = warp_sum(im);
+    if (lane == 0) sm.corr[l] = make_double2(re, im);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += blockDim.x) {
+    const int j = idx / n, k = idx - j * n;
+    double2 v;
+    if (j < t && k < t) {
+      const int d = j - k;
+      v = d >= 0 ? sm.corr[d] : zconj(sm.corr[-d]);
+    } else if (j >= t && k >= t) {
+      const int d = (j - t) - (k - t);
+      v = d >= 0 ? sm.corr[t + d] : zconj(sm.corr[t - d]);
+    } else if (j < t) {  // -r_pq[j - k']
+      const double2 c = sm.corr[2 * t + (t - 1) + (j - (k - t))];
+      v = make_double2(-c.x, -c.y);
+    } else {  // -conj(r_pq[k - j'])
+      const double2 c = sm.corr[2 * t + (t - 1) + (k - (j - t))];
+      v = make_double2(-c.x, c.y);
+    }
+    sm.G[j * n + k] = v;
+  }
+  __syncthreads();
+  herm_jacobi(sm.G, n, sm.V, n, n, sm.js);
+  __shared__ int kmin_s, k2_s;
+  __shared__ double lmax_s, lmin_s;
+  if (tid == 0) {
+    int k0 = 0;
+    for (int k = 1; k < n; ++k)
+      if (sm.G[k * n + k].x < sm.G[k0 * n + k0].x) k0 = k;
+    int k1 = -1;
+    for (int k = 0; k < n; ++k)
+      if (k != k0 && (k1 < 0 || sm.G[k * n + k].x < sm.G[k1 * n + k1].x)) k1 = k;
+    double mx = 0.0;
+    for (int k = 0; k < n; ++k) mx = fmax(mx, sm.G[k * n + k].x);
+    kmin_s = k0;
+    k2_s = k1;
+    lmax_s = mx;
+    lmin_s = sm.G[k0 * n + k0].x;
+  }
+  __syncthreads();
+  const int kmin = kmin_s;
+  for (int i = tid; i < n; i += blockDim.x) sm.x[i] = sm.V[i * n + kmin];
+  __syncthreads();
+  const int R = max(lp, lq) + t - 1;
+  // two steps of residual-corrected refinement of the null vector
+  for (int it = 0; it < 2 && n > 1; ++it) {
+    apply_A(p, lp, q, lq, t, sm.x, r, R, sm.red);
+    apply_AH(p, lp, q, lq, t, r, sm.g);
+    for (int k = tid; k < n; k += blockDim.x) {
+      double2 c = make_double2(0.0, 0.0);
+      const double den = sm.G[k * n + k].x - lmin_s;
+      if (k != kmin && den > 1e-30 * lmax_s) {
+        for (int i = 0; i < n; ++i) {
+          const double2 u = zcmul(sm.V[i * n + k], sm.g[i]);
+          c.x += u.x;
+          c.y += u.y;
+        }
+        c = zscale(c, 1.0 / den);
+      }
+      sm.coef[k] = c;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+      double2 d = make_double2(0.0, 0.0);
+      for (int k = 0; k < n; ++k) {
+        const double2 u = zmul(sm.V[i * n + k], sm.coef[k]);
+        d.x += u.x;
+        d.y += u.y;
+      }
+      sm.g[i] = zsub(sm.x[i], d);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += zabs2(sm.g[i]);
+      sm.red[0] = 1.0 / sqrt(s);
+    }
+    __syncthreads();
+    const double inv = sm.red[0];
+    for (int i = tid; i < n; i += blockDim.x) sm.x[i] = zscale(sm.g[i], inv);
+    __syncthreads();
+  }
+  // gap = sigma_{2t-2} / sigma_0 (poly.cpp:105-110) with sigma_{2t-2} = |A v_2|
+  double sig2 = 0.0;
+  if (n >= 2) {
+    for (int i = tid; i < n; i += blockDim.x) sm.g[i] = sm.V[i * n + k2_s];
+    __syncthreads();
+    sig2 = sqrt(apply_A(p, lp, q, lq, t, sm.g, r, R, sm.red));
+  }
+  const double sig0 = sqrt(fmax(lmax_s, 0.0));
+  SolveResult res;
+  res.gap = sig0 == 0.0 ? 0.0 : sig2 / sig0;
+  res.status = res.gap < gap_threshold ? CBP_REASON_GAP : 0;
+  // normalize_phase (poly.cpp:18-23): largest |x_i| (first index) real positive
+  if (tid == 0) {
+    int im = 0;
+    double best = -1.0;
+    for (int i = 0; i < n; ++i) {
+      const double v = zabs(sm.x[i]);
+      if (v > best) best = v, im = i;
+    }
+    const double a = zabs(sm.x[im]);
+    if (a > 0.0) {
+      const double2 rot = zscale(zconj(sm.x[im]), 1.0 / a);
+      for (int i = 0; i < n; ++i) sm.x[i] = zmul(sm.x[i], rot);
+    }
+  }
+  __syncthreads();
+  return res;
+}
+
+__host__ __device__ inline size_t solve_smem_bytes(int t) {
+  const int n = 2 * t;
+  return (size_t(2) * n * n + (4 * t - 1) + 3 * n + (n / 2 + 1)) * sizeof(double2) +
+         (32 + 2 * (n / 2 + 1)) * sizeof(double) + 16;
+}
+
+__device__ SolveSmem carve_solve(void* base, int t) {
+  const int n = 2 * t;
+  SolveSmem sm;
+  double2* z = static_cast<double2*>(base);
+  sm.G = z;
+  z += n * n;
+  sm.V = z;
+  z += n * n;
+  sm.corr = z;
+  z += 4 * t - 1;
+  sm.x = z;
+  z += n;
+  sm.g = z;
+  z += n;
+  sm.coef = z;
+  z += n;
+  sm.js.e = z;
+  z += n / 2 + 1;
+  double* d = reinterpret_cast<double*>(z);
+  sm.red = d;
+  d += 32;
+  sm.js.cs = d;
+  d += n / 2 + 1;
+  sm.js.sn = d;
+  d += n / 2 + 1;
+  sm.js.flag = reinterpret_cast<int*>(d);
+  return sm;
+}
+
+// grid (t_max, 2 axes, batch): slice i of axis `axis` of frame b (decoder.cpp:94-123).
+__global__ void __launch_bounds__(256) k_solve(RecoverArgs a) {
+  extern __shared__ double2 shs[];
+  const int i = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
+  cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  if (t > kSolveMaxWidth) {  // the 2t x 2t Gram and eigenvectors must fit in shared memory
+    if (i == 0 && axis == 0 && threadIdx.x == 0)
+      slot_fail(slot, CBP_UNSUPPORTED, CBP_STAGE_KERNEL_ESTIMATION_1D, -1, -1, 0.0, CBP_REASON_WIDTH_LIMIT);
+    return;
+  }
+  if (i >= t) return;
+  const int L = axis == 0 ? a.cols : a.rows;
+  const double2* p = a.slices + slice_offset(a, b, axis, 0, i);
+  const double2* q = a.slices + slice_offset(a, b, axis, 1, i);
+  double2* r = a.scratch + ((size_t(b) * 2 + axis) * a.t_max + i) * size_t(a.lmax + a.t_max);
+  SolveSmem sm = carve_solve(shs, t);
+  SolveResult res = cofactor_solve_cta(p, L, q, L, t, a.gap_threshold, r, sm);
+  // k1 = tail, unit norm, into row i (z1) or column i (z2)
+  __shared__ double nrm;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < t; ++k) s += zabs2(sm.x[t + k]);
+    nrm = sqrt(s);
+  }
+  __syncthreads();
+  const size_t base = (size_t(b) * 2 + axis) * a.t_max;
+  if (threadIdx.x == 0) {
+    a.gaps[base + i] = res.gap;
+    a.slice_status[base + i] = res.status ? res.status : (nrm == 0.0 ? CBP_REASON_VANISHING_COFACTOR : 0);
+  }
+  double2* vals = a.values + base * a.t_max;
+  if (nrm > 0.0)
+    for (int k = threadIdx.x; k < t; k += blockDim.x) {
+      const double2 v = zscale(sm.x[t + k], 1.0 / nrm);
+      if (axis == 0)
+        vals[i * t + k] = v;
+      else
+        vals[k * t + i] = v;
+    }
+}
+
+cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  const int tc = min(a.t_max, kSolveMaxWidth);
+  dim3 g(tc, 2, a.batch);
+  k_solve<<<g, 256, solve_smem_bytes(tc), s>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_cofactor_batch(const double2* P, int lp, const double2* Q, int lq,
+                                                        int t, double gap_threshold, double2* k1, double2* k2,
+                                                        double* gaps, int* status, double2* scratch) {
+  extern __shared__ double2 shs[];
+  const int b = blockIdx.x;
+  SolveSmem sm = carve_solve(shs, t);
+  SolveResult res = cofactor_solve_cta(P + size_t(b) * lp, lp, Q + size_t(b) * lq, lq, t, gap_threshold,
+                                       scratch + size_t(b) * (max(lp, lq) + t), sm);
+  for (int k = threadIdx.x; k < t; k += blockDim.x) {
+    k2[size_t(b) * t + k] = sm.x[k];
+    k1[size_t(b) * t + k] = sm.x[t + k];
+  }
+  if (threadIdx.x == 0) {
+    gaps[b] = res.gap;
+    status[b] = res.status ? CBP_ILL_CONDITIONED : 0;
+  }
+}
+
+cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, int lq, int batch, int t,
+                                  double gap_threshold, double2* k1, double2* k2, double* gaps,
+                                  int* status, double2* scratch, cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_cofactor_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  k_cofactor_batch<<<batch, 256, solve_smem_bytes(t), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
+                                                            status, scratch);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------- kernel estimation 2D
+// complete_to_spectrum (decoder.cpp:240-246): Z1 values*W, Z2 W*values.
+__device__ void complete_cta(const double2* vals, int t, int axis, const double2* root, double2* out) {
+  for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
+    const int i = idx / t, j = idx - i * t;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < t; ++k) {
+      const double2 w = root[axis == 0 ? (k * j) % t : (i * k) % t];
+      const double2 v = axis == 0 ? vals[i * t + k] : vals[k * t + j];
+      const double2 u = zmul(axis == 0 ? v : w, axis == 0 ? w : v);
+      acc.x += u.x;
+      acc.y += u.y;
+    }
+    out[idx] = acc;
+  }
+}
+
+struct ComposeSmem {
+  double2 *root, *A, *B, *G, *V, *x, *g, *coef, *r, *K, *T;
+  double* w;  // t*t
+  double* red;
+  JacobiScratch js;
+};
+
+__device__ ComposeSmem carve_compose(void* base, int t) {
+  const int n = 2 * t;
+  ComposeSmem s;
+  double2* z = static_cast<double2*>(base);
+  s.root = z, z += t;
+  s.A = z, z += t * t;
+  s.B = z, z += t * t;
+  s.G = z, z += n * n;
+  s.V = z, z += n * n;
+  s.x = z, z += n;
+  s.g = z, z += n;
+  s.coef = z, z += n;
+  s.r = z, z += t * t;
+  s.K = z, z += t * t;
+  s.T = z, z += t * t;
+  s.js.e = z, z += n / 2 + 1;
+  double* d = reinterpret_cast<double*>(z);
+  s.w = d, d += t * t;
+  s.red = d, d += 32;
+  s.js.cs = d, d += n / 2 + 1;
+  s.js.sn = d, d += n / 2 + 1;
+  s.js.flag = reinterpret_cast<int*>(d);
+  return s;
+}
+
+__host__ __device__ inline size_t compose_smem_bytes(int t) {
+  const int n = 2 * t;
+  return (size_t(t) + 5 * t * t + 2 * n * n + 3 * n + (n / 2 + 1)) * sizeof(double2) +
+         (size_t(t) * t + 32 + 2 * (n / 2 + 1)) * sizeof(double) + 16;
+}
+
+// sys row i*t+j: col i = -B'(i,j), col t+j = A'(i,j) (decoder.cpp:137-143); r = sys x.
+__device__ double sys_apply(const ComposeSmem& s, int t, const double2* x) {
+  for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
+    const int i = idx / t, j = idx - i * t;
+    const double2 u = zmul(s.B[idx], x[i]), v = zmul(s.A[idx], x[t + j]);
+    s.r[idx] = make_double2(v.x - u.x, v.y - u.y);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int idx = 0; idx < t * t; ++idx) acc += zabs2(s.r[idx]);
+    s.red[0] = acc;
+  }
+  __syncthreads();
+  const double v = s.red[0];
+  __syncthreads();
+  return v;
+}
+
+// resolve_completed (decoder.cpp:133-155) via the 2t x 2t Gram of the t^2 x 2t system
+// plus direct-residual refinement. Returns 0 or CBP_REASON_SCALE_RATIO; x holds
+// [lambda; mu]; *residual = |sys x|, *ratio = min|x|/max|x|.
+__device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* ratio) {
+  const int n = 2 * t;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int j = idx / n, k = idx - j * n;
+    double2 v = make_double2(0.0, 0.0);
+    if (j < t && k < t) {
+      if (j == k) {
+        double acc = 0.0;
+        for (int jj = 0; jj < t; ++jj) acc += zabs2(s.B[j * t + jj]);
+        v.x = acc;
+      }
+    } else if (j >= t && k >= t) {
+      if (j == k) {
+        double acc = 0.0;
+        for (int ii = 0; ii < t; ++ii) acc += zabs2(s.A[ii * t + (j - t)]);
+        v.x = acc;
+      }
+    } else if (j < t) {  // conj(-B(j,k')) * A(j,k')
+      const double2 u = zcmul(s.B[j * t + (k - t)], s.A[j * t + (k - t)]);
+      v = make_double2(-u.x, -u.y);
+    } else {  // conj(A(k, j')) * (-B(k, j'))
+      const double2 u = zcmul(s.A[k * t + (j - t)], s.B[k * t + (j - t)]);
+      v = make_double2(-u.x, -u.y);
+    }
+    s.G[idx] = v;
+  }
+  __syncthreads();
+  herm_jacobi(s.G, n, s.V, n, n, s.js);
+  __shared__ int kmin_s;
+  __shared__ double lmax_s, lmin_s;
+  if (threadIdx.x == 0) {
+    int k0 = 0;
+    double mx = 0.0;
+    for (int k = 0; k < n; ++k) {
+      if (s.G[k * n + k].x < s.G[k0 * n + k0].x) k0 = k;
+      mx = fmax(mx, s.G[k * n + k].x);
+    }
+    kmin_s = k0;
+    lmax_s = mx;
+    lmin_s = s.G[k0 * n + k0].x;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s.x[i] = s.V[i * n + kmin_s];
+  __syncthreads();
+  for (int it = 0; it < 2; ++it) {
+    sys_apply(s, t, s.x);
+    // g = sys^H r
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double2 acc = make_double2(0.0, 0.0);
+      if (j < t) {
+        for (int jj = 0; jj < t; ++jj) {
+          const double2 u = zcmul(s.B[j * t + jj], s.r[j * t + jj]);
+          acc.x -= u.x;
+          acc.y -= u.y;
+        }
+      } else {
+        for (int ii = 0; ii < t; ++ii) {
+          const double2 u = zcmul(s.A[ii * t + (j - t)], s.r[ii * t + (j - t)]);
+          acc.x += u.x;
+          acc.y += u.y;
+        }
+      }
+      s.g[j] = acc;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      double2 c = make_double2(0.0, 0.0);
+      const double den = s.G[k * n + k].x - lmin_s;
+      if (k != kmin_s && den > 1e-30 * lmax_s) {
+        for (int i = 0; i < n; ++i) {
+          const double2 u = zcmul(s.V[i * n + k], s.g[i]);
+          c.x += u.x;
+          c.y += u.y;
+        }
+        c = zscale(c, 1.0 / den);
+      }
+      s.coef[k] = c;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double2 d = make_double2(0.0, 0.0);
+      for (int k = 0; k < n; ++k) {
+        const double2 u = zmul(s.V[i * n + k], s.coef[k]);
+        d.x += u.x;
+        d.y += u.y;
+      }
+      s.g[i] = zsub(s.x[i], d);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) acc += zabs2(s.g[i]);
+      s.red[1] = 1.0 / sqrt(acc);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s.x[i] = zscale(s.g[i], s.red[1]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {  // normalize_phase (poly.cpp:18-23)
+    int im = 0;
+    double best = -1.0;
+    for (int i = 0; i < n; ++i) {
+      const double v = zabs(s.x[i]);
+      if (v > best) best = v, im = i;
+    }
+    const double a = zabs(s.x[im]);
+    if (a > 0.0) {
+      const double2 rot = zscale(zconj(s.x[im]), 1.0 / a);
+      for (int i = 0; i < n; ++i) s.x[i] = zmul(s.x[i], rot);
+    }
+  }
+  __syncthreads();
+  *residual = sqrt(sys_apply(s, t, s.x));
+  double mx = 0.0, mn = 1e300;
+  for (int i = 0; i < n; ++i) {
+    const double v = zabs(s.x[i]);
+    mx = fmax(mx, v);
+    mn = fmin(mn, v);
+  }
+  *ratio = mx == 0.0 ? 0.0 : mn / mx;
+  return (mx == 0.0 || mn < 1e-10 * mx) ? CBP_REASON_SCALE_RATIO : 0;
+}
+
+// realize_kernel (decoder.cpp:159-176) on s.K (t x t complex, serial on thread 0).
+// Returns 0 or a CBP_REASON_* of non_real_kernel; writes s.w.
+__device__ int realize_serial(ComposeSmem& s, int t, double max_imag, double neg_tol, double* value) {
+  double2 mass = make_double2(0.0, 0.0);
+  for (int i = 0; i < t * t; ++i) mass = zadd(mass, s.K[i]);
+  const double am = zabs(mass);
+  if (!(am > 0.0)) return CBP_REASON_VANISHING_MASS;
+  const double2 rot = zscale(zconj(mass), 1.0 / am);
+  double total = 0.0, imag = 0.0;
+  for (int i = 0; i < t * t; ++i) {
+    s.K[i] = zmul(s.K[i], rot);
+    total += zabs2(s.K[i]);
+    imag += s.K[i].y * s.K[i].y;
+  }
+  if (!(total > 0.0)) return CBP_REASON_ZERO_KERNEL;
+  if (imag > max_imag * total) {
+    *value = imag / total;
+    return CBP_REASON_IMAG_ENERGY;
+  }
+  double mx = -1e300, mn = 1e300;
+  for (int i = 0; i < t * t; ++i) mx = fmax(mx, s.K[i].x), mn = fmin(mn, s.K[i].x);
+  if (!(mx > 0.0)) return CBP_REASON_NO_POSITIVE;
+  if (mn < -neg_tol * mx) {
+    *value = mn / mx;
+    return CBP_REASON_NEGATIVE_WEIGHT;
+  }
+  double sum = 0.0;
+  for (int i = 0; i < t * t; ++i) sum += fmax(s.K[i].x, 0.0);
+  for (int i = 0; i < t * t; ++i) s.w[i] = fmax(s.K[i].x, 0.0) / sum;
+  return 0;
+}
+
+// ifft2 of a t x t spectrum (fft.cpp:191-195, 1/t^2) from s.K into s.K (via s.T).
+__device__ void ifft2_small(ComposeSmem& s, int t) {
+  for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {  // along columns index v
+    const int u = idx / t, nn = idx - u * t;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int v = 0; v < t; ++v) acc = zadd(acc, zmul(s.K[u * t + v], zconj(s.root[(v * nn) % t])));
+    s.T[idx] = acc;
+  }
+  __syncthreads();
+  const double sc = 1.0 / (double(t) * double(t));
+  for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
+    const int m = idx / t, nn = idx - m * t;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int u = 0; u < t; ++u) acc = zadd(acc, zmul(s.T[u * t + nn], zconj(s.root[(u * m) % t])));
+    s.K[idx] = zscale(acc, sc);
+  }
+  __syncthreads();
+}
+
+// assemble_kernel (decoder.cpp:256-271) from s.A, s.B, lambda = x[0:t], mu = x[t:2t].
+// Returns a CBP status (0, DEGENERATE_SCALES, NON_REAL_KERNEL); weights in `out`.
+__device__ int assemble_cta(ComposeSmem& s, int t, double max_imag, double neg_tol, double* out,
+                            int* reason, double* value) {
+  __shared__ int st_s, rs_s;
+  __shared__ double val_s;
+  if (threadIdx.x == 0) {
+    st_s = 0;
+    double mnl = 1e300, mnm = 1e300;
+    for (int i = 0; i < t; ++i) mnl = fmin(mnl, zabs(s.x[i])), mnm = fmin(mnm, zabs(s.x[t + i]));
+    if (!(mnl > 0.0 && mnm > 0.0)) st_s = CBP_DEGENERATE_SCALES, rs_s = CBP_REASON_SCALE_ZERO;
+  }
+  __syncthreads();
+  if (st_s) {
+    *reason = rs_s;
+    return st_s;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
+      const int i = idx / t, j = idx - i * t;
+      s.K[idx] = pass == 0 ? zdiv(s.A[idx], s.x[i]) : zdiv(s.B[idx], s.x[t + j]);
+    }
+    __syncthreads();
+    ifft2_small(s, t);
+    if (threadIdx.x == 0) {
+      double v = 0.0;
+      int r = realize_serial(s, t, max_imag, neg_tol, &v);
+      if (r) {
+        st_s = CBP_NON_REAL_KERNEL, rs_s = r, val_s = v;
+      } else {
+        for (int i = 0; i < t * t; ++i) out[i] = pass == 0 ? 0.5 * s.w[i] : out[i] + 0.5 * s.w[i];
+      }
+    }
+    __syncthreads();
+    if (st_s) {
+      *reason = rs_s;
+      *value = val_s;
+      return st_s;
+    }
+  }
+  return 0;
+}
+
+// One CTA per frame: first failing slice (reference order), complete_to_spectrum x2,
+// resolve, assemble, epsilon (decoder.cpp:333-353).
+__global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
+  extern __shared__ double2 shc[];
+  const int b = blockIdx.x;
+  cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  const size_t base0 = size_t(b) * 2 * a.t_max;
+  // the reference solves z1 slices 0..t-1 then z2 and stops at the first failure
+  if (threadIdx.x == 0) {
+    for (int axis = 0; axis < 2 && slot->status == 0; ++axis)
+      for (int i = 0; i < t; ++i) {
+        const int st = a.slice_status[base0 + size_t(axis) * a.t_max + i];
+        if (st) {
+          slot_fail(slot, CBP_ILL_CONDITIONED_SLICE, CBP_STAGE_KERNEL_ESTIMATION_1D, axis, i,
+                    a.gaps[base0 + size_t(axis) * a.t_max + i], st);
+          break;
+        }
+      }
+  }
+  __syncthreads();
+  if (slot->status != 0) return;
+  ComposeSmem s = carve_compose(shc, t);
+  for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
+  __syncthreads();
+  const double2* v1 = a.values + base0 * a.t_max;
+  const double2* v2 = a.values + (base0 + a.t_max) * a.t_max;
+  complete_cta(v1, t, 0, s.root, s.A);
+  complete_cta(v2, t, 1, s.root, s.B);
+  __syncthreads();
+  double residual = 0.0, ratio = 0.0;
+  const int rs = resolve_cta(s, t, &residual, &ratio);
+  if (rs) {
+    if (threadIdx.x == 0) {
+      slot_fail(slot, CBP_DEGENERATE_SCALES, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, ratio, rs);
+    }
+    return;
+  }
+  int reason = 0;
+  double value = 0.0;
+  const int st = assemble_cta(s, t, a.max_imag_energy, a.negative_weight_tol, slot->weights, &reason, &value);
+  if (threadIdx.x == 0) {
+    if (st) {
+      slot_fail(slot, st, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, value, reason);
+      return;
+    }
+    slot->scale_residual = residual;
+    // epsilon = 1e-8 * peak|K|^2 (decoder.cpp:198-199). The estimate is clamped
+    // nonnegative, so |K(u,v)| <= sum w = K(0,0) and the peak is the weight sum.
+    double sum = 0.0;
+    for (int i = 0; i < t * t; ++i) sum += slot->weights[i];
+    slot->epsilon = a.has_epsilon ? a.epsilon : 1e-8 * sum * sum;
+  }
+}
+
+cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cfg = true;
+  }
+  k_compose<<<a.batch, 256, compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s>>>(a);
+  return cudaGetLastError();
+}
+
+// stage-level single-problem kernels
+__global__ void k_complete(const double2* values, int t, int axis, double2* out) {
+  extern __shared__ double2 shc[];
+  for (int i = threadIdx.x; i < t; i += blockDim.x) shc[i] = zroot(i, t);
+  __syncthreads();
+  complete_cta(values, t, axis, shc, out);
+}
+
+cudaError_t launch_complete(const double2* values, int t, int axis, double2* out, cudaStream_t s) {
+  k_complete<<<1, 256, t * sizeof(double2), s>>>(values, t, axis, out);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_resolve(const double2* av, const double2* bv, int t, double2* lambda,
+                                                 double2* mu, double* residual, int* status, double* value) {
+  extern __shared__ double2 shc[];
+  ComposeSmem s = carve_compose(shc, t);
+  for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
+  __syncthreads();
+  complete_cta(av, t, 0, s.root, s.A);
+  complete_cta(bv, t, 1, s.root, s.B);
+  __syncthreads();
+  double res = 0.0, ratio = 0.0;
+  const int rs = resolve_cta(s, t, &res, &ratio);
+  for (int i = threadIdx.x; i < t; i += blockDim.x) lambda[i] = s.x[i], mu[i] = s.x[t + i];
+  if (threadIdx.x == 0) {
+    *residual = res;
+    *status = rs ? CBP_DEGENERATE_SCALES : 0;
+    *value = ratio;
+  }
+}
+
+cudaError_t launch_resolve(const double2* a_values, const double2* b_values, int t, double2* lambda,
+                           double2* mu, double* residual, int* status, double* value, cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cfg = true;
+  }
+  k_resolve<<<1, 256, compose_smem_bytes(t), s>>>(a_values, b_values, t, lambda, mu, residual, status, value);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_assemble(const double2* as, const double2* bs, const double2* lambda,
+                                                  const double2* mu, int t, double max_imag, double neg_tol,
+                                                  cbp_kernel_slot* slot) {
+  extern __shared__ double2 shc[];
+  ComposeSmem s = carve_compose(shc, t);
+  for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
+  for (int i = threadIdx.x; i < t * t; i += blockDim.x) s.A[i] = as[i], s.B[i] = bs[i];
+  for (int i = threadIdx.x; i < t; i += blockDim.x) s.x[i] = lambda[i], s.x[t + i] = mu[i];
+  __syncthreads();
+  int reason = 0;
+  double value = 0.0;
+  const int st = assemble_cta(s, t, max_imag, neg_tol, slot->weights, &reason, &value);
+  if (threadIdx.x == 0) {
+    slot->status = st;
+    slot->fail_reason = reason;
+    slot->fail_value = value;
+    slot->width = t;
+  }
+}
+
+cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const double2* lambda,
+                            const double2* mu, int t, double max_imag, double neg_tol, cbp_kernel_slot* slot,
+                            cudaStream_t s) {
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cfg = true;
+  }
+  k_assemble<<<1, 256, compose_smem_bytes(t), s>>>(a_spec, b_spec, lambda, mu, t, max_imag, neg_tol, slot);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- validation residual
+// Full 2-D convolution (poly.cpp:27-38) evaluated at output (i, j) from a shared tile.
+constexpr int VT_R = 16, VT_C = 64;
+
+int validate_tiles(int rows, int cols) { return ((rows + VT_R - 1) / VT_R) * ((cols + VT_C - 1) / VT_C); }
+
+// mode 0: a = conv(X, K) over the Ro x Co output, y = Y[i][j]; num += (a-y)^2, den += y^2.
+// mode 1: a = conv(X, K), y = conv(X2, K2); num += (a-y)^2, den += a^2.
+struct ConvResidArgs {
+  const float* X;
+  int xr, xc, xld;
+  size_t x_plane;
+  const float* Y;  // mode 0: compared plane; mode 1: X2
+  int yld;
+  size_t y_plane;
+  const double* K;  // weights (row-major t x t) for X
+  const double* K2;
+  size_t k_stride;  // per-frame kernel stride (slot) or 0
+  const cbp_kernel_slot* slots;  // mode 0: kernel and t from slots[frame]
+  int channels;
+  int t;
+  int mode;
+  int ro, co;  // output extent
+  double2* part;
+  int ntiles;
+};
+
+__device__ __forceinline__ double conv_at(const float* tile, int tw, const double* K, int t, int li, int lj) {
+  // out(i,j) = sum_{a,b} K[a][b] X[i-a][j-b]; tile holds X rows [i0-t+1, i0+VT_R), cols [j0-t+1, ...)
+  double acc = 0.0;
+  for (int a2 = 0; a2 < t; ++a2) {
+    const float* row = tile + (li + t - 1 - a2) * tw + (lj + t - 1);
+    const double* kr = K + a2 * t;
+    for (int b2 = 0; b2 < t; ++b2) acc = fma(kr[b2], double(row[-b2]), acc);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
+  extern __shared__ double shd[];
+  const int plane = blockIdx.y;
+  const int frame = plane / a.channels;
+  int t = a.t;
+  const double* K = a.K;
+  if (a.slots) {
+    const cbp_kernel_slot* slot = a.slots + frame;
+    if (slot->status != 0) return;
+    t = slot->width;
+    K = slot->weights;
+  }
+  // mode 0: X is the (rows-t+1) x (cols-t+1) latent, output is the rows x cols frame
+  const int xr = a.mode == 0 ? a.xr - t + 1 : a.xr;
+  const int xc = a.mode == 0 ? a.xc - t + 1 : a.xc;
+  const int ro = a.mode == 0 ? a.xr : a.ro;
+  const int co = a.mode == 0 ? a.xc : a.co;
+  const int tiles_c = (co + VT_C - 1) / VT_C;
+  const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - tr * tiles_c;
+  const int i0 = tr * VT_R, j0 = tc * VT_C;
+  if (i0 >= ro) return;
+  double* kw = shd;                      // t*t
+  double* kw2 = kw + t * t;              // t*t (mode 1)
+  const int tw = VT_C + t - 1, th = VT_R + t - 1;
+  float* tile = reinterpret_cast<float*>(kw2 + t * t);
+  float* tile2 = tile + th * tw;
+  for (int i = threadIdx.x; i < t * t; i += blockDim.x) {
+    kw[i] = K[i];
+    if (a.mode == 1) kw2[i] = a.K2[i];
+  }
+  const float* X = a.X + size_t(plane) * a.x_plane;
+  const float* Y = a.Y + size_t(plane) * a.y_plane;
+  for (int idx = threadIdx.x; idx < th * tw; idx += blockDim.x) {
+    const int li = idx / tw, lj = idx - li * tw;
+    const int gi = i0 - t + 1 + li, gj = j0 - t + 1 + lj;
+    const bool in = gi >= 0 && gi < xr && gj >= 0 && gj < xc;
+    tile[idx] = in ? X[size_t(gi) * a.xld + gj] : 0.0f;
+    if (a.mode == 1) tile2[idx] = in ? Y[size_t(gi) * a.yld + gj] : 0.0f;
+  }
+  __syncthreads();
+  double num = 0.0, den = 0.0;
+  for (int e = threadIdx.x; e < VT_R * VT_C; e += blockDim.x) {
+    const int li = e / VT_C, lj = e - li * VT_C;
+    const int gi = i0 + li, gj = j0 + lj;
+    if (gi >= ro || gj >= co) continue;
+    const double c1 = conv_at(tile, tw, kw, t, li, lj);
+    double y;
+    if (a.mode == 0) {
+      y = double(Y[size_t(gi) * a.yld + gj]);
+      den += y * y;
+    } else {
+      y = conv_at(tile2, tw, kw2, t, li, lj);
+      den += c1 * c1;
+    }
+    num += (c1 - y) * (c1 - y);
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  __shared__ double rn[8], rd[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) rn[warp] = num, rd[warp] = den;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sn = 0, sd = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) sn += rn[w], sd += rd[w];
+    a.part[size_t(plane) * a.ntiles + blockIdx.x] = make_double2(sn, sd);
+  }
+}
+
+// Per frame: fixed-order sum of the tile partials (zeros for tiles that exited early).
+__global__ void k_resid_reduce(const double2* part, int ntiles, int channels, cbp_kernel_slot* slots,
+                               double* out, int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  if (slots && slots[b].status != 0) return;
+  double num = 0.0, den = 0.0;
+  for (int c = 0; c < channels; ++c)
+    for (int i = 0; i < ntiles; ++i) {
+      const double2 v = part[(size_t(b) * channels + c) * ntiles + i];
+      num += v.x;
+      den += v.y;
+    }
+  if (!(den > 0.0)) {
+    if (slots) {
+      slot_fail(slots + b, CBP_DEGENERATE_INPUT, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_ZERO_PUBLIC);
+    } else {
+      out[b] = -1.0;
+    }
+    return;
+  }
+  const double r = sqrt(num / den);
+  if (slots)
+    slots[b].residual = r;
+  else
+    out[b] = r;
+}
+
+cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_out, double* part,
+                            int ntiles_max, cudaStream_t s) {
+  ConvResidArgs a{};
+  a.X = latent;
+  a.xld = ld_out;
+  a.x_plane = size_t(ra.rows) * ld_out;
+  a.Y = ra.pub;
+  a.yld = ra.ld;
+  a.y_plane = size_t(ra.rows) * ra.ld;
+  a.slots = ra.slots;
+  a.channels = ra.channels;
+  a.mode = 0;
+  a.part = reinterpret_cast<double2*>(part);
+  a.ntiles = ntiles_max;
+  cudaMemsetAsync(part, 0, sizeof(double2) * size_t(ntiles_max) * ra.batch * ra.channels, s);
+  // the latent extent depends on the device-side t; the kernel derives it from xr/xc
+  a.xr = ra.rows;
+  a.xc = ra.cols;
+  a.ro = ra.rows;
+  a.co = ra.cols;
+  dim3 g(ntiles_max, ra.batch * ra.channels);
+  const size_t sm = 2 * size_t(ra.t_max) * ra.t_max * sizeof(double) +
+                    2 * size_t(VT_R + ra.t_max - 1) * (VT_C + ra.t_max - 1) * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cfg = true;
+  }
+  k_conv_resid<<<g, 256, sm, s>>>(a);
+  k_resid_reduce<<<(ra.batch + 127) / 128, 128, 0, s>>>(a.part, ntiles_max, ra.channels, ra.slots, nullptr,
+                                                         ra.batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_pair(const float* pub, const float* prv, int channels, int rows, int cols, int ld,
+                                 const double* k1, const double* k2, int t, double* part, cudaStream_t s) {
+  ConvResidArgs a{};
+  a.X = pub;
+  a.xr = rows;
+  a.xc = cols;
+  a.xld = ld;
+  a.x_plane = size_t(rows) * ld;
+  a.Y = prv;
+  a.yld = ld;
+  a.y_plane = size_t(rows) * ld;
+  a.K = k2;  // lhs = pub (*) k2
+  a.K2 = k1; // rhs = prv (*) k1
+  a.channels = channels;
+  a.t = t;
+  a.mode = 1;
+  a.ro = rows + t - 1;
+  a.co = cols + t - 1;
+  const int nt = validate_tiles(a.ro, a.co);
+  a.ntiles = nt;
+  a.part = reinterpret_cast<double2*>(part);
+  cudaMemsetAsync(part, 0, sizeof(double2) * size_t(nt) * channels, s);
+  dim3 g(nt, channels);
+  const size_t sm = 2 * size_t(t) * t * sizeof(double) + 2 * size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cfg = true;
+  }
+  k_conv_resid<<<g, 256, sm, s>>>(a);
+  k_resid_reduce<<<1, 32, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------- CBP generation
+// encode_frame (encoder.cpp:96-99): conv2_full(plane, k) with the reference's
+// accumulation order (kernel column outer, kernel row inner; poly.cpp:32-36) and
+// unfused multiply/add, so the FP64 result is bit-identical to the CPU restatement.
+__global__ void __launch_bounds__(256) k_encode(const float* latent, int rows, int cols, int ld, const double* k,
+                                                int t, float* out, int ld_out) {
+  extern __shared__ double she[];
+  const int plane = blockIdx.y;
+  const int ro = rows + t - 1, co = cols + t - 1;
+  const int tiles_c = (co + VT_C - 1) / VT_C;
+  const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - tr * tiles_c;
+  const int i0 = tr * VT_R, j0 = tc * VT_C;
+  double* kw = she;
+  const int tw = VT_C + t - 1, th = VT_R + t - 1;
+  float* tile = reinterpret_cast<float*>(kw + t * t);
+  for (int i = threadIdx.x; i < t * t; i += blockDim.x) kw[i] = k[i];
+  const float* X = latent + size_t(plane) * rows * ld;
+  for (int idx = threadIdx.x; idx < th * tw; idx += blockDim.x) {
+    const int li = idx / tw, lj = idx - li * tw;
+    const int gi = i0 - t + 1 + li, gj = j0 - t + 1 + lj;
+    tile[idx] = (gi >= 0 && gi < rows && gj >= 0 && gj < cols) ? X[size_t(gi) * ld + gj] : 0.0f;
+  }
+  __syncthreads();
+  float* O = out + size_t(plane) * ro * ld_out;
+  for (int e = threadIdx.x; e < VT_R * VT_C; e += blockDim.x) {
+    const int li = e / VT_C, lj = e - li * VT_C;
+    const int gi = i0 + li, gj = j0 + lj;
+    if (gi >= ro || gj >= co) continue;
+    double acc = 0.0;
+    for (int nb = 0; nb < t; ++nb)
+      for (int ma = 0; ma < t; ++ma) {
+        const double w = kw[ma * t + nb];
+        if (w == 0.0) continue;
+        const int si = gi - ma, sj = gj - nb;
+        if (si < 0 || si >= rows || sj < 0 || sj >= cols) continue;
+        acc = __dadd_rn(acc, __dmul_rn(w, double(tile[(li + t - 1 - ma) * tw + (lj + t - 1 - nb)])));
+      }
+    O[size_t(gi) * ld_out + gj] = float(acc);
+  }
+}
+
+cudaError_t launch_encode(const float* latent, int planes, int rows, int cols, int ld, const double* k, int t,
+                          float* out, int ld_out, cudaStream_t s) {
+  const int nt = validate_tiles(rows + t - 1, cols + t - 1);
+  dim3 g(nt, planes);
+  const size_t sm = size_t(t) * t * sizeof(double) + size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cfg = true;
+  }
+  k_encode<<<g, 256, sm, s>>>(latent, rows, cols, ld, k, t, out, ld_out);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ unsigned long long smix(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void k_synth(float* out, int planes, int rows, int cols, int ld, unsigned long long seed) {
+  const size_t total = size_t(planes) * rows * cols;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t pl = i / (size_t(rows) * cols);
+    const size_t rem = i - pl * size_t(rows) * cols;
+    const size_t m = rem / cols, n = rem - m * cols;
+    const unsigned long long h = smix(seed ^ smix(i + 0x632BE59BD9B4E019ull));
+    out[(pl * rows + m) * ld + n] = float(h >> 40) * 0x1.0p-24f;
+  }
+}
+
+cudaError_t launch_synth(float* out, int planes, int rows, int cols, int ld, unsigned long long seed,
+                         cudaStream_t s) {
+  k_synth<<<148 * 8, 256, 0, s>>>(out, planes, rows, cols, ld, seed);
+  return cudaGetLastError();
+}
+
+}  // namespace cbp_dev
