@@ -228,15 +228,36 @@ int cbp_synth_frames(cbp_ctx* ctx, float* out_dev, int planes, int rows, int col
                      uint64_t seed, void* stream);
 
 /* ---- host-buffer pipeline (the e2e path) ------------------------------------
- * Decodes a run of frames held in host memory: frame j uses pub[j] (and prv[j] when
- * recover[j] != 0). Recovery frames run decode_frame; the others reuse the most
- * recent recovered kernel through spectral_deblur. H2D, compute and D2H are
- * overlapped on internal streams. latent (host) receives (rows-t+1) x (cols-t+1)
- * planes packed with pitch cols-t+1... see INTEGRATION.md. Pinned host memory gives
- * full PCIe bandwidth; pageable memory works but is slower. */
+ * Decodes a run of frames held in host memory, like the reference CLI
+ * (tools/cbp.cpp:130-207): frame j uses pub[j] and, when recover[j] != 0, prv[j]
+ * (frames packed [n_frames][channels][rows][cols]). Recovery frames run decode_frame
+ * (width_hint > 0 with cfg->trust_hint skips the width search); the others reuse the
+ * most recent recovered kernel through spectral_deblur on the device. H2D, compute
+ * and D2H overlap on internal streams. latent receives frames in the input geometry
+ * (top-left (rows-t+1) x (cols-t+1) of each plane). slots_host (may be NULL) gets
+ * one cbp_kernel_slot per recovery frame. Synchronizes before returning.
+ * Pinned host memory gives full PCIe bandwidth. recover[0] must be nonzero. */
 int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames,
-                        int channels, int rows, int cols, const int* recover,
-                        const cbp_decode_cfg* cfg, float* latent, cbp_decode_info* info);
+                        int channels, int rows, int cols, const int* recover, int width_hint,
+                        const cbp_decode_cfg* cfg, float* latent, cbp_kernel_slot* slots_host);
+
+/* ---- reference-exact input generators (host; untimed) ------------------------
+ * frame_seed / splitmix64 (rng.hpp:8-29), random_frame (synth.cpp:12-22: mt19937_64,
+ * column-major draw, returned row-major FP32), coprimality_check and
+ * generate_coprime_pair (encoder.cpp:45-81; k1/k2 t x t row-major). */
+uint64_t cbp_frame_seed(uint64_t stream_seed, int frame_index);
+uint64_t cbp_splitmix64(uint64_t x);
+int cbp_random_frame(int rows, int cols, int channels, uint64_t seed, float* out);
+double cbp_coprimality_check(const double* k1, const double* k2, int t, int trials);
+int cbp_generate_coprime_pair(int width, uint64_t seed, int max_retries, double margin_threshold,
+                              int trials, double* k1, double* k2, double* margin);
+
+/* ---- instrumentation ----------------------------------------------------------
+ * Kernels enqueued by this context so far; optional CUDA-event timing of the three
+ * deconvolution passes (A rows forward, B columns + filter, C rows inverse). */
+long long cbp_launch_count(const cbp_ctx* ctx);
+int cbp_profile(cbp_ctx* ctx, int enable);
+int cbp_profile_read(cbp_ctx* ctx, double* pass_ms, long long* planes, int* groups);
 
 #ifdef __cplusplus
 }

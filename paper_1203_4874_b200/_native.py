@@ -93,7 +93,15 @@ _SIGS = {
     "cbp_validate_pair": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, _P]),
     "cbp_encode_frames": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _I, _P]),
     "cbp_synth_frames": (_I, [_P, _P, _I, _I, _I, _I, C.c_uint64, _P]),
-    "cbp_decode_run_host": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "cbp_decode_run_host": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _P, _P]),
+    "cbp_frame_seed": (C.c_uint64, [C.c_uint64, _I]),
+    "cbp_splitmix64": (C.c_uint64, [C.c_uint64]),
+    "cbp_random_frame": (_I, [_I, _I, _I, C.c_uint64, _P]),
+    "cbp_coprimality_check": (_D, [_P, _P, _I, _I]),
+    "cbp_generate_coprime_pair": (_I, [_I, C.c_uint64, _I, _D, _I, _P, _P, _P]),
+    "cbp_launch_count": (C.c_longlong, [_P]),
+    "cbp_profile": (_I, [_P, _I]),
+    "cbp_profile_read": (_I, [_P, _P, _P, _P]),
 }
 
 

@@ -318,3 +318,122 @@ def synth_frames(planes: int, rows: int, cols: int, seed: int, device=None) -> t
     ctx.check(N.lib().cbp_synth_frames(ctx.ptr, C.c_void_p(out.data_ptr()), planes, rows, cols, cols,
                                        C.c_uint64(seed), _stream_ptr(dev)))
     return out
+
+
+# ------------------------------------------------------- CBP generation inputs
+def frame_seed(stream_seed: int, frame_index: int) -> int:
+    """rng.hpp:27-29."""
+    return int(N.lib().cbp_frame_seed(C.c_uint64(stream_seed), int(frame_index)))
+
+
+def splitmix64(x: int) -> int:
+    return int(N.lib().cbp_splitmix64(C.c_uint64(x)))
+
+
+def random_frame(rows: int, cols: int, channels: int, seed: int) -> np.ndarray:
+    """synth.cpp:12-22 (mt19937_64, column-major draw) as float32 (channels, rows, cols)."""
+    out = np.empty((channels, rows, cols), np.float32)
+    st = N.lib().cbp_random_frame(rows, cols, channels, C.c_uint64(seed), out.ctypes.data_as(C.c_void_p))
+    if st:
+        raise CbpError(st, "InvalidArgument: bad frame geometry")
+    return out
+
+
+def coprimality_check(k1, k2, trials: int = 4) -> float:
+    k1 = np.ascontiguousarray(k1, np.float64); k2 = np.ascontiguousarray(k2, np.float64)
+    return float(N.lib().cbp_coprimality_check(k1.ctypes.data_as(C.c_void_p), k2.ctypes.data_as(C.c_void_p),
+                                               k1.shape[0], trials))
+
+
+@dataclass
+class CoprimePair:
+    """kernel.hpp:19-24."""
+    k1: np.ndarray
+    k2: np.ndarray
+    coprimality_margin: float
+    seed: int
+
+
+def generate_coprime_pair(width: int, seed: int, max_retries: int = 16, margin_threshold: float = 1e-6,
+                          trials: int = 4) -> CoprimePair:
+    """encoder.cpp:66-81 (host: seeded draw + Sylvester coprimality check)."""
+    k1 = np.empty((width, width)); k2 = np.empty((width, width)); m = C.c_double()
+    st = N.lib().cbp_generate_coprime_pair(width, C.c_uint64(seed), max_retries, margin_threshold, trials,
+                                           k1.ctypes.data_as(C.c_void_p), k2.ctypes.data_as(C.c_void_p),
+                                           C.byref(m))
+    if st == 5:
+        raise CbpError(st, f"CoprimalityFailure: no coprime pair of width {width} within {max_retries} draws")
+    if st:
+        raise CbpError(st, "InvalidArgument: kernel width must be odd, within [3,63]")
+    return CoprimePair(k1, k2, m.value, seed)
+
+
+def decode_run_host(pub: torch.Tensor, prv: torch.Tensor, recover, cfg: DecodeCfg | None = None,
+                    width_hint: int = 0, out: torch.Tensor | None = None, device: int | None = None):
+    """Host-buffer run decode (the end-to-end path): pub/prv are CPU float32 tensors
+    (n, channels, rows, cols), ideally pinned; returns (latent CPU tensor in the input
+    geometry, list of KernelSlot for the recovery frames)."""
+    assert pub.device.type == "cpu" and pub.dtype == torch.float32 and pub.is_contiguous()
+    n, ch, rows, cols = pub.shape
+    rec = np.ascontiguousarray(np.asarray(recover, np.int32))
+    cfg = cfg or make_cfg()
+    if out is None:
+        out = torch.empty_like(pub, pin_memory=pub.is_pinned())
+    nrec = int((rec != 0).sum())
+    slots = (KernelSlot * max(nrec, 1))()
+    ctx = context(device)
+    ctx.check(N.lib().cbp_decode_run_host(ctx.ptr, C.c_void_p(pub.data_ptr()),
+                                          C.c_void_p(prv.data_ptr()) if prv is not None else None, n, ch, rows,
+                                          cols, rec.ctypes.data_as(C.c_void_p), int(width_hint), C.byref(cfg),
+                                          C.c_void_p(out.data_ptr()), slots))
+    return out, [slots[i] for i in range(nrec)]
+
+
+def launch_count(device: int | None = None) -> int:
+    return int(N.lib().cbp_launch_count(context(device).ptr))
+
+
+def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, out: torch.Tensor,
+                        slots: torch.Tensor, hints=None):
+    """cbp_decode_frames_async on device tensors (batch, ch, rows, cols); ``slots`` is a
+    uint8 device tensor of batch * sizeof(KernelSlot) bytes receiving the per-frame state."""
+    B, ch, rows, cols = pub.shape
+    ctx = context(pub.device.index)
+    hint_arr = None
+    if hints is not None:
+        hint_arr = (C.c_int * B)(*[int(h) for h in hints])
+    ctx.check(N.lib().cbp_decode_frames_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(prv.data_ptr()), B,
+                                              ch, rows, cols, pub.stride(-2), hint_arr, C.byref(cfg),
+                                              C.c_void_p(out.data_ptr()), out.stride(-2),
+                                              C.c_void_p(slots.data_ptr()), _stream_ptr(pub.device)))
+
+
+def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor):
+    """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device."""
+    B, ch, rows, cols = blurred.shape
+    ctx = context(blurred.device.index)
+    ctx.check(N.lib().cbp_spectral_deblur_slot(ctx.ptr, C.c_void_p(blurred.data_ptr()), B, ch, rows, cols,
+                                               blurred.stride(-2), C.c_void_p(slot_ptr),
+                                               C.c_void_p(out.data_ptr()), out.stride(-2),
+                                               _stream_ptr(blurred.device)))
+
+
+def read_slots(slots: torch.Tensor, count: int) -> list:
+    host = (KernelSlot * count)()
+    ctx = context(slots.device.index)
+    ctx.check(N.lib().cbp_read_slots(ctx.ptr, C.c_void_p(slots.data_ptr()), count, host, _stream_ptr(slots.device)))
+    return [host[i] for i in range(count)]
+
+
+def profile(enable: bool, device: int | None = None):
+    N.lib().cbp_profile(context(device).ptr, int(enable))
+
+
+def profile_read(device: int | None = None):
+    ms = (C.c_double * 3)(); planes = C.c_longlong(); groups = C.c_int()
+    ctx = context(device)
+    ctx.check(N.lib().cbp_profile_read(ctx.ptr, ms, C.byref(planes), C.byref(groups)))
+    return list(ms), planes.value, groups.value
+
+
+SLOT_BYTES = C.sizeof(KernelSlot)

@@ -143,8 +143,26 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
     a.in = in0 + size_t(p0) * in_plane_stride;
     a.out = out0 + size_t(p0) * out_plane_stride;
     a.slot = slot0 + (a.slot_per_frame ? p0 / ch : 0);
-    int st = cuda_check(ctx, launch_deblur(a, np, stream), "deconvolution launch");
-    if (st) return st;
+    cudaEvent_t* ev = nullptr;
+    if (ctx->prof) {
+      if (ctx->prof_used + 4 > int(ctx->prof_ev.size())) {
+        for (int k = 0; k < 256; ++k) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          ctx->prof_ev.push_back(e);
+        }
+      }
+      ev = &ctx->prof_ev[ctx->prof_used];
+      ctx->prof_used += 4;
+      ctx->prof_planes += np;
+      cudaEventRecord(ev[0], stream);
+    }
+    for (int pass = 0; pass < 3; ++pass) {
+      int st = cuda_check(ctx, launch_deblur_pass(a, np, pass, stream), "deconvolution launch");
+      if (st) return st;
+      ++ctx->launches;
+      if (ev) cudaEventRecord(ev[pass + 1], stream);
+    }
   }
   return 0;
 }
@@ -204,6 +222,33 @@ void cbp_destroy(cbp_ctx* ctx) {
 }
 
 const char* cbp_last_error(const cbp_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+long long cbp_launch_count(const cbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cbp_profile(cbp_ctx* ctx, int enable) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  ctx->prof = enable;
+  ctx->prof_used = 0;
+  ctx->prof_planes = 0;
+  return 0;
+}
+
+// Sums the per-pass device times recorded since cbp_profile(ctx, 1); call after the
+// work has completed. pass_ms[3] = A, B, C totals; *planes = planes processed.
+int cbp_profile_read(cbp_ctx* ctx, double* pass_ms, long long* planes, int* groups) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  pass_ms[0] = pass_ms[1] = pass_ms[2] = 0.0;
+  for (int g = 0; g + 4 <= ctx->prof_used; g += 4)
+    for (int p = 0; p < 3; ++p) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ctx->prof_ev[g + p], ctx->prof_ev[g + p + 1]) != cudaSuccess)
+        return cuda_check(ctx, cudaGetLastError(), "profile read");
+      pass_ms[p] += ms;
+    }
+  *planes = ctx->prof_planes;
+  *groups = ctx->prof_used / 4;
+  return 0;
+}
 
 // validate_kernel (kernel.cpp:7-17)
 static int check_kernel(cbp_ctx* ctx, const double* w, int t) {

@@ -19,6 +19,12 @@ struct cbp_ctx {
   cbp_kernel_slot* host_slot = nullptr;  // pinned staging
   cudaEvent_t ev[8] = {};
   int num_sms = 148;
+  // optional per-pass timing of the deconvolution (cbp_profile)
+  int prof = 0;
+  std::vector<cudaEvent_t> prof_ev;
+  int prof_used = 0;
+  long long prof_planes = 0;
+  long long launches = 0;  // kernels enqueued by this context
 };
 
 namespace cbp_host {

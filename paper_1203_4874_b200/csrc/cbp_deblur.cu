@@ -204,7 +204,7 @@ static size_t smem_cols(const DeblurArgs& a, int W) {
   return (size_t(2) * a.Gr * W + size_t(W) * CBP_MAX_WIDTH) * sizeof(float2);
 }
 
-cudaError_t launch_deblur(DeblurArgs a, int planes, cudaStream_t stream) {
+cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_rows_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -216,16 +216,20 @@ cudaError_t launch_deblur(DeblurArgs a, int planes, cudaStream_t stream) {
     configured = true;
   }
   dim3 ga((a.Mb + a.rows_per_cta - 1) / a.rows_per_cta, planes);
-  k_rows_forward<<<ga, 256, smem_rows(a), stream>>>(a);
-  const int W = a.col_width;
-  dim3 gb((a.Hc + W - 1) / W, planes);
-  switch (W) {
-    case 8: k_cols_filter<8><<<gb, 256, smem_cols(a, 8), stream>>>(a); break;
-    case 4: k_cols_filter<4><<<gb, 256, smem_cols(a, 4), stream>>>(a); break;
-    case 2: k_cols_filter<2><<<gb, 256, smem_cols(a, 2), stream>>>(a); break;
-    default: k_cols_filter<1><<<gb, 256, smem_cols(a, 1), stream>>>(a); break;
+  if (pass == 0) {
+    k_rows_forward<<<ga, 256, smem_rows(a), stream>>>(a);
+  } else if (pass == 1) {
+    const int W = a.col_width;
+    dim3 gb((a.Hc + W - 1) / W, planes);
+    switch (W) {
+      case 8: k_cols_filter<8><<<gb, 256, smem_cols(a, 8), stream>>>(a); break;
+      case 4: k_cols_filter<4><<<gb, 256, smem_cols(a, 4), stream>>>(a); break;
+      case 2: k_cols_filter<2><<<gb, 256, smem_cols(a, 2), stream>>>(a); break;
+      default: k_cols_filter<1><<<gb, 256, smem_cols(a, 1), stream>>>(a); break;
+    }
+  } else {
+    k_rows_inverse<<<ga, 256, smem_rows(a), stream>>>(a);
   }
-  k_rows_inverse<<<ga, 256, smem_rows(a), stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -31,6 +31,7 @@ struct DeblurArgs {
 };
 
 int deblur_col_width(int Gr, int t_max);
-cudaError_t launch_deblur(DeblurArgs a, int planes, cudaStream_t stream);
+// pass 0: rows forward (A), 1: columns + filter (B), 2: rows inverse + crop (C)
+cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaStream_t stream);
 
 }  // namespace cbp_dev

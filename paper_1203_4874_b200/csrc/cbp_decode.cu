@@ -110,7 +110,6 @@ struct RecoverPlan {
   RecoverArgs a;
   double* vpart = nullptr;
   int vtiles = 0;
-  int* hints_dev = nullptr;
 };
 
 int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* prv, int batch, int channels,
@@ -155,7 +154,6 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   const size_t o_scratch = take(B * 2 * T * (L + T) * sizeof(double2));
   const size_t o_ratios = take(B * 2 * std::max(a.nsizes, 1) * sizeof(double));
   const size_t o_flags = take(B * sizeof(int));
-  const size_t o_hints = take(B * sizeof(int));
   const size_t o_vpart = take(B * channels * std::max(P.vtiles, 1) * sizeof(double2) + 64);
   char* base = static_cast<char*>(workspace(ctx, WS_MISC, off));
   if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
@@ -167,7 +165,6 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.scratch = reinterpret_cast<double2*>(base + o_scratch);
   a.ratios = reinterpret_cast<double*>(base + o_ratios);
   a.flags = reinterpret_cast<int*>(base + o_flags);
-  P.hints_dev = reinterpret_cast<int*>(base + o_hints);
   P.vpart = reinterpret_cast<double*>(base + o_vpart);
   return 0;
 }
@@ -234,17 +231,16 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
     return st;
   RecoverArgs& a = P.a;
   a.slots = slots;
-  int* hpin = pinned<int>(ctx, size_t(batch));
-  if (!hpin) return set_error(ctx, CBP_CUDA_ERROR, "pinned allocation failed");
-  for (int b = 0; b < batch; ++b) hpin[b] = hints ? hints[b] : 0;
-  cudaMemcpyAsync(P.hints_dev, hpin, sizeof(int) * batch, cudaMemcpyHostToDevice, s);
   if (record_events) cudaEventRecord(ctx->ev[0], s);
-  cudaError_t e = launch_init_slots(a, P.hints_dev, s);
+  cudaError_t e = launch_init_slots(a, hints, s);
+  ctx->launches += (batch + HintChunk::kMax - 1) / HintChunk::kMax;
   if (e == cudaSuccess && need_est) e = launch_fold(a, 1, s);  // DC slices (decoder.cpp:58-64)
   if (e == cudaSuccess && need_est) e = launch_width(a, s);
+  if (need_est) ctx->launches += 5;
   if (record_events) cudaEventRecord(ctx->ev[1], s);
   // the solve sizes shared memory for min(t_max, 31); wider kernels are flagged in k_solve
   if (e == cudaSuccess) e = launch_fold(a, 0, s);  // axis_roots_dft x4 (decoder.cpp:323-326)
+  ctx->launches += 5;  // fold x3, solve, compose
   if (record_events) cudaEventRecord(ctx->ev[2], s);
   if (e == cudaSuccess) e = launch_solve(a, s);
   if (record_events) cudaEventRecord(ctx->ev[3], s);
@@ -265,6 +261,7 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
     a.pub = pub;
     if ((st = cuda_check(ctx, launch_validate(a, latent, ld_out, P.vpart, P.vtiles, s), "validation launch")))
       return st;
+    ctx->launches += 2;
   }
   (void)t_solve;
   return 0;
@@ -415,10 +412,8 @@ int cbp_sample_cofactors(cbp_ctx* ctx, const float* pub_dev, const float* prv_de
     return st;
   cbp_kernel_slot* slots = ws<cbp_kernel_slot>(ctx, WS_SLOTS, 64);
   P.a.slots = slots;
-  int* hpin = pinned<int>(ctx, 1);
-  *hpin = width;
-  cudaMemcpyAsync(P.hints_dev, hpin, sizeof(int), cudaMemcpyHostToDevice, s);
-  cudaError_t e = launch_init_slots(P.a, P.hints_dev, s);
+  const int hint = width;
+  cudaError_t e = launch_init_slots(P.a, &hint, s);
   if (e == cudaSuccess) e = launch_fold(P.a, 0, s);
   if (e == cudaSuccess) e = launch_solve(P.a, s);
   if ((st = cuda_check(ctx, e, "solve launch"))) return st;

@@ -10,9 +10,10 @@ namespace cbp_dev {
 constexpr int kSolveMaxWidth = 31;  // 2t x 2t complex Gram + eigenvectors in shared memory
 
 // ----------------------------------------------------------------- slots
-__global__ void k_init_slots(RecoverArgs a, const int* hints) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= a.batch) return;
+__global__ void k_init_slots(RecoverArgs a, HintChunk hc) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= hc.count) return;
+  const int b = hc.first + j;
   cbp_kernel_slot* s = a.slots + b;
   s->status = 0;
   s->fail_stage = 0;
@@ -25,13 +26,20 @@ __global__ void k_init_slots(RecoverArgs a, const int* hints) {
   s->residual = 0.0;
   s->scale_residual = 0.0;
   s->epsilon = 0.0;
-  const int h = hints ? hints[b] : 0;
+  const int h = hc.hint[j];
   s->width = (a.trust_hint && h > 0) ? h : 0;  // decoder.cpp:302-306
   a.flags[b] = 0;
 }
 
-cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_dev, cudaStream_t s) {
-  k_init_slots<<<(a.batch + 127) / 128, 128, 0, s>>>(a, hints_dev);
+cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaStream_t s) {
+  // hints travel as kernel parameters: no host staging buffer to race with
+  for (int first = 0; first < a.batch; first += HintChunk::kMax) {
+    HintChunk hc;
+    hc.first = first;
+    hc.count = a.batch - first < HintChunk::kMax ? a.batch - first : HintChunk::kMax;
+    for (int j = 0; j < hc.count; ++j) hc.hint[j] = hints_host ? hints_host[first + j] : 0;
+    k_init_slots<<<(hc.count + 127) / 128, 128, 0, s>>>(a, hc);
+  }
   return cudaGetLastError();
 }
 

@@ -38,7 +38,12 @@ __host__ __device__ inline size_t slice_offset(const RecoverArgs& a, int b, int 
   return ((size_t(b) * 2 + axis) * 2 + q) * size_t(a.t_max) * a.lmax + size_t(i) * a.lmax;
 }
 
-cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_dev, cudaStream_t s);
+struct HintChunk {
+  static constexpr int kMax = 1024;
+  int first, count;
+  int hint[kMax];
+};
+cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaStream_t s);
 // t_fixed > 0 folds with that t (1 = DC sums); otherwise with slots[b].width.
 cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s);
 cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s);
