@@ -135,14 +135,30 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   a.x_plane = size_t(a.Mb) * a.xp;
   a.in_plane = in_plane_stride;
   a.out_plane = out_plane_stride;
+  // Wiener filter table(s) H[u][v] for the kernel slot(s) of this batch
+  const int nslots = a.slot_per_frame ? std::max(frames, 1) : 1;
+  a.s_frame = size_t(a.Hc) * CBP_MAX_WIDTH;
+  a.h_frame = size_t(a.Gr) * a.xp;
+  a.S = static_cast<double2*>(workspace(ctx, WS_RED + 1, sizeof(double2) * a.s_frame * nslots));
+  a.H = static_cast<float2*>(workspace(ctx, WS_RED + 2, sizeof(float2) * a.h_frame * nslots));
+  if (!a.S || !a.H) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  if (int st = cuda_check(ctx, launch_wiener_tables(a, nslots, stream), "filter table launch")) return st;
+  ctx->launches += 2;
   const float* in0 = a.in;
   float* out0 = a.out;
   const cbp_kernel_slot* slot0 = a.slot;
+  double2* const S0 = a.S;
+  float2* const H0 = a.H;
   for (int p0 = 0; p0 < planes; p0 += group_planes) {
     const int np = std::min(group_planes, planes - p0);
     a.in = in0 + size_t(p0) * in_plane_stride;
     a.out = out0 + size_t(p0) * out_plane_stride;
     a.slot = slot0 + (a.slot_per_frame ? p0 / ch : 0);
+    a.S = S0 + (a.slot_per_frame ? size_t(p0 / ch) * a.s_frame : 0);
+    a.H = H0 + (a.slot_per_frame ? size_t(p0 / ch) * a.h_frame : 0);
+    a.in_vec2 = (reinterpret_cast<uintptr_t>(a.in) % 8 == 0) && a.in_ld % 2 == 0 && in_plane_stride % 2 == 0;
+    a.out_vec2 = (reinterpret_cast<uintptr_t>(a.out) % 8 == 0) && a.out_ld % 2 == 0 && out_plane_stride % 2 == 0;
+    a.in_vec4 = (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) && a.in_ld % 4 == 0 && in_plane_stride % 4 == 0;
     cudaEvent_t* ev = nullptr;
     if (ctx->prof) {
       if (ctx->prof_used + 4 > int(ctx->prof_ev.size())) {

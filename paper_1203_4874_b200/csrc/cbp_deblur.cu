@@ -11,6 +11,8 @@
 //   C  row c2r, 1/(Gr*Gc) folded into the filter, crop                 L2 X -> HBM out
 // The row-major grid halves the column axis where column-major FFTW halves rows
 // (fft.cpp:45); the arithmetic is the same transform.
+#include <cstdlib>
+
 #include "cbp_deblur.cuh"
 #include "cbp_fft.cuh"
 
@@ -205,6 +207,8 @@ static size_t smem_cols(const DeblurArgs& a, int W) {
 }
 
 cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaStream_t stream) {
+  static const bool force_generic = getenv("CBP_GENERIC_FFT") != nullptr;
+  if (!force_generic && launch_deblur_pass_ct(a, planes, pass, stream)) return cudaGetLastError();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_rows_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -19,6 +19,9 @@ struct DeblurArgs {
   int Gr, Gc, Hc;   // grid and half-spectrum width Gc/2+1
   int even;         // Gc even: half-length complex row transform
   int rows_per_cta; // pass A/C rows per CTA
+  int in_vec2;      // input rows 8-byte aligned (float2 loads)
+  int out_vec2;     // output rows 8-byte aligned (float2 stores)
+  int in_vec4;      // input rows 16-byte aligned (16-byte cp.async)
   int col_width;    // pass B columns per CTA
   const cbp_kernel_slot* slot;
   int slot_per_frame;  // 1: slot[p / channels]; 0: slot[0] for every plane
@@ -28,10 +31,19 @@ struct DeblurArgs {
   const float2* tw_row;   // exp(-2 pi i k / plan_row.n)
   const float2* tw_post;  // exp(-2 pi i k / Gc), k <= Gc/2
   const float2* tw_col;   // exp(-2 pi i k / Gr)
+  double2* S;             // per-slot column kernel transforms S[v][a] (k_wiener_s)
+  size_t s_frame;         // S stride per slot
+  float2* H;              // per-slot Wiener filter H[u][v] (pitch xp), scaled by 1/(Gr*Gc)
+  size_t h_frame;         // H stride per slot
 };
 
 int deblur_col_width(int Gr, int t_max);
 // pass 0: rows forward (A), 1: columns + filter (B), 2: rows inverse + crop (C)
 cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaStream_t stream);
+// compile-time-planned passes (cbp_deblur_ct.cu); false if the grid has no specialisation
+bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream_t stream);
+bool deblur_has_ct(int Gr, int Gc, int pass);
+// Wiener filter tables of `frames` slots: S (column transforms) then H (cbp_deblur_ct.cu)
+cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s);
 
 }  // namespace cbp_dev

@@ -1,0 +1,383 @@
+// Compile-time-planned deconvolution passes for the production grids (1080p, 4K,
+// 640x480, 256x256 configs of BASELINE.json). Same math as cbp_deblur.cu (reference
+// decoder.cpp:187-214); grids without a specialisation use the runtime-planned kernels.
+//
+// Each pass is a persistent kernel: a CTA walks tiles (plane x row group, or plane x
+// column strip) with stride gridDim.x and keeps two tile buffers in shared memory;
+// the next tile's global->shared copies (cp.async, zero-filled outside the frame) are
+// in flight while the current tile is transformed, so HBM/L2 latency overlaps the FFT.
+#include "cbp_deblur.cuh"
+#include "cbp_fft_ct.cuh"
+
+namespace cbp_dev {
+
+constexpr int kNT = 256;
+
+template <int L_, int RPC_, class Rs>
+struct RowPlan {
+  static constexpr int L = L_;
+  static constexpr int RPC = RPC_;
+  using R = Rs;
+};
+template <int G_, int W_, class Rs>
+struct ColPlan {
+  static constexpr int G = G_;
+  static constexpr int W = W_;
+  using R = Rs;
+};
+
+__device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a, int p) {
+  return a.slot + (a.slot_per_frame ? p / a.channels : 0);
+}
+
+// ------------------------------------------------------------ pass A (rows r2c)
+// Row s of a tile holds z[m] = (x[2m], x[2m+1]); forward DIF leaves Z[k] in slot pos(k).
+template <class P>
+__global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int planes) {
+  constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
+  using R = typename P::R;
+  using FFT = FftIP<L, RPC, L, 1, kNT, false>;
+  extern __shared__ __align__(16) float2 sm[];
+  short* pos = reinterpret_cast<short*>(sm + 2 * TILE);  // slot of Z[k] after the DIF
+  for (int i = threadIdx.x; i < L; i += kNT) pos[i] = short(Pos<R>::get(i));
+  const int groups = (a.Mb + RPC - 1) / RPC;
+  const int total = planes * groups;
+  const bool v16 = a.in_vec4 && (L % 2 == 0);
+  auto issue = [&](int tile, float2* dst) {
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    const float* src = a.in + size_t(p) * a.in_plane + size_t(r0) * a.in_ld;
+#pragma unroll
+    for (int s = 0; s < RPC; ++s) {
+      const bool ok = r0 + s < a.Mb;
+      const float* row = src + size_t(s) * a.in_ld;
+      if (v16) {
+        for (int c = threadIdx.x; c < L / 2; c += kNT) {
+          const int bytes = ok ? min(max((a.Nb - 4 * c) * 4, 0), 16) : 0;
+          cp_async16(dst + s * L + 2 * c, bytes ? row + 4 * c : a.in, bytes);
+        }
+      } else {
+        for (int m = threadIdx.x; m < L; m += kNT) {
+          const int bytes = ok ? min(max((a.Nb - 2 * m) * 4, 0), 8) : 0;
+          cp_async8(dst + s * L + m, bytes ? row + 2 * m : a.in, bytes);
+        }
+      }
+    }
+  };
+  int tile = blockIdx.x;
+  if (tile < total) issue(tile, sm);
+  cp_async_commit();
+  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+    float2* cur = sm + (it & 1) * TILE;
+    const int next = tile + gridDim.x;
+    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    FFT::template dif<false>(cur, a.tw_row, R{});
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    float2* X = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
+#pragma unroll
+    for (int s = 0; s < RPC; ++s) {
+      if (r0 + s >= a.Mb) break;
+      const float2* z = cur + s * L;
+      for (int k = threadIdx.x; k <= L; k += kNT) {
+        const float2 zk = z[pos[k == L ? 0 : k]];
+        const float2 zc = cconj(z[pos[k == 0 ? 0 : L - k]]);
+        const float2 e = cscale(cadd(zk, zc), 0.5f);
+        const float2 d = csub(zk, zc);
+        const float2 o = make_float2(0.5f * d.y, -0.5f * d.x);  // -i/2 * d
+        X[size_t(s) * a.xp + k] = cadd(e, cmul(__ldg(&a.tw_post[k]), o));
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ----------------------------------------------- pass B (columns + Wiener filter)
+// Forward DIF leaves spectrum row u in slot pos(u); the filter H (precomputed per kernel
+// slot by k_wiener_h) is applied there; inverse DIT returns natural rows.
+template <class P>
+__global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes) {
+  constexpr int G = P::G, W = P::W, TILE = G * W;
+  using R = typename P::R;
+  using FFT = FftIP<G, W, 1, W, kNT, true>;
+  extern __shared__ __align__(16) float2 sm[];
+  short* freq = reinterpret_cast<short*>(sm + 2 * TILE);  // slot -> spectrum row after the DIF
+  for (int i = threadIdx.x; i < G; i += kNT) freq[i] = short(InvPos<R>::get(i));
+  const int strips = (a.Hc + W - 1) / W;
+  const int total = planes * strips;
+  auto issue = [&](int tile, float2* dst) {
+    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const float2* X = a.X + size_t(p) * a.x_plane + v0;
+    if (W % 2 == 0) {  // 16-byte copies of column pairs (xp and v0 even)
+      for (int idx = threadIdx.x; idx < TILE / 2; idx += kNT) {
+        const int u = idx / (W / 2), c = idx - u * (W / 2);
+        const int bytes = u < a.Mb ? min(max((a.Hc - v0 - 2 * c) * 8, 0), 16) : 0;
+        cp_async16(dst + u * W + 2 * c, bytes ? X + size_t(u) * a.xp + 2 * c : a.X, bytes);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < TILE; idx += kNT) {
+        const int u = idx / W, s = idx - u * W;
+        const int bytes = (u < a.Mb && v0 + s < a.Hc) ? 8 : 0;
+        cp_async8(dst + idx, bytes ? X + size_t(u) * a.xp + s : a.X, bytes);
+      }
+    }
+  };
+  int tile = blockIdx.x;
+  if (tile < total) issue(tile, sm);
+  cp_async_commit();
+  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+    float2* cur = sm + (it & 1) * TILE;
+    const int next = tile + gridDim.x;
+    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    cp_async_commit();
+    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const int f = a.slot_per_frame ? p / a.channels : 0;
+    const cbp_kernel_slot* slot = a.slot + f;
+    const int status = slot->status;
+    cp_async_wait<1>();
+    __syncthreads();
+    if (status == 0) {  // uniform over the CTA
+      const int t = slot->width;
+      FFT::template dif<false>(cur, a.tw_col, R{});
+      const float2* Ht = a.H + size_t(f) * a.h_frame + v0;
+      for (int idx = threadIdx.x; idx < TILE; idx += kNT) {
+        const int sp = idx / W, s = idx - sp * W;
+        const int u = freq[sp];
+        cur[idx] = cmul(cur[idx], __ldg(Ht + size_t(u) * a.xp + s));
+      }
+      __syncthreads();
+      FFT::template dit<true>(cur, a.tw_col, R{});
+      const int M = a.Mb - t + 1;
+      float2* X = a.X + size_t(p) * a.x_plane + v0;
+      const int wv = min(W, a.Hc - v0);
+      for (int idx = threadIdx.x; idx < M * W; idx += kNT) {
+        const int u = idx / W, s = idx - u * W;
+        if (s < wv) X[size_t(u) * a.xp + s] = cur[idx];
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// ------------------------------------------------- pass C (rows c2r + crop)
+template <class P>
+__global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int planes) {
+  constexpr int L = P::L, RPC = P::RPC, H = L + 1, HP = (L + 2) & ~1, TILE = RPC * HP;
+  using R = typename P::R;
+  using FFT = FftIP<L, RPC, HP, 1, kNT, false>;
+  extern __shared__ __align__(16) float2 sm[];
+  short* pos = reinterpret_cast<short*>(sm + 2 * TILE);  // slot of z[n] after the DIF
+  for (int i = threadIdx.x; i < L; i += kNT) pos[i] = short(Pos<R>::get(i));
+  const int groups = (a.Mb + RPC - 1) / RPC;
+  const int total = planes * groups;
+  auto rows_of = [&](int p) {
+    const cbp_kernel_slot* sl = plane_slot(a, p);
+    return sl->status == 0 ? a.Mb - sl->width + 1 : 0;  // failed frames: nothing to write
+  };
+  auto issue = [&](int tile, float2* dst) {
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    const int M = rows_of(p);
+    const float2* Y = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
+#pragma unroll
+    for (int s = 0; s < RPC; ++s) {
+      const bool ok = r0 + s < M;
+      for (int c = threadIdx.x; c < HP / 2; c += kNT) {
+        const int bytes = ok ? min(max((H - 2 * c) * 8, 0), 16) : 0;
+        cp_async16(dst + s * HP + 2 * c, bytes ? Y + size_t(s) * a.xp + 2 * c : a.X, bytes);
+      }
+    }
+  };
+  int tile = blockIdx.x;
+  if (tile < total) issue(tile, sm);
+  cp_async_commit();
+  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+    float2* cur = sm + (it & 1) * TILE;
+    const int next = tile + gridDim.x;
+    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    const int M = rows_of(p);
+    const int nrows = min(RPC, M - r0);
+    if (nrows > 0) {
+      // inverse split in place, one thread per pair (k, L-k) (fft.cpp:257-270 c2r)
+      constexpr int NP = L / 2 + 1;
+#pragma unroll
+      for (int s = 0; s < RPC; ++s) {
+        float2* row = cur + s * HP;
+        for (int k = threadIdx.x; k < NP; k += kNT) {
+          const float2 A = row[k], B = row[L - k];
+          const float2 e1 = cadd(A, cconj(B));
+          const float2 o1 = cmul(csub(A, cconj(B)), cconj(__ldg(&a.tw_post[k])));
+          const float2 e2 = cadd(B, cconj(A));
+          const float2 o2 = cmul(csub(B, cconj(A)), cconj(__ldg(&a.tw_post[L - k])));
+          row[k] = make_float2(e1.x - o1.y, e1.y + o1.x);
+          if (k != 0 && 2 * k != L) row[L - k] = make_float2(e2.x - o2.y, e2.y + o2.x);
+        }
+      }
+      __syncthreads();
+      FFT::template dif<true>(cur, a.tw_row, R{});  // natural -> slot order
+      const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
+      float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
+      if (a.out_vec2 && N % 2 == 0) {
+        const int h = N / 2;
+        for (int s = 0; s < nrows; ++s)
+          for (int n = threadIdx.x; n < h; n += kNT)
+            __stcs(reinterpret_cast<float2*>(dst + size_t(s) * a.out_ld) + n, cur[s * HP + pos[n]]);
+      } else {
+        for (int s = 0; s < nrows; ++s)
+          for (int n = threadIdx.x; n < N; n += kNT) {
+            const float2 z = cur[s * HP + pos[n >> 1]];
+            __stcs(dst + size_t(s) * a.out_ld + n, (n & 1) ? z.y : z.x);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+// --------------------------------------------- Wiener filter tables (per slot)
+// S[f][v][a] = sum_b w[a][b] exp(-2 pi i v b / Gc)  (FP64)
+__global__ void k_wiener_s(DeblurArgs a, int frames) {
+  const int f = blockIdx.y;
+  const cbp_kernel_slot* slot = a.slot + f;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= a.Hc * t) return;
+  const int v = idx / t, ai = idx - v * t;
+  double re = 0.0, im = 0.0;
+  for (int bj = 0; bj < t; ++bj) {
+    const double w = slot->weights[ai * t + bj];
+    double sn, cs;
+    sincospi(-2.0 * double((long(v) * bj) % a.Gc) / double(a.Gc), &sn, &cs);
+    re = fma(w, cs, re);
+    im = fma(w, sn, im);
+  }
+  a.S[size_t(f) * a.s_frame + idx] = make_double2(re, im);
+}
+
+// H[f][u][v] = conj(K)/(|K|^2 + eps) / (Gr*Gc), K(u,v) = sum_a S[v][a] exp(-2 pi i u a / Gr)
+// in FP64 (decoder.cpp:209-211, fft.cpp:268); grid (ceil(Hc/32), ceil(Gr/8), frames).
+__global__ void __launch_bounds__(256) k_wiener_h(DeblurArgs a, int frames) {
+  __shared__ double2 Ss[32 * CBP_MAX_WIDTH];
+  const int f = blockIdx.z;
+  const cbp_kernel_slot* slot = a.slot + f;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  const int v0 = blockIdx.x * 32;
+  const double2* S = a.S + size_t(f) * a.s_frame;
+  for (int i = threadIdx.x; i < 32 * t; i += blockDim.x) {
+    const int vv = i / t, ai = i - vv * t;
+    Ss[i] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int vv = threadIdx.x & 31, v = v0 + vv;
+  const int u = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (v >= a.Hc || u >= a.Gr) return;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int ai = 0; ai < t; ++ai) {
+    const double2 w = zroot(long(u) * ai, a.Gr);
+    acc = zadd(acc, zmul(Ss[vv * t + ai], w));
+  }
+  const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
+  const double den = (acc.x * acc.x + acc.y * acc.y + slot->epsilon);
+  a.H[size_t(f) * a.h_frame + size_t(u) * a.xp + v] =
+      make_float2(float(acc.x * sc / den), float(-acc.y * sc / den));
+}
+
+cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s) {
+  dim3 g1((a.Hc * CBP_MAX_WIDTH + 255) / 256, frames);
+  k_wiener_s<<<g1, 256, 0, s>>>(a, frames);
+  dim3 g2((a.Hc + 31) / 32, (a.Gr + 7) / 8, frames);
+  k_wiener_h<<<g2, 256, 0, s>>>(a, frames);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------- dispatch
+template <class K>
+int persistent_grid(K kernel, size_t smem, int total, int sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kNT, smem);
+  per_sm = per_sm < 1 ? 1 : per_sm;
+  const int g = sms * per_sm;
+  return total < g ? total : g;
+}
+
+template <class P>
+void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
+  const size_t smA = 2 * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
+  const size_t smC = 2 * size_t(P::RPC) * ((P::L + 2) & ~1) * sizeof(float2) + P::L * sizeof(short);
+  static int gA = 0, gC = 0, sms = 0;
+  if (!sms) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(k_rows_forward_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
+    cudaFuncSetAttribute(k_rows_inverse_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
+    gA = persistent_grid(k_rows_forward_ct<P>, smA, 1 << 30, sms);
+    gC = persistent_grid(k_rows_inverse_ct<P>, smC, 1 << 30, sms);
+  }
+  const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
+  if (inverse)
+    k_rows_inverse_ct<P><<<total < gC ? total : gC, kNT, smC, s>>>(a, planes);
+  else
+    k_rows_forward_ct<P><<<total < gA ? total : gA, kNT, smA, s>>>(a, planes);
+}
+
+template <class P>
+void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
+  const size_t sm = 2 * size_t(P::G) * P::W * sizeof(float2) + P::G * sizeof(short);
+  static int g = 0, sms = 0;
+  if (!sms) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    g = persistent_grid(k_cols_filter_ct<P>, sm, 1 << 30, sms);
+  }
+  const int total = planes * ((a.Hc + P::W - 1) / P::W);
+  k_cols_filter_ct<P><<<total < g ? total : g, kNT, sm, s>>>(a, planes);
+}
+
+using Row972 = RowPlan<972, 4, Radices<4, 9, 9, 3>>;     // 1080p: Gc = 1944
+using Row1944 = RowPlan<1944, 2, Radices<8, 9, 9, 3>>;   // 4K: Gc = 3888
+using Row324 = RowPlan<324, 8, Radices<4, 9, 9>>;        // 640x480: Gc = 648
+using Row135 = RowPlan<135, 8, Radices<9, 3, 5>>;        // 256x256: Gc = 270
+using Col1120 = ColPlan<1120, 4, Radices<8, 4, 5, 7>>;   // 1080p: Gr = 1120
+using Col2187 = ColPlan<2187, 2, Radices<9, 9, 9, 3>>;   // 4K: Gr = 2187
+using Col490 = ColPlan<490, 8, Radices<2, 5, 7, 7>>;     // 640x480: Gr = 490
+using Col270 = ColPlan<270, 8, Radices<2, 9, 3, 5>>;     // 256x256: Gr = 270
+
+bool deblur_has_ct(int Gr, int Gc, int pass) {
+  if (pass == 1) return Gr == 1120 || Gr == 2187 || Gr == 490 || Gr == 270;
+  if (Gc % 2) return false;
+  const int L = Gc / 2;
+  return L == 972 || L == 1944 || L == 324 || L == 135;
+}
+
+bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream_t s) {
+  if (!deblur_has_ct(a.Gr, a.Gc, pass)) return false;
+  if (pass == 0 && !a.in_vec2) return false;  // cp.async 8-byte copies need aligned rows
+  if (pass == 1) {
+    if (!a.H) return false;
+    switch (a.Gr) {
+      case 1120: launch_cols<Col1120>(a, planes, s); return true;
+      case 2187: launch_cols<Col2187>(a, planes, s); return true;
+      case 490: launch_cols<Col490>(a, planes, s); return true;
+      case 270: launch_cols<Col270>(a, planes, s); return true;
+    }
+    return false;
+  }
+  const bool inv = pass == 2;
+  switch (a.Gc / 2) {
+    case 972: launch_rows<Row972>(a, planes, inv, s); return true;
+    case 1944: launch_rows<Row1944>(a, planes, inv, s); return true;
+    case 324: launch_rows<Row324>(a, planes, inv, s); return true;
+    case 135: launch_rows<Row135>(a, planes, inv, s); return true;
+  }
+  return false;
+}
+
+}  // namespace cbp_dev

@@ -1,0 +1,178 @@
+// Compile-time-planned in-place shared-memory FFT for the production grid sizes.
+//
+// Mixed-radix Cooley-Tukey with radices (R_1, ..., R_m), N = prod R_s, P_s = R_1...R_s.
+// Stage s combines R_s sub-transforms of length P_{s-1}: butterfly (block, k) touches
+// positions block*P_s + k + i*P_{s-1}, i < R_s, and writes its outputs back to the same
+// positions, so a stage needs one barrier and only one butterfly in registers.
+//  - DIT (twiddle, then DFT_R; s = 1..m) maps digit-reversed input to natural output.
+//  - DIF (DFT_R, then twiddle; s = m..1) maps natural input to digit-reversed output.
+// Digit reversal: pos(n) = (n mod R_m) * N/R_m + pos'(n / R_m) (pos' over R_1..R_{m-1}).
+// Element n of sequence q lives at buf[q*SP + pos*ES]. Twiddles W_{P_s}^{ik} are read
+// (through L1) from a global table exp(-2 pi i j / N).
+#pragma once
+
+#include "cbp_fft.cuh"
+
+namespace cbp_dev {
+
+template <int... Rs>
+struct Radices {};
+
+template <int... Rs>
+struct RadixProduct;
+template <>
+struct RadixProduct<> {
+  static constexpr int value = 1;
+};
+template <int R, int... Rs>
+struct RadixProduct<R, Rs...> {
+  static constexpr int value = R * RadixProduct<Rs...>::value;
+};
+
+// ---------------------------------------------------------------- cp.async
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+// 16-byte copy that bypasses L1 (.cg); src_bytes < 16 zero-fills the tail
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// pos over (R_1..R_m): peel R_m (the last template argument) by recursion on the list.
+template <int... Rs>
+struct LastRadix;
+template <int R>
+struct LastRadix<R> {
+  static constexpr int value = R;
+};
+template <int R, int... Rest>
+struct LastRadix<R, Rest...> {
+  static constexpr int value = LastRadix<Rest...>::value;
+};
+
+template <class Done, class Todo>
+struct DropLast;
+template <int... Ds, int R>
+struct DropLast<Radices<Ds...>, Radices<R>> {
+  using type = Radices<Ds...>;
+};
+template <int... Ds, int R, int R2, int... Rest>
+struct DropLast<Radices<Ds...>, Radices<R, R2, Rest...>> {
+  using type = typename DropLast<Radices<Ds..., R>, Radices<R2, Rest...>>::type;
+};
+
+template <class Rs>
+struct Pos;
+template <>
+struct Pos<Radices<>> {
+  __device__ __forceinline__ static int get(int) { return 0; }
+};
+template <int R0, int... Rest>
+struct Pos<Radices<R0, Rest...>> {
+  static constexpr int Rm = LastRadix<R0, Rest...>::value;
+  static constexpr int N = RadixProduct<R0, Rest...>::value;
+  using Head = typename DropLast<Radices<>, Radices<R0, Rest...>>::type;
+  __device__ __forceinline__ static int get(int n) { return (n % Rm) * (N / Rm) + Pos<Head>::get(n / Rm); }
+};
+
+// inverse of Pos<R_1..R_m>: the digit reversal for the reversed radix list
+template <class Done, class Todo>
+struct Reverse;
+template <int... Ds>
+struct Reverse<Radices<Ds...>, Radices<>> {
+  using type = Radices<Ds...>;
+};
+template <int... Ds, int R, int... Rest>
+struct Reverse<Radices<Ds...>, Radices<R, Rest...>> {
+  using type = typename Reverse<Radices<R, Ds...>, Radices<Rest...>>::type;
+};
+template <class Rs>
+using InvPos = Pos<typename Reverse<Radices<>, Rs>::type>;
+
+// NSEQ sequences of length N; element position p of sequence q at buf[q*SP + p*ES].
+// SEQ_FAST: consecutive threads walk sequences first (column strips).
+template <int N, int NSEQ, int SP, int ES, int NT, bool SEQ_FAST>
+struct FftIP {
+  static_assert(NT % NSEQ == 0, "threads must split evenly over sequences");
+  static constexpr int TPS = NT / NSEQ;
+
+  // DIT = false: DIF stage (DFT, then twiddle); true: DIT stage (twiddle, then DFT).
+  template <bool DIT, bool INV, int R, int PP>
+  __device__ __forceinline__ static void stage(float2* buf, const float2* tw) {
+    constexpr int PS = PP * R;
+    constexpr int NB = N / R;
+    constexpr int STEP = N / PS;
+    constexpr int BPT = (NB + TPS - 1) / TPS;
+    const int q = SEQ_FAST ? int(threadIdx.x % NSEQ) : int(threadIdx.x / TPS);
+    const int tl = SEQ_FAST ? int(threadIdx.x / NSEQ) : int(threadIdx.x % TPS);
+    float2* sb = buf + q * SP;
+#pragma unroll 2
+    for (int m = 0; m < BPT; ++m) {
+      const int b = tl + m * TPS;
+      if (NB % TPS == 0 || b < NB) {
+        const int k = b % PP;
+        const int base = (b - k) * R + k;  // block * PS + k
+        float2 v[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
+        if (DIT && PP > 1 && k != 0) {
+#pragma unroll
+          for (int i = 1; i < R; ++i) {
+            float2 w = __ldg(&tw[i * k * STEP]);
+            if (INV) w.y = -w.y;
+            v[i] = cmul(v[i], w);
+          }
+        }
+        dft<R, INV>(v);
+        if (!DIT && PP > 1 && k != 0) {
+#pragma unroll
+          for (int i = 1; i < R; ++i) {
+            float2 w = __ldg(&tw[i * k * STEP]);
+            if (INV) w.y = -w.y;
+            v[i] = cmul(v[i], w);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
+      }
+    }
+    __syncthreads();
+  }
+
+  template <bool INV, int PP>
+  __device__ __forceinline__ static void dit_impl(float2*, const float2*, Radices<>) {}
+  template <bool INV, int PP, int R, int... Rest>
+  __device__ __forceinline__ static void dit_impl(float2* buf, const float2* tw, Radices<R, Rest...>) {
+    stage<true, INV, R, PP>(buf, tw);
+    dit_impl<INV, PP * R>(buf, tw, Radices<Rest...>{});
+  }
+  template <bool INV, int PP>
+  __device__ __forceinline__ static void dif_impl(float2*, const float2*, Radices<>) {}
+  template <bool INV, int PP, int R, int... Rest>
+  __device__ __forceinline__ static void dif_impl(float2* buf, const float2* tw, Radices<R, Rest...>) {
+    dif_impl<INV, PP * R>(buf, tw, Radices<Rest...>{});
+    stage<false, INV, R, PP>(buf, tw);
+  }
+
+  // digit-reversed input -> natural output. Contains __syncthreads (whole CTA).
+  template <bool INV, int... Rs>
+  __device__ __forceinline__ static void dit(float2* buf, const float2* tw, Radices<Rs...> r) {
+    static_assert(RadixProduct<Rs...>::value == N, "radix plan does not multiply to N");
+    dit_impl<INV, 1>(buf, tw, r);
+  }
+  // natural input -> digit-reversed output.
+  template <bool INV, int... Rs>
+  __device__ __forceinline__ static void dif(float2* buf, const float2* tw, Radices<Rs...> r) {
+    static_assert(RadixProduct<Rs...>::value == N, "radix plan does not multiply to N");
+    dif_impl<INV, 1>(buf, tw, r);
+  }
+};
+
+}  // namespace cbp_dev

@@ -1,0 +1,13 @@
+"""Profiling driver: 1080p RGB spectral_deblur of a few frames (for ncu)."""
+import sys
+sys.path.insert(0, ".")
+import torch
+from paper_1203_4874_b200 import api
+pair = api.generate_coprime_pair(11, api.frame_seed(2, 0))
+lat = api.synth_frames(4 * 3, 1080, 1920, seed=1).view(4, 3, 1080, 1920)
+pub, prv = api.encode_frame(lat, pair.k1, pair.k2)
+out = torch.empty_like(pub)
+for it in range(4):
+    api.spectral_deblur(pub, pair.k1, 1e-8, out=out)
+torch.cuda.synchronize()
+print("ok")
