@@ -136,6 +136,17 @@ def dist_setup():
     return world, rank, local
 
 
+def streams_for_rank(n_streams: int, world: int, rank: int) -> list:
+    """Stream s of a multi-camera run goes to GPU s mod G (SURVEY.md section 8(e));
+    frames of different streams are independent, so there is no data-path collective."""
+    return [s for s in range(n_streams) if s % world == rank]
+
+
+def epoch_seed(e: int, rank: int) -> int:
+    """Per-rank kernel epochs for the weak-scaling run: rank r decodes its own epochs."""
+    return e + 1000 * rank
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -218,9 +229,9 @@ def run_b200(args, world, rank, local):
     prv = torch.empty((E, 1, CH, Mb, Nb), dtype=torch.float32, device=dev)
     pairs = []
     for e in range(E):
-        pair = api.generate_coprime_pair(T, api.frame_seed(2, e + 1000 * rank))
+        pair = api.generate_coprime_pair(T, api.frame_seed(2, epoch_seed(e, rank)))
         pairs.append(pair)
-        lat = api.synth_frames(EPOCH * CH, ROWS, COLS, seed=api.frame_seed(1, e + 1000 * rank))
+        lat = api.synth_frames(EPOCH * CH, ROWS, COLS, seed=api.frame_seed(1, epoch_seed(e, rank)))
         lat = lat.view(EPOCH, CH, ROWS, COLS)
         p, q = api.encode_frame(lat, pair.k1, pair.k2)
         pub[e].copy_(p)

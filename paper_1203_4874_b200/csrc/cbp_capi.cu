@@ -1,6 +1,7 @@
 // C ABI: context, workspaces, FFT plans/tables and the fixed-kernel deconvolution
 // entry points (reference decoder.cpp:273-278 spectral_deblur).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -46,6 +47,33 @@ void* workspace(cbp_ctx* ctx, int id, size_t bytes) {
   if (cudaMalloc(&ctx->ws[id], want) != cudaSuccess) return nullptr;
   ctx->ws_bytes[id] = want;
   return ctx->ws[id];
+}
+
+// Per-stage twiddles of a compile-time plan, DIT stage order; stage s (radix R, sub-length
+// PP, PS = PP*R, NB = n/R) holds W_PS^{i*(b % PP)} at [(i-1)*NB + b]. See cbp_fft_ct.cuh.
+const float2* stage_twiddles(cbp_ctx* ctx, int n, bool column) {
+  std::vector<int> rad;
+  if (!ct_radices(n, column, rad)) return nullptr;
+  const int key = column ? -2 * n - 1 : -2 * n - 2;
+  auto it = ctx->tw.find(key);
+  if (it != ctx->tw.end()) return it->second;
+  std::vector<float2> h;
+  int pp = 1;
+  for (int r : rad) {
+    const int ps = pp * r, nb = n / r;
+    for (int i = 1; i < r; ++i)
+      for (int b = 0; b < nb; ++b) {
+        const long e = long(i) * (b % pp);
+        const double ang = -2.0 * M_PI * double(e % ps) / double(ps);
+        h.push_back(make_float2(float(std::cos(ang)), float(std::sin(ang))));
+      }
+    pp = ps;
+  }
+  float2* d = nullptr;
+  if (cudaMalloc(&d, std::max<size_t>(h.size(), 1) * sizeof(float2)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  ctx->tw[key] = d;
+  return d;
 }
 
 const float2* twiddles(cbp_ctx* ctx, int n) {
@@ -111,6 +139,8 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.tw_row = twiddles(ctx, L);
   a.tw_post = twiddles(ctx, a.Gc);
   a.tw_col = twiddles(ctx, a.Gr);
+  a.twst_row = a.even ? stage_twiddles(ctx, L, false) : nullptr;
+  a.twst_col = stage_twiddles(ctx, a.Gr, true);
   if (!a.tw_row || !a.tw_post || !a.tw_col)
     return set_error(ctx, CBP_CUDA_ERROR, "twiddle table allocation failed");
   if (size_t(2) * rpc * L * sizeof(float2) > 200 * 1024)
@@ -124,7 +154,10 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   // rewritten by B, read by C) stays resident in the 126 MB L2.
   const size_t plane_bytes = size_t(a.Mb) * a.xp * sizeof(float2);
   const int ch = std::max(a.channels, 1);
-  const size_t budget = 40ull << 20;
+  static const size_t budget = [] {
+    const char* e = getenv("CBP_L2_BUDGET_MB");
+    return size_t(e ? atoi(e) : 40) << 20;
+  }();
   int frames_per_group = int(std::max<size_t>(1, budget / (plane_bytes * ch)));
   const int frames = planes / ch;
   frames_per_group = std::min(frames_per_group, std::max(frames, 1));

@@ -1,6 +1,8 @@
 // Launch interface of the three-pass deconvolution (see cbp_deblur.cu).
 #pragma once
 
+#include <vector>
+
 #include "cbp_fft.cuh"
 
 namespace cbp_dev {
@@ -31,6 +33,8 @@ struct DeblurArgs {
   const float2* tw_row;   // exp(-2 pi i k / plan_row.n)
   const float2* tw_post;  // exp(-2 pi i k / Gc), k <= Gc/2
   const float2* tw_col;   // exp(-2 pi i k / Gr)
+  const float2* twst_row; // per-stage twiddles of the specialised row plan (or null)
+  const float2* twst_col; // per-stage twiddles of the specialised column plan (or null)
   double2* S;             // per-slot column kernel transforms S[v][a] (k_wiener_s)
   size_t s_frame;         // S stride per slot
   float2* H;              // per-slot Wiener filter H[u][v] (pitch xp), scaled by 1/(Gr*Gc)
@@ -43,6 +47,7 @@ cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaSt
 // compile-time-planned passes (cbp_deblur_ct.cu); false if the grid has no specialisation
 bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream_t stream);
 bool deblur_has_ct(int Gr, int Gc, int pass);
+bool ct_radices(int n, bool column, std::vector<int>& r);
 // Wiener filter tables of `frames` slots: S (column transforms) then H (cbp_deblur_ct.cu)
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s);
 

@@ -6,6 +6,8 @@
 // column strip) with stride gridDim.x and keeps two tile buffers in shared memory;
 // the next tile's global->shared copies (cp.async, zero-filled outside the frame) are
 // in flight while the current tile is transformed, so HBM/L2 latency overlaps the FFT.
+#include <vector>
+
 #include "cbp_deblur.cuh"
 #include "cbp_fft_ct.cuh"
 
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int plane
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    FFT::template dif<false>(cur, a.tw_row, R{});
+    FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     float2* X = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
 #pragma unroll
@@ -95,13 +97,15 @@ __global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int plane
 }
 
 // ----------------------------------------------- pass B (columns + Wiener filter)
-// Forward DIF leaves spectrum row u in slot pos(u); the filter H (precomputed per kernel
-// slot by k_wiener_h) is applied there; inverse DIT returns natural rows.
+// The tile holds W columns as contiguous sequences (layout [column][row], pitch GP with
+// GP = 4 mod 16 so 4 columns x 4 rows hit distinct banks). Forward DIF leaves spectrum
+// row u in slot pos(u); the filter H (precomputed per kernel slot by k_wiener_h) is
+// applied there; the inverse DIT returns natural rows.
 template <class P>
 __global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes) {
-  constexpr int G = P::G, W = P::W, TILE = G * W;
+  constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;
   using R = typename P::R;
-  using FFT = FftIP<G, W, 1, W, kNT, true>;
+  using FFT = FftIP<G, W, GP, 1, kNT, false>;
   extern __shared__ __align__(16) float2 sm[];
   short* freq = reinterpret_cast<short*>(sm + 2 * TILE);  // slot -> spectrum row after the DIF
   for (int i = threadIdx.x; i < G; i += kNT) freq[i] = short(InvPos<R>::get(i));
@@ -110,18 +114,11 @@ __global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / strips, v0 = (tile - p * strips) * W;
     const float2* X = a.X + size_t(p) * a.x_plane + v0;
-    if (W % 2 == 0) {  // 16-byte copies of column pairs (xp and v0 even)
-      for (int idx = threadIdx.x; idx < TILE / 2; idx += kNT) {
-        const int u = idx / (W / 2), c = idx - u * (W / 2);
-        const int bytes = u < a.Mb ? min(max((a.Hc - v0 - 2 * c) * 8, 0), 16) : 0;
-        cp_async16(dst + u * W + 2 * c, bytes ? X + size_t(u) * a.xp + 2 * c : a.X, bytes);
-      }
-    } else {
-      for (int idx = threadIdx.x; idx < TILE; idx += kNT) {
-        const int u = idx / W, s = idx - u * W;
-        const int bytes = (u < a.Mb && v0 + s < a.Hc) ? 8 : 0;
-        cp_async8(dst + idx, bytes ? X + size_t(u) * a.xp + s : a.X, bytes);
-      }
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < G * W; idx += kNT) {
+      const int u = idx / W, s = idx - u * W;
+      const int bytes = (u < a.Mb && v0 + s < a.Hc) ? 8 : 0;
+      cp_async8(dst + s * GP + u, bytes ? X + size_t(u) * a.xp + s : a.X, bytes);
     }
   };
   int tile = blockIdx.x;
@@ -140,21 +137,21 @@ __global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes
     __syncthreads();
     if (status == 0) {  // uniform over the CTA
       const int t = slot->width;
-      FFT::template dif<false>(cur, a.tw_col, R{});
+      FFT::template dif<false>(cur, a.twst_col, R{});
       const float2* Ht = a.H + size_t(f) * a.h_frame + v0;
-      for (int idx = threadIdx.x; idx < TILE; idx += kNT) {
+      for (int idx = threadIdx.x; idx < G * W; idx += kNT) {
         const int sp = idx / W, s = idx - sp * W;
         const int u = freq[sp];
-        cur[idx] = cmul(cur[idx], __ldg(Ht + size_t(u) * a.xp + s));
+        cur[s * GP + sp] = cmul(cur[s * GP + sp], __ldg(Ht + size_t(u) * a.xp + s));
       }
       __syncthreads();
-      FFT::template dit<true>(cur, a.tw_col, R{});
+      FFT::template dit<true>(cur, a.twst_col, R{});
       const int M = a.Mb - t + 1;
       float2* X = a.X + size_t(p) * a.x_plane + v0;
       const int wv = min(W, a.Hc - v0);
       for (int idx = threadIdx.x; idx < M * W; idx += kNT) {
         const int u = idx / W, s = idx - u * W;
-        if (s < wv) X[size_t(u) * a.xp + s] = cur[idx];
+        if (s < wv) X[size_t(u) * a.xp + s] = cur[s * GP + u];
       }
     }
     __syncthreads();
@@ -220,7 +217,7 @@ __global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int plane
         }
       }
       __syncthreads();
-      FFT::template dif<true>(cur, a.tw_row, R{});  // natural -> slot order
+      FFT::template dif<true>(cur, a.twst_row, R{});  // natural -> slot order
       const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
       float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
       if (a.out_vec2 && N % 2 == 0) {
@@ -330,7 +327,8 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
 
 template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
-  const size_t sm = 2 * size_t(P::G) * P::W * sizeof(float2) + P::G * sizeof(short);
+  constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
+  const size_t sm = 2 * size_t(GP) * P::W * sizeof(float2) + P::G * sizeof(short);
   static int g = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -350,6 +348,26 @@ using Col2187 = ColPlan<2187, 2, Radices<9, 9, 9, 3>>;   // 4K: Gr = 2187
 using Col490 = ColPlan<490, 8, Radices<2, 5, 7, 7>>;     // 640x480: Gr = 490
 using Col270 = ColPlan<270, 8, Radices<2, 9, 3, 5>>;     // 256x256: Gr = 270
 
+// Radix plans of the specialisations above (host mirror; DIT stage order).
+bool ct_radices(int n, bool column, std::vector<int>& r) {
+  if (column) {
+    switch (n) {
+      case 1120: r = {8, 4, 5, 7}; return true;
+      case 2187: r = {9, 9, 9, 3}; return true;
+      case 490: r = {2, 5, 7, 7}; return true;
+      case 270: r = {2, 9, 3, 5}; return true;
+    }
+    return false;
+  }
+  switch (n) {
+    case 972: r = {4, 9, 9, 3}; return true;
+    case 1944: r = {8, 9, 9, 3}; return true;
+    case 324: r = {4, 9, 9}; return true;
+    case 135: r = {9, 3, 5}; return true;
+  }
+  return false;
+}
+
 bool deblur_has_ct(int Gr, int Gc, int pass) {
   if (pass == 1) return Gr == 1120 || Gr == 2187 || Gr == 490 || Gr == 270;
   if (Gc % 2) return false;
@@ -361,7 +379,7 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
   if (!deblur_has_ct(a.Gr, a.Gc, pass)) return false;
   if (pass == 0 && !a.in_vec2) return false;  // cp.async 8-byte copies need aligned rows
   if (pass == 1) {
-    if (!a.H) return false;
+    if (!a.H || !a.twst_col) return false;
     switch (a.Gr) {
       case 1120: launch_cols<Col1120>(a, planes, s); return true;
       case 2187: launch_cols<Col2187>(a, planes, s); return true;
@@ -370,6 +388,7 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
     }
     return false;
   }
+  if (!a.twst_row) return false;
   const bool inv = pass == 2;
   switch (a.Gc / 2) {
     case 972: launch_rows<Row972>(a, planes, inv, s); return true;

@@ -7,8 +7,8 @@
 //  - DIT (twiddle, then DFT_R; s = 1..m) maps digit-reversed input to natural output.
 //  - DIF (DFT_R, then twiddle; s = m..1) maps natural input to digit-reversed output.
 // Digit reversal: pos(n) = (n mod R_m) * N/R_m + pos'(n / R_m) (pos' over R_1..R_{m-1}).
-// Element n of sequence q lives at buf[q*SP + pos*ES]. Twiddles W_{P_s}^{ik} are read
-// (through L1) from a global table exp(-2 pi i j / N).
+// Element n of sequence q lives at buf[q*SP + pos*ES]. Twiddles come from per-stage
+// tables in butterfly order (stage_twiddles() on the host), stages in DIT order.
 #pragma once
 
 #include "cbp_fft.cuh"
@@ -104,43 +104,65 @@ struct FftIP {
   static constexpr int TPS = NT / NSEQ;
 
   // DIT = false: DIF stage (DFT, then twiddle); true: DIT stage (twiddle, then DFT).
+  // twst: this stage's twiddles in butterfly order, twst[(i-1)*NB + b] = W_{PS}^{i*(b % PP)},
+  // so a warp's twiddle loads are contiguous.
   template <bool DIT, bool INV, int R, int PP>
-  __device__ __forceinline__ static void stage(float2* buf, const float2* tw) {
+  __device__ __forceinline__ static void stage(float2* buf, const float2* __restrict__ twst) {
     constexpr int PS = PP * R;
     constexpr int NB = N / R;
-    constexpr int STEP = N / PS;
     constexpr int BPT = (NB + TPS - 1) / TPS;
     const int q = SEQ_FAST ? int(threadIdx.x % NSEQ) : int(threadIdx.x / TPS);
     const int tl = SEQ_FAST ? int(threadIdx.x / NSEQ) : int(threadIdx.x % TPS);
     float2* sb = buf + q * SP;
+    if constexpr (PP == 1 && ES == 1 && R % 2 == 0 && SP % 2 == 0) {
+      // contiguous butterflies: 16-byte accesses keep the stride-R pattern conflict-free
 #pragma unroll 2
-    for (int m = 0; m < BPT; ++m) {
-      const int b = tl + m * TPS;
-      if (NB % TPS == 0 || b < NB) {
-        const int k = b % PP;
-        const int base = (b - k) * R + k;  // block * PS + k
-        float2 v[R];
+      for (int m = 0; m < BPT; ++m) {
+        const int b = tl + m * TPS;
+        if (NB % TPS == 0 || b < NB) {
+          float4* p4 = reinterpret_cast<float4*>(sb + b * R);
+          float2 v[R];
 #pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
-        if (DIT && PP > 1 && k != 0) {
-#pragma unroll
-          for (int i = 1; i < R; ++i) {
-            float2 w = __ldg(&tw[i * k * STEP]);
-            if (INV) w.y = -w.y;
-            v[i] = cmul(v[i], w);
+          for (int j = 0; j < R / 2; ++j) {
+            const float4 x = p4[j];
+            v[2 * j] = make_float2(x.x, x.y);
+            v[2 * j + 1] = make_float2(x.z, x.w);
           }
-        }
-        dft<R, INV>(v);
-        if (!DIT && PP > 1 && k != 0) {
+          dft<R, INV>(v);
 #pragma unroll
-          for (int i = 1; i < R; ++i) {
-            float2 w = __ldg(&tw[i * k * STEP]);
-            if (INV) w.y = -w.y;
-            v[i] = cmul(v[i], w);
+          for (int j = 0; j < R / 2; ++j) p4[j] = make_float4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y);
+        }
+      }
+    } else {
+#pragma unroll 2
+      for (int m = 0; m < BPT; ++m) {
+        const int b = tl + m * TPS;
+        if (NB % TPS == 0 || b < NB) {
+          const int k = PP > 1 ? b % PP : 0;
+          const int base = (b - k) * R + k;  // block * PS + k
+          float2 v[R];
+#pragma unroll
+          for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
+          if (DIT && PP > 1) {
+#pragma unroll
+            for (int i = 1; i < R; ++i) {
+              float2 w = __ldg(&twst[(i - 1) * NB + b]);
+              if (INV) w.y = -w.y;
+              v[i] = cmul(v[i], w);
+            }
           }
-        }
+          dft<R, INV>(v);
+          if (!DIT && PP > 1) {
 #pragma unroll
-        for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
+            for (int i = 1; i < R; ++i) {
+              float2 w = __ldg(&twst[(i - 1) * NB + b]);
+              if (INV) w.y = -w.y;
+              v[i] = cmul(v[i], w);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
+        }
       }
     }
     __syncthreads();
@@ -151,13 +173,13 @@ struct FftIP {
   template <bool INV, int PP, int R, int... Rest>
   __device__ __forceinline__ static void dit_impl(float2* buf, const float2* tw, Radices<R, Rest...>) {
     stage<true, INV, R, PP>(buf, tw);
-    dit_impl<INV, PP * R>(buf, tw, Radices<Rest...>{});
+    dit_impl<INV, PP * R>(buf, tw + (R - 1) * (N / R), Radices<Rest...>{});
   }
   template <bool INV, int PP>
   __device__ __forceinline__ static void dif_impl(float2*, const float2*, Radices<>) {}
   template <bool INV, int PP, int R, int... Rest>
   __device__ __forceinline__ static void dif_impl(float2* buf, const float2* tw, Radices<R, Rest...>) {
-    dif_impl<INV, PP * R>(buf, tw, Radices<Rest...>{});
+    dif_impl<INV, PP * R>(buf, tw + (R - 1) * (N / R), Radices<Rest...>{});
     stage<false, INV, R, PP>(buf, tw);
   }
 

@@ -1,0 +1,390 @@
+"""GPU parity: the CUDA path (libcbp_cuda.so through the C ABI) against the FP64 oracle on
+identical FP32 inputs, plus the reference's error behaviour.
+
+Tolerances (BASELINE.md "Correctness gates", floating point):
+  kernel   relative L2 <= 1e-5 after the sum-to-1 normalisation;
+  latent   max-abs <= 1e-4 and PSNR(gpu, oracle) >= 90 dB;
+  truth    PSNR(gpu, ground-truth latent) >= 40 dB (acceptance.cpp:78);
+  widths / clamped flags / error codes exact; GPU encode bit-exact.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+KREL = 1e-5
+LMAX = 1e-4
+LPSNR = 90.0
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1203_4874_b200 import api as A
+    torch.cuda.set_device(0)
+    return A
+
+
+def make(oracle, rows, cols, ch, t, lseed, pseed):
+    lat = oracle.random_frame(rows, cols, ch, lseed)
+    pair = oracle.generate_coprime_pair(t, pseed)
+    pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+    return lat, pair, pub.astype(np.float32), prv.astype(np.float32)
+
+
+def krel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def check_decode(oracle, api, lat, pub, prv, lo, hi, hint=None, trust=False, epsilon=None):
+    cfg_o = oracle.make_cfg(lo, hi, trust_hint=trust, epsilon=epsilon)
+    ref = oracle.decode_frame(pub.astype(np.float64), prv.astype(np.float64), hint=hint, cfg=cfg_o)
+    d = api.decode_frame(torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda(), hint=hint,
+                         cfg=api.make_cfg(lo, hi, trust_hint=trust, epsilon=epsilon))
+    got = d.latent.cpu().numpy().astype(np.float64)
+    assert d.width_used == ref.width_used and d.width_clamped == ref.width_clamped
+    assert krel(d.kernel_estimate, ref.kernel) <= KREL
+    assert got.shape == ref.latent.shape
+    assert np.abs(got - ref.latent).max() <= LMAX
+    assert oracle.psnr(ref.latent, got) >= LPSNR
+    assert abs(d.validation_residual - ref.validation_residual) <= 1e-6
+    assert abs(d.epsilon_used - ref.epsilon_used) <= 1e-12
+    if lat is not None:
+        assert oracle.psnr(lat, got) >= 40.0
+    return d, ref
+
+
+# ------------------------------------------------------------------ decode_frame
+FIXTURES = sorted(glob.glob(os.path.join(HERE, "golden", "*.npz")))
+
+
+@pytest.mark.parametrize("path", FIXTURES, ids=[os.path.basename(p) for p in FIXTURES])
+def test_golden_fixtures(oracle, api, path):
+    g = np.load(path)
+    lat, pair, pub, prv = make(oracle, int(g["rows"]), int(g["cols"]), int(g["channels"]), int(g["t"]),
+                               int(g["latent_seed"]), int(g["pair_seed"]))
+    d = api.decode_frame(torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda(),
+                         cfg=api.make_cfg(int(g["search_min"]), int(g["search_max"])))
+    got = d.latent.cpu().numpy()
+    assert d.width_used == int(g["t"])
+    assert krel(d.kernel_estimate, g["kernel"]) <= KREL
+    assert np.abs(got - g["latent"]).max() <= LMAX
+    assert oracle.psnr(g["latent"].astype(np.float64), got.astype(np.float64)) >= LPSNR
+    assert abs(d.validation_residual - float(g["validation_residual"])) <= 1e-6
+
+
+@pytest.mark.parametrize("rows,cols,ch,t,lo,hi,hint,trust", [
+    (64, 64, 1, 5, 3, 9, None, False),       # decoder_test.cpp:311 round trip
+    (64, 64, 1, 5, 3, 9, 5, True),           # trusted hint
+    (48, 40, 1, 5, 3, 9, None, False),       # non-square
+    (24, 24, 3, 3, 3, 7, None, False),       # RGB via luma
+    (96, 96, 1, 9, 3, 9, None, False),
+    (128, 128, 1, 13, 9, 25, None, False),
+    (256, 256, 1, 7, 3, 25, None, False),    # BASELINE config 1
+    (480, 640, 1, 9, 3, 25, None, False),    # BASELINE config 2 frame
+    (101, 67, 1, 7, 3, 25, None, False),     # odd grids (generic FFT path)
+])
+def test_decode_frame_parity(oracle, api, rows, cols, ch, t, lo, hi, hint, trust):
+    lat, pair, pub, prv = make(oracle, rows, cols, ch, t, oracle.frame_seed(1, rows + t), oracle.frame_seed(2, cols + t))
+    d, _ = check_decode(oracle, api, lat, pub, prv, lo, hi, hint=hint, trust=trust)
+    assert krel(d.kernel_estimate, pair.k1) <= 1e-4
+
+
+def test_decode_1080p_rgb_parity(oracle, api):
+    """BASELINE config 3 frame at full size: 1920x1080 RGB, t = 11."""
+    lat, pair, pub, prv = make(oracle, 1080, 1920, 3, 11, oracle.frame_seed(1, 0), oracle.frame_seed(2, 0))
+    check_decode(oracle, api, lat, pub, prv, 9, 25)
+
+
+def test_decode_4k_parity(oracle, api):
+    """BASELINE config 4 frame at full size: 3840x2160 gray, t = 15 (trusted hint)."""
+    lat, pair, pub, prv = make(oracle, 2160, 3840, 1, 15, oracle.frame_seed(1, 4), oracle.frame_seed(2, 4))
+    check_decode(oracle, api, lat, pub, prv, 9, 25, hint=15, trust=True)
+
+
+def test_decode_exact_epsilon_and_swap(oracle, api):
+    lat, pair, pub, prv = make(oracle, 32, 32, 1, 3, 145, 145)
+    d, _ = check_decode(oracle, api, lat, pub, prv, 3, 7, epsilon=1e-12)
+    s, _ = check_decode(oracle, api, lat, prv, pub, 3, 7, epsilon=1e-12)
+    assert np.abs(d.kernel_estimate - pair.k1).max() <= 1e-6
+    assert np.abs(s.kernel_estimate - pair.k2).max() <= 1e-6
+
+
+def test_decode_batch_equals_single(oracle, api):
+    frames = [make(oracle, 72, 80, 1, 5, oracle.frame_seed(7, i), oracle.frame_seed(8, i)) for i in range(4)]
+    P = torch.from_numpy(np.stack([f[2] for f in frames])).cuda()
+    Q = torch.from_numpy(np.stack([f[3] for f in frames])).cuda()
+    cfg = api.make_cfg(3, 9)
+    batch = api.decode_frames(P, Q, cfg=cfg)
+    for i, f in enumerate(frames):
+        one = api.decode_frame(P[i], Q[i], cfg=cfg)
+        assert batch[i].width_used == one.width_used == 5
+        assert np.array_equal(batch[i].kernel_estimate, one.kernel_estimate)
+        assert torch.equal(batch[i].latent, one.latent)
+
+
+def test_decode_u16_quantized(oracle, api):
+    lat = oracle.random_mat(48, 48, 153)
+    pair = oracle.generate_coprime_pair(5, 153)
+    pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+    pub = oracle.quantize(pub, 16).astype(np.float32)
+    prv = oracle.quantize(prv, 16).astype(np.float32)
+    d, _ = check_decode(oracle, api, None, pub, prv, 3, 9, hint=5, trust=True)
+    assert oracle.psnr(lat, d.latent[0].cpu().numpy().astype(np.float64)) >= 40.0
+
+
+# ----------------------------------------------------------------- spectral_deblur
+@pytest.mark.parametrize("rows,cols,t,ch", [(16, 16, 3, 1), (24, 24, 3, 1), (61, 97, 7, 1), (480, 640, 9, 1),
+                                            (256, 256, 7, 2), (1080, 1920, 11, 3), (2160, 3840, 15, 1)])
+def test_spectral_deblur_parity(oracle, api, rows, cols, t, ch):
+    chn = 3 if ch == 3 else 1
+    lat, pair, pub, _ = make(oracle, rows, cols, chn, t, oracle.frame_seed(3, rows), oracle.frame_seed(4, cols))
+    ref = np.stack([oracle.spectral_deblur(pub[k].astype(np.float64), pair.k1, 1e-8) for k in range(chn)])
+    x = torch.from_numpy(pub).cuda()
+    if ch == 2:  # batch of two identical frames through the batched entry point
+        x = torch.stack([x, x])
+    got = api.spectral_deblur(x, pair.k1, 1e-8).cpu().numpy().astype(np.float64)
+    if ch == 2:
+        assert np.array_equal(got[0], got[1])
+        got = got[0]
+    assert np.abs(got - ref).max() <= LMAX
+    assert oracle.psnr(ref, got) >= LPSNR
+
+
+def test_spectral_deblur_identity_and_pitched(oracle, api):
+    b = oracle.random_mat(9, 7, 131).astype(np.float32)
+    got = api.spectral_deblur(torch.from_numpy(b).cuda(), [[1.0]], 0.0).cpu().numpy()
+    assert np.abs(got - b).max() <= 1e-6
+    # pitched input rows (ld > cols) through the C ABI
+    import ctypes as C
+    lat, pair, pub, _ = make(oracle, 480, 640, 1, 9, 5, 6)
+    rows, cols = pub.shape[1:]
+    ld = cols + 6
+    dev = torch.zeros((rows, ld), dtype=torch.float32, device="cuda")
+    dev[:, :cols] = torch.from_numpy(pub[0]).cuda()
+    out = torch.zeros((rows, ld + 2), dtype=torch.float32, device="cuda")
+    ctx = api.context()
+    k = np.ascontiguousarray(pair.k1)
+    ctx.check(api.N.lib().cbp_spectral_deblur(ctx.ptr, C.c_void_p(dev.data_ptr()), 1, 1, rows, cols, ld,
+                                              k.ctypes.data_as(C.c_void_p), 9, 1e-8, C.c_void_p(out.data_ptr()),
+                                              ld + 2, api._stream_ptr(dev.device)))
+    got = out[: rows - 8, : cols - 8].cpu().numpy().astype(np.float64)
+    ref = oracle.spectral_deblur(pub[0].astype(np.float64), pair.k1, 1e-8)
+    assert np.abs(got - ref).max() <= LMAX
+
+
+def test_slot_chaining_equals_spectral_deblur(oracle, api):
+    """decode_frames_async -> spectral_deblur_slot (the bench path) matches the host-kernel
+    spectral_deblur with the decoded kernel and epsilon."""
+    lat = oracle.random_frame(96, 128, 3, 11)
+    pair = oracle.generate_coprime_pair(7, 12)
+    frames = []
+    for i in range(3):
+        l = oracle.random_frame(96, 128, 3, 20 + i)
+        frames.append(oracle.encode_frame(l, pair.k1, pair.k2))
+    P = torch.from_numpy(np.stack([f[0] for f in frames]).astype(np.float32)).cuda()
+    Q = torch.from_numpy(np.stack([f[1] for f in frames]).astype(np.float32)).cuda()
+    cfg = api.make_cfg(3, 9)
+    out = torch.zeros_like(P)
+    slots = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    api.decode_frames_async(P[0:1], Q[0:1], cfg, out[0:1], slots[0])
+    api.spectral_deblur_slot(P[1:], slots[0].data_ptr(), out[1:])
+    sl = api.read_slots(slots, 1)[0]
+    assert sl.status == 0 and sl.width == 7
+    k = np.array(sl.weights[:49]).reshape(7, 7)
+    ref = api.spectral_deblur(P[1:], k, sl.epsilon)
+    assert torch.equal(out[1:, :, :96, :128], ref)
+
+
+def test_host_pipeline_equals_device_path(oracle, api):
+    pair = oracle.generate_coprime_pair(5, 31)
+    frames = [oracle.encode_frame(oracle.random_frame(60, 70, 1, 40 + i), pair.k1, pair.k2) for i in range(5)]
+    pub = torch.from_numpy(np.stack([f[0] for f in frames]).astype(np.float32)).pin_memory()
+    prv = torch.from_numpy(np.stack([f[1] for f in frames]).astype(np.float32)).pin_memory()
+    rec = [1, 0, 0, 1, 0]
+    cfg = api.make_cfg(3, 9)
+    out, slots = api.decode_run_host(pub, prv, rec, cfg)
+    assert len(slots) == 2 and all(s.status == 0 and s.width == 5 for s in slots)
+    d0 = api.decode_frame(pub[0], prv[0], cfg=cfg)
+    assert torch.equal(out[0, :, :60, :70], d0.latent.cpu())
+    k = np.array(slots[0].weights[:25]).reshape(5, 5)
+    ref = api.spectral_deblur(pub[1:3].cuda(), k, slots[0].epsilon).cpu()
+    assert torch.equal(out[1:3, :, :60, :70], ref)
+
+
+# ----------------------------------------------------------------- stage level
+def test_sample_slices_parity(oracle, api):
+    lat, pair, pub, prv = make(oracle, 90, 110, 3, 9, 3, 4)
+    for axis in (0, 1):
+        sp, sq = api.sample_slices(torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda(), 9, axis)
+        rp = oracle.axis_roots_dft(oracle.luma(pub.astype(np.float64)), axis, 9)
+        rq = oracle.axis_roots_dft(oracle.luma(prv.astype(np.float64)), axis, 9)
+        if axis == 1:
+            rp, rq = rp.T, rq.T
+        assert np.abs(sp - rp).max() <= 1e-12 * np.abs(rp).max()
+        assert np.abs(sq - rq).max() <= 1e-12 * np.abs(rq).max()
+
+
+def aligned(e1, e2, r1, r2):
+    e = np.concatenate([e1, e2]); r = np.concatenate([r1, r2])
+    c = np.vdot(e, r) / np.vdot(e, e)
+    return float(np.abs(c * e - r).max())
+
+
+def test_cofactor_solve_known_answers(oracle, api):
+    k1, k2, gap = api.cofactor_null_solve([1, 3, 2], [3, 4, 1], 2)
+    assert aligned(k1, k2, [1, 2], [3, 1]) <= 1e-12 and gap > 1e-3
+    k1, k2, _ = api.cofactor_null_solve([1, 1], [1, 1], 1)
+    assert abs(k1[0] - k2[0]) <= 1e-14 and abs(abs(k1[0]) - 2 ** -0.5) <= 1e-12
+    with pytest.raises(api.CbpError) as e:
+        api.cofactor_null_solve([1, 2, 1], [1, 2, 1], 2)
+    assert e.value.code == "IllConditioned"
+    rng = np.random.default_rng(99)
+    for _ in range(6):
+        l = rng.uniform(-1, 1, 7) + 1j * rng.uniform(-1, 1, 7)
+        u = rng.uniform(-1, 1, 3) + 1j * rng.uniform(-1, 1, 3)
+        v = rng.uniform(-1, 1, 3) + 1j * rng.uniform(-1, 1, 3)
+        k1, k2, _ = api.cofactor_null_solve(np.convolve(l, u), np.convolve(l, v), 3)
+        assert aligned(k1, k2, u, v) <= 1e-8
+
+
+def test_cofactor_batch_vs_oracle(oracle, api):
+    lat, pair, pub, prv = make(oracle, 200, 300, 1, 11, 5, 6)
+    s1 = oracle.axis_roots_dft(pub[0].astype(np.float64), 0, 11)
+    s2 = oracle.axis_roots_dft(prv[0].astype(np.float64), 0, 11)
+    k1, k2, gaps = api.cofactor_solve_batch(s1, s2, 11)
+    for i in range(11):
+        r1, r2, g = oracle.cofactor_null_solve(s1[i], s2[i], 11)
+        assert aligned(k1[i], k2[i], r1, r2) <= 1e-9
+        assert abs(gaps[i] - g) <= 1e-6 * g
+
+
+def test_sample_cofactors_and_2d_stages(oracle, api):
+    lat, pair, pub, prv = make(oracle, 40, 44, 1, 5, 17, 18)
+    P, Q = torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda()
+    vals = []
+    for axis in (0, 1):
+        v, g = api.sample_cofactors(P, Q, 5, axis)
+        rv, rg = oracle.sample_cofactors(pub.astype(np.float64), prv.astype(np.float64), 5, axis)
+        for i in range(5):
+            a = v[i] if axis == 0 else v[:, i]
+            b = rv[i] if axis == 0 else rv[:, i]
+            assert aligned(a, a[:0], b, b[:0]) <= 1e-9
+        assert np.abs(g - rg).max() <= 1e-6 * rg.max()
+        vals.append(v)
+    for axis in (0, 1):
+        assert np.abs(api.complete_to_spectrum(vals[axis], axis) - oracle.complete_to_spectrum(vals[axis], axis)).max() <= 1e-12
+    lam, mu, res = api.resolve_scales(vals[0], vals[1])
+    rl, rm, rr = oracle.resolve_scales(vals[0], vals[1])
+    assert aligned(lam, mu, rl, rm) <= 1e-10 and abs(res - rr) <= 1e-10
+    A = api.complete_to_spectrum(vals[0], 0)
+    B = api.complete_to_spectrum(vals[1], 1)
+    w = api.assemble_kernel(A, B, lam, mu)
+    assert np.abs(w - oracle.assemble_kernel(A, B, rl, rm)).max() <= 1e-9
+    assert krel(w, pair.k1) <= 1e-5
+
+
+def test_estimate_width_parity(oracle, api):
+    for (size, t, lo, hi, lseed, kseed) in [(24, 5, 3, 7, 101, 101), (20, 3, 3, 9, 102, 102),
+                                           (64, 25, 9, 25, 103, 101), (64, 27, 9, 25, 104, 101)]:
+        lat = oracle.random_mat(size, size, lseed)
+        pair = oracle.generate_coprime_pair(t, kseed)
+        pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+        got = api.estimate_kernel_width(pub.astype(np.float32), prv.astype(np.float32), lo, hi, 1e-6)
+        ref = oracle.estimate_kernel_width(pub.astype(np.float32).astype(np.float64),
+                                           prv.astype(np.float32).astype(np.float64), lo, hi, 1e-6)
+        assert got == ref
+
+
+def test_validate_pair_parity(oracle, api):
+    lat, pair, pub, prv = make(oracle, 16, 16, 1, 3, 155, 155)
+    r = api.validate_pair(pub, prv, pair.k1, pair.k2)
+    assert abs(r - oracle.validate_pair(pub.astype(np.float64), prv.astype(np.float64), pair.k1, pair.k2)) <= 1e-9
+    bad = oracle.conv2_full(oracle.random_mat(16, 16, 156), pair.k2).astype(np.float32)
+    assert api.validate_pair(pub, bad[None], pair.k1, pair.k2) > 0.1
+
+
+def test_encode_bit_exact(oracle, api):
+    lat = oracle.random_frame(50, 70, 3, 9).astype(np.float32)
+    pair = oracle.generate_coprime_pair(7, 9)
+    pub, prv = api.encode_frame(torch.from_numpy(lat).cuda(), pair.k1, pair.k2)
+    rp, rq = oracle.encode_frame(lat.astype(np.float64), pair.k1, pair.k2)
+    assert np.array_equal(pub.cpu().numpy(), rp.astype(np.float32))
+    assert np.array_equal(prv.cpu().numpy(), rq.astype(np.float32))
+
+
+# ------------------------------------------------------------------ errors
+def test_error_messages_match_reference(oracle, api):
+    z = np.zeros((12, 12), np.float32)
+    with pytest.raises(api.CbpError) as e:
+        api.decode_frame(z, z, hint=3, cfg=api.make_cfg(3, 7, trust_hint=True))
+    with pytest.raises(oracle.OracleError) as r:
+        oracle.decode_frame(z.astype(np.float64), z.astype(np.float64), hint=3, cfg=oracle.make_cfg(3, 7, trust_hint=True))
+    assert e.value.code == r.value.code == "IllConditionedSlice"
+    assert str(e.value) == str(r.value)
+    lat = oracle.random_mat(16, 16, 105)
+    a1 = oracle.random_mat(3, 5, 106, 0.05, 1.0)
+    a2 = oracle.random_mat(3, 5, 107, 0.05, 1.0)
+    p = oracle.conv2_full(lat, a1).astype(np.float32)
+    q = oracle.conv2_full(lat, a2).astype(np.float32)
+    with pytest.raises(api.CbpError) as e:
+        api.decode_frame(p, q, cfg=api.make_cfg(3, 7))
+    with pytest.raises(oracle.OracleError) as r:
+        oracle.decode_frame(p.astype(np.float64), q.astype(np.float64), cfg=oracle.make_cfg(3, 7))
+    assert e.value.code == r.value.code == "InconsistentAxes" and str(e.value) == str(r.value)
+
+
+@pytest.mark.parametrize("kwargs,code", [
+    (dict(search_min=4, search_max=9), "InvalidArgument"),
+    (dict(search_min=3, search_max=65), "InvalidArgument"),
+    (dict(tau=1.5), "InvalidArgument"),
+])
+def test_config_errors(api, kwargs, code):
+    x = np.random.default_rng(0).uniform(0, 1, (40, 40)).astype(np.float32)
+    with pytest.raises(api.CbpError) as e:
+        api.decode_frame(x, x, cfg=api.make_cfg(**kwargs))
+    assert e.value.code == code
+
+
+def test_input_errors(api):
+    x = np.random.default_rng(0).uniform(0, 1, (40, 40)).astype(np.float32)
+    with pytest.raises(api.CbpError) as e:  # decoder.cpp:47
+        api.decode_frame(x[:20, :20], x[:20, :20], cfg=api.make_cfg(9, 25))
+    assert e.value.code == "FrameTooSmall"
+    y = x.copy(); y[3, 4] = np.nan
+    with pytest.raises(api.CbpError) as e:  # image.cpp:33
+        api.decode_frame(y, y, cfg=api.make_cfg(3, 9))
+    assert e.value.code == "RangeExceeded"
+    with pytest.raises(api.CbpError) as e:  # decoder.cpp:26-28
+        api.decode_frame(x, x, hint=4, cfg=api.make_cfg(3, 9))
+    assert e.value.code == "InvalidArgument"
+    k = np.full((3, 3), 1 / 9.0); k[0, 0] = -0.1
+    with pytest.raises(api.CbpError) as e:  # kernel.cpp:7-17
+        api.spectral_deblur(x, k, 1e-8)
+    assert e.value.code == "InvalidArgument"
+    with pytest.raises(api.CbpError) as e:
+        api.spectral_deblur(x, np.full((3, 3), 0.1), 1e-8)
+    assert e.value.code == "InvalidArgument"
+    with pytest.raises(api.CbpError) as e:
+        api.spectral_deblur(x, np.full((3, 3), 1 / 9.0), -1.0)
+    assert e.value.code == "InvalidArgument"
+
+
+def test_acceptance_1_on_gpu(oracle, api):
+    """Criterion 1 (subset) through the GPU path: PSNR >= 40 dB, residual <= 1e-4."""
+    for t in (3, 5, 9):
+        for s in range(1, 5):
+            lat = oracle.random_frame(64, 64, 1, oracle.frame_seed(100 + t, s))
+            pair = oracle.generate_coprime_pair(t, oracle.frame_seed(100 + 31 * t, s))
+            pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+            d = api.decode_frame(pub.astype(np.float32), prv.astype(np.float32), cfg=api.make_cfg(3, 9))
+            assert d.width_used == t
+            assert oracle.psnr(lat, d.latent.cpu().numpy().astype(np.float64)) >= 40.0
+            assert d.validation_residual <= 1e-4
