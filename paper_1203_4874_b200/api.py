@@ -394,28 +394,32 @@ def launch_count(device: int | None = None) -> int:
 
 
 def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, out: torch.Tensor,
-                        slots: torch.Tensor, hints=None):
+                        slots: torch.Tensor, hints=None, ctx: N.Context | None = None, stream=None):
     """cbp_decode_frames_async on device tensors (batch, ch, rows, cols); ``slots`` is a
-    uint8 device tensor of batch * sizeof(KernelSlot) bytes receiving the per-frame state."""
+    uint8 device tensor of batch * sizeof(KernelSlot) bytes receiving the per-frame state.
+    ``ctx`` / ``stream`` select the context (workspaces) and CUDA stream (default: the
+    thread's context and torch's current stream)."""
     B, ch, rows, cols = pub.shape
-    ctx = context(pub.device.index)
+    ctx = ctx or context(pub.device.index)
     hint_arr = None
     if hints is not None:
         hint_arr = (C.c_int * B)(*[int(h) for h in hints])
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
     ctx.check(N.lib().cbp_decode_frames_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(prv.data_ptr()), B,
                                               ch, rows, cols, pub.stride(-2), hint_arr, C.byref(cfg),
                                               C.c_void_p(out.data_ptr()), out.stride(-2),
-                                              C.c_void_p(slots.data_ptr()), _stream_ptr(pub.device)))
+                                              C.c_void_p(slots.data_ptr()), st))
 
 
-def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor):
+def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor, ctx: N.Context | None = None,
+                         stream=None):
     """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device."""
     B, ch, rows, cols = blurred.shape
-    ctx = context(blurred.device.index)
+    ctx = ctx or context(blurred.device.index)
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(blurred.device)
     ctx.check(N.lib().cbp_spectral_deblur_slot(ctx.ptr, C.c_void_p(blurred.data_ptr()), B, ch, rows, cols,
                                                blurred.stride(-2), C.c_void_p(slot_ptr),
-                                               C.c_void_p(out.data_ptr()), out.stride(-2),
-                                               _stream_ptr(blurred.device)))
+                                               C.c_void_p(out.data_ptr()), out.stride(-2), st))
 
 
 def read_slots(slots: torch.Tensor, count: int) -> list:

@@ -141,6 +141,10 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.tw_col = twiddles(ctx, a.Gr);
   a.twst_row = a.even ? stage_twiddles(ctx, L, false) : nullptr;
   a.twst_col = stage_twiddles(ctx, a.Gr, true);
+  static const int dbg = getenv("CBP_DEBLUR_DBG") ? atoi(getenv("CBP_DEBLUR_DBG")) : 0;
+  a.dbg = dbg;
+  static const int variant = getenv("CBP_FFT_VARIANT") ? atoi(getenv("CBP_FFT_VARIANT")) : 0;
+  a.variant = variant;
   if (!a.tw_row || !a.tw_post || !a.tw_col)
     return set_error(ctx, CBP_CUDA_ERROR, "twiddle table allocation failed");
   if (size_t(2) * rpc * L * sizeof(float2) > 200 * 1024)

@@ -24,6 +24,8 @@ struct DeblurArgs {
   int in_vec2;      // input rows 8-byte aligned (float2 loads)
   int out_vec2;     // output rows 8-byte aligned (float2 stores)
   int in_vec4;      // input rows 16-byte aligned (16-byte cp.async)
+  int dbg;          // experiment switches (CBP_DEBLUR_DBG): 1 skip FFT stages, 2 skip filter
+  int variant;      // kernel configuration variant (CBP_FFT_VARIANT), 0 = default
   int col_width;    // pass B columns per CTA
   const cbp_kernel_slot* slot;
   int slot_per_frame;  // 1: slot[p / channels]; 0: slot[0] for every plane

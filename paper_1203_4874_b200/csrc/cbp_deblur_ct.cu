@@ -13,18 +13,23 @@
 
 namespace cbp_dev {
 
-constexpr int kNT = 256;
 
-template <int L_, int RPC_, class Rs>
+// PIPE: persistent CTAs with a double-buffered cp.async prefetch of the next tile;
+// otherwise one tile per CTA and latency is hidden by many resident CTAs.
+template <int L_, int RPC_, class Rs, int NT_, bool PIPE_ = true>
 struct RowPlan {
   static constexpr int L = L_;
   static constexpr int RPC = RPC_;
+  static constexpr int NT = NT_;
+  static constexpr bool PIPE = PIPE_;
   using R = Rs;
 };
-template <int G_, int W_, class Rs>
+template <int G_, int W_, class Rs, int NT_, bool PIPE_ = true>
 struct ColPlan {
   static constexpr int G = G_;
   static constexpr int W = W_;
+  static constexpr int NT = NT_;
+  static constexpr bool PIPE = PIPE_;
   using R = Rs;
 };
 
@@ -35,13 +40,14 @@ __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a
 // ------------------------------------------------------------ pass A (rows r2c)
 // Row s of a tile holds z[m] = (x[2m], x[2m+1]); forward DIF leaves Z[k] in slot pos(k).
 template <class P>
-__global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int planes) {
+  constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, L, 1, kNT, false>;
+  using FFT = FftIP<L, RPC, L, 1, NT, false>;
   extern __shared__ __align__(16) float2 sm[];
-  short* pos = reinterpret_cast<short*>(sm + 2 * TILE);  // slot of Z[k] after the DIF
-  for (int i = threadIdx.x; i < L; i += kNT) pos[i] = short(Pos<R>::get(i));
+  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // slot of Z[k] after the DIF
+  for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
   const bool v16 = a.in_vec4 && (L % 2 == 0);
@@ -53,12 +59,12 @@ __global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int plane
       const bool ok = r0 + s < a.Mb;
       const float* row = src + size_t(s) * a.in_ld;
       if (v16) {
-        for (int c = threadIdx.x; c < L / 2; c += kNT) {
+        for (int c = threadIdx.x; c < L / 2; c += NT) {
           const int bytes = ok ? min(max((a.Nb - 4 * c) * 4, 0), 16) : 0;
           cp_async16(dst + s * L + 2 * c, bytes ? row + 4 * c : a.in, bytes);
         }
       } else {
-        for (int m = threadIdx.x; m < L; m += kNT) {
+        for (int m = threadIdx.x; m < L; m += NT) {
           const int bytes = ok ? min(max((a.Nb - 2 * m) * 4, 0), 8) : 0;
           cp_async8(dst + s * L + m, bytes ? row + 2 * m : a.in, bytes);
         }
@@ -69,20 +75,20 @@ __global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int plane
   if (tile < total) issue(tile, sm);
   cp_async_commit();
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
-    float2* cur = sm + (it & 1) * TILE;
+    float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int next = tile + gridDim.x;
-    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    FFT::template dif<false>(cur, a.twst_row, R{});
+    if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     float2* X = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
 #pragma unroll
     for (int s = 0; s < RPC; ++s) {
       if (r0 + s >= a.Mb) break;
       const float2* z = cur + s * L;
-      for (int k = threadIdx.x; k <= L; k += kNT) {
+      for (int k = threadIdx.x; k <= L; k += NT) {
         const float2 zk = z[pos[k == L ? 0 : k]];
         const float2 zc = cconj(z[pos[k == 0 ? 0 : L - k]]);
         const float2 e = cscale(cadd(zk, zc), 0.5f);
@@ -102,20 +108,24 @@ __global__ void __launch_bounds__(kNT) k_rows_forward_ct(DeblurArgs a, int plane
 // row u in slot pos(u); the filter H (precomputed per kernel slot by k_wiener_h) is
 // applied there; the inverse DIT returns natural rows.
 template <class P>
-__global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int planes) {
+  constexpr int NT = P::NT;
   constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;
+  constexpr int NBUF = P::PIPE ? 2 : 1;
   using R = typename P::R;
-  using FFT = FftIP<G, W, GP, 1, kNT, false>;
+  using FFT = FftIP<G, W, GP, 1, NT, false>;
   extern __shared__ __align__(16) float2 sm[];
-  short* freq = reinterpret_cast<short*>(sm + 2 * TILE);  // slot -> spectrum row after the DIF
-  for (int i = threadIdx.x; i < G; i += kNT) freq[i] = short(InvPos<R>::get(i));
+  float2* Hs = sm + NBUF * TILE;                           // filter strip, slot order
+  short* pos = reinterpret_cast<short*>(Hs + TILE);        // spectrum row u -> slot after the DIF
+  for (int i = threadIdx.x; i < G; i += NT) pos[i] = short(Pos<R>::get(i));
+  __syncthreads();
   const int strips = (a.Hc + W - 1) / W;
   const int total = planes * strips;
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / strips, v0 = (tile - p * strips) * W;
     const float2* X = a.X + size_t(p) * a.x_plane + v0;
 #pragma unroll 4
-    for (int idx = threadIdx.x; idx < G * W; idx += kNT) {
+    for (int idx = threadIdx.x; idx < G * W; idx += NT) {
       const int u = idx / W, s = idx - u * W;
       const int bytes = (u < a.Mb && v0 + s < a.Hc) ? 8 : 0;
       cp_async8(dst + s * GP + u, bytes ? X + size_t(u) * a.xp + s : a.X, bytes);
@@ -125,31 +135,41 @@ __global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes
   if (tile < total) issue(tile, sm);
   cp_async_commit();
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
-    float2* cur = sm + (it & 1) * TILE;
-    const int next = tile + gridDim.x;
-    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
-    cp_async_commit();
+    float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int p = tile / strips, v0 = (tile - p * strips) * W;
     const int f = a.slot_per_frame ? p / a.channels : 0;
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
-    cp_async_wait<1>();
+    cp_async_wait<0>();
     __syncthreads();
+    // filter strip H[u][v0+s] -> Hs[s][pos(u)], in flight during the forward transform
+    if (status == 0) {
+      const float2* Ht = a.H + size_t(f) * a.h_frame + v0;
+      for (int idx = threadIdx.x; idx < G * W; idx += NT) {
+        const int u = idx / W, s = idx - u * W;
+        cp_async8(Hs + s * GP + pos[u], Ht + size_t(u) * a.xp + s, 8);
+      }
+    }
+    cp_async_commit();
+    const int next = tile + gridDim.x;
+    if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    cp_async_commit();
     if (status == 0) {  // uniform over the CTA
       const int t = slot->width;
-      FFT::template dif<false>(cur, a.twst_col, R{});
-      const float2* Ht = a.H + size_t(f) * a.h_frame + v0;
-      for (int idx = threadIdx.x; idx < G * W; idx += kNT) {
-        const int sp = idx / W, s = idx - sp * W;
-        const int u = freq[sp];
-        cur[s * GP + sp] = cmul(cur[s * GP + sp], __ldg(Ht + size_t(u) * a.xp + s));
-      }
+      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
+      cp_async_wait<1>();  // the filter strip (the next tile's copies may still fly)
       __syncthreads();
-      FFT::template dit<true>(cur, a.twst_col, R{});
+      if (!(a.dbg & 2))
+        for (int idx = threadIdx.x; idx < G * W; idx += NT) {
+          const int s = idx / G, sp = idx - s * G;
+          cur[s * GP + sp] = cmul(cur[s * GP + sp], Hs[s * GP + sp]);
+        }
+      __syncthreads();
+      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_col, R{});
       const int M = a.Mb - t + 1;
       float2* X = a.X + size_t(p) * a.x_plane + v0;
       const int wv = min(W, a.Hc - v0);
-      for (int idx = threadIdx.x; idx < M * W; idx += kNT) {
+      for (int idx = threadIdx.x; idx < M * W; idx += NT) {
         const int u = idx / W, s = idx - u * W;
         if (s < wv) X[size_t(u) * a.xp + s] = cur[s * GP + u];
       }
@@ -161,13 +181,14 @@ __global__ void __launch_bounds__(kNT) k_cols_filter_ct(DeblurArgs a, int planes
 
 // ------------------------------------------------- pass C (rows c2r + crop)
 template <class P>
-__global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int planes) {
+  constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, H = L + 1, HP = (L + 2) & ~1, TILE = RPC * HP;
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, HP, 1, kNT, false>;
+  using FFT = FftIP<L, RPC, HP, 1, NT, false>;
   extern __shared__ __align__(16) float2 sm[];
-  short* pos = reinterpret_cast<short*>(sm + 2 * TILE);  // slot of z[n] after the DIF
-  for (int i = threadIdx.x; i < L; i += kNT) pos[i] = short(Pos<R>::get(i));
+  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // slot of z[n] after the DIF
+  for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
   auto rows_of = [&](int p) {
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int plane
 #pragma unroll
     for (int s = 0; s < RPC; ++s) {
       const bool ok = r0 + s < M;
-      for (int c = threadIdx.x; c < HP / 2; c += kNT) {
+      for (int c = threadIdx.x; c < HP / 2; c += NT) {
         const int bytes = ok ? min(max((H - 2 * c) * 8, 0), 16) : 0;
         cp_async16(dst + s * HP + 2 * c, bytes ? Y + size_t(s) * a.xp + 2 * c : a.X, bytes);
       }
@@ -191,9 +212,9 @@ __global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int plane
   if (tile < total) issue(tile, sm);
   cp_async_commit();
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
-    float2* cur = sm + (it & 1) * TILE;
+    float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int next = tile + gridDim.x;
-    if (next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+    if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -206,7 +227,7 @@ __global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int plane
 #pragma unroll
       for (int s = 0; s < RPC; ++s) {
         float2* row = cur + s * HP;
-        for (int k = threadIdx.x; k < NP; k += kNT) {
+        for (int k = threadIdx.x; k < NP; k += NT) {
           const float2 A = row[k], B = row[L - k];
           const float2 e1 = cadd(A, cconj(B));
           const float2 o1 = cmul(csub(A, cconj(B)), cconj(__ldg(&a.tw_post[k])));
@@ -217,17 +238,17 @@ __global__ void __launch_bounds__(kNT) k_rows_inverse_ct(DeblurArgs a, int plane
         }
       }
       __syncthreads();
-      FFT::template dif<true>(cur, a.twst_row, R{});  // natural -> slot order
+      if (!(a.dbg & 1)) FFT::template dif<true>(cur, a.twst_row, R{});  // natural -> slot order
       const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
       float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
       if (a.out_vec2 && N % 2 == 0) {
         const int h = N / 2;
         for (int s = 0; s < nrows; ++s)
-          for (int n = threadIdx.x; n < h; n += kNT)
+          for (int n = threadIdx.x; n < h; n += NT)
             __stcs(reinterpret_cast<float2*>(dst + size_t(s) * a.out_ld) + n, cur[s * HP + pos[n]]);
       } else {
         for (int s = 0; s < nrows; ++s)
-          for (int n = threadIdx.x; n < N; n += kNT) {
+          for (int n = threadIdx.x; n < N; n += NT) {
             const float2 z = cur[s * HP + pos[n >> 1]];
             __stcs(dst + size_t(s) * a.out_ld + n, (n & 1) ? z.y : z.x);
           }
@@ -298,9 +319,9 @@ cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s
 
 // --------------------------------------------------------------- dispatch
 template <class K>
-int persistent_grid(K kernel, size_t smem, int total, int sms) {
+int persistent_grid(K kernel, int nt, size_t smem, int total, int sms) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kNT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
   per_sm = per_sm < 1 ? 1 : per_sm;
   const int g = sms * per_sm;
   return total < g ? total : g;
@@ -308,62 +329,69 @@ int persistent_grid(K kernel, size_t smem, int total, int sms) {
 
 template <class P>
 void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
-  const size_t smA = 2 * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
-  const size_t smC = 2 * size_t(P::RPC) * ((P::L + 2) & ~1) * sizeof(float2) + P::L * sizeof(short);
+  constexpr int NB = P::PIPE ? 2 : 1;
+  const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
+  const size_t smC = NB * size_t(P::RPC) * ((P::L + 2) & ~1) * sizeof(float2) + P::L * sizeof(short);
   static int gA = 0, gC = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_rows_forward_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
     cudaFuncSetAttribute(k_rows_inverse_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
-    gA = persistent_grid(k_rows_forward_ct<P>, smA, 1 << 30, sms);
-    gC = persistent_grid(k_rows_inverse_ct<P>, smC, 1 << 30, sms);
+    gA = P::PIPE ? persistent_grid(k_rows_forward_ct<P>, P::NT, smA, 1 << 30, sms) : (1 << 30);
+    gC = P::PIPE ? persistent_grid(k_rows_inverse_ct<P>, P::NT, smC, 1 << 30, sms) : (1 << 30);
   }
   const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
   if (inverse)
-    k_rows_inverse_ct<P><<<total < gC ? total : gC, kNT, smC, s>>>(a, planes);
+    k_rows_inverse_ct<P><<<total < gC ? total : gC, P::NT, smC, s>>>(a, planes);
   else
-    k_rows_forward_ct<P><<<total < gA ? total : gA, kNT, smA, s>>>(a, planes);
+    k_rows_forward_ct<P><<<total < gA ? total : gA, P::NT, smA, s>>>(a, planes);
 }
 
 template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
   constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
-  const size_t sm = 2 * size_t(GP) * P::W * sizeof(float2) + P::G * sizeof(short);
+  const size_t sm = ((P::PIPE ? 2 : 1) + 1) * size_t(GP) * P::W * sizeof(float2) + P::G * sizeof(short);
   static int g = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    g = persistent_grid(k_cols_filter_ct<P>, sm, 1 << 30, sms);
+    g = P::PIPE ? persistent_grid(k_cols_filter_ct<P>, P::NT, sm, 1 << 30, sms) : (1 << 30);
   }
   const int total = planes * ((a.Hc + P::W - 1) / P::W);
-  k_cols_filter_ct<P><<<total < g ? total : g, kNT, sm, s>>>(a, planes);
+  k_cols_filter_ct<P><<<total < g ? total : g, P::NT, sm, s>>>(a, planes);
 }
 
-using Row972 = RowPlan<972, 4, Radices<4, 9, 9, 3>>;     // 1080p: Gc = 1944
-using Row1944 = RowPlan<1944, 2, Radices<8, 9, 9, 3>>;   // 4K: Gc = 3888
-using Row324 = RowPlan<324, 8, Radices<4, 9, 9>>;        // 640x480: Gc = 648
-using Row135 = RowPlan<135, 8, Radices<9, 3, 5>>;        // 256x256: Gc = 270
-using Col1120 = ColPlan<1120, 4, Radices<8, 4, 5, 7>>;   // 1080p: Gr = 1120
-using Col2187 = ColPlan<2187, 2, Radices<9, 9, 9, 3>>;   // 4K: Gr = 2187
-using Col490 = ColPlan<490, 8, Radices<2, 5, 7, 7>>;     // 640x480: Gr = 490
-using Col270 = ColPlan<270, 8, Radices<2, 9, 3, 5>>;     // 256x256: Gr = 270
+// Radix plans in DIT order; the first (contiguous-butterfly) radix is odd so its strided
+// shared-memory accesses are bank-conflict free. Large radices run in registers.
+using Row972 = RowPlan<972, 4, Radices<27, 36>, 160>;      // 1080p: Gc = 1944
+using Row972b = RowPlan<972, 2, Radices<27, 36>, 96, false>;
+using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false>;
+using Row1944 = RowPlan<1944, 2, Radices<27, 8, 9>, 256>;  // 4K: Gc = 3888
+using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
+using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
+using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160>;    // 1080p: Gr = 1120
+using Col1120b = ColPlan<1120, 2, Radices<35, 32>, 96, false>;
+using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false>;
+using Col2187 = ColPlan<2187, 2, Radices<27, 9, 9>, 256>;  // 4K: Gr = 2187
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 288>;      // 640x480: Gr = 490
+using Col270 = ColPlan<270, 8, Radices<27, 10>, 224>;      // 256x256: Gr = 270
 
 // Radix plans of the specialisations above (host mirror; DIT stage order).
 bool ct_radices(int n, bool column, std::vector<int>& r) {
   if (column) {
     switch (n) {
-      case 1120: r = {8, 4, 5, 7}; return true;
-      case 2187: r = {9, 9, 9, 3}; return true;
-      case 490: r = {2, 5, 7, 7}; return true;
-      case 270: r = {2, 9, 3, 5}; return true;
+      case 1120: r = {35, 32}; return true;
+      case 2187: r = {27, 9, 9}; return true;
+      case 490: r = {35, 14}; return true;
+      case 270: r = {27, 10}; return true;
     }
     return false;
   }
   switch (n) {
-    case 972: r = {4, 9, 9, 3}; return true;
-    case 1944: r = {8, 9, 9, 3}; return true;
-    case 324: r = {4, 9, 9}; return true;
-    case 135: r = {9, 3, 5}; return true;
+    case 972: r = {27, 36}; return true;
+    case 1944: r = {27, 8, 9}; return true;
+    case 324: r = {27, 12}; return true;
+    case 135: r = {27, 5}; return true;
   }
   return false;
 }
@@ -381,7 +409,11 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
   if (pass == 1) {
     if (!a.H || !a.twst_col) return false;
     switch (a.Gr) {
-      case 1120: launch_cols<Col1120>(a, planes, s); return true;
+      case 1120:
+        if (a.variant == 1) launch_cols<Col1120b>(a, planes, s);
+        else if (a.variant == 2) launch_cols<Col1120c>(a, planes, s);
+        else launch_cols<Col1120>(a, planes, s);
+        return true;
       case 2187: launch_cols<Col2187>(a, planes, s); return true;
       case 490: launch_cols<Col490>(a, planes, s); return true;
       case 270: launch_cols<Col270>(a, planes, s); return true;
@@ -391,7 +423,11 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
   if (!a.twst_row) return false;
   const bool inv = pass == 2;
   switch (a.Gc / 2) {
-    case 972: launch_rows<Row972>(a, planes, inv, s); return true;
+    case 972:
+      if (a.variant == 1) launch_rows<Row972b>(a, planes, inv, s);
+      else if (a.variant == 2) launch_rows<Row972c>(a, planes, inv, s);
+      else launch_rows<Row972>(a, planes, inv, s);
+      return true;
     case 1944: launch_rows<Row1944>(a, planes, inv, s); return true;
     case 324: launch_rows<Row324>(a, planes, inv, s); return true;
     case 135: launch_rows<Row135>(a, planes, inv, s); return true;

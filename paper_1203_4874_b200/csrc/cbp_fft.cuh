@@ -8,6 +8,7 @@
 #pragma once
 
 #include "cbp_common.cuh"
+#include "cbp_roots.cuh"
 
 namespace cbp_dev {
 
@@ -121,9 +122,54 @@ __device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2&
   v3 = csub(b, jd);
 }
 
+// smallest factor used to split a composite radix R = A * B in registers
+template <int R>
+struct Split {
+  static constexpr int A = (R % 9 == 0 && R != 9) ? 9 : (R % 8 == 0 && R != 8) ? 8 : (R % 4 == 0 && R != 4) ? 4
+                         : (R % 7 == 0 && R != 7) ? 7 : (R % 5 == 0 && R != 5) ? 5 : (R % 3 == 0 && R != 3) ? 3
+                         : (R % 2 == 0 && R != 2) ? 2 : R;
+  static constexpr int B = R / A;
+};
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft(float2* v);
+
+// Composite in-register DFT, R = A*B (four-step): A-point DFTs of the B strided
+// subsequences, twiddles W_R^{b*ka} (compile-time constants, cbp_roots.cuh), then B-point
+// DFTs; output in natural order.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_composite(float2* v) {
+  constexpr int A = Split<R>::A, B = Split<R>::B;
+  float2 z[B][A];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int a = 0; a < A; ++a) z[b][a] = v[b + B * a];
+#pragma unroll
+  for (int b = 0; b < B; ++b) dft<A, INV>(z[b]);
+#pragma unroll
+  for (int b = 1; b < B; ++b)
+#pragma unroll
+    for (int ka = 1; ka < A; ++ka) {
+      const int m = (b * ka) % R;
+      const float2 w = make_float2(Root<R>::re(m), INV ? -Root<R>::im(m) : Root<R>::im(m));
+      z[b][ka] = cmul(z[b][ka], w);
+    }
+#pragma unroll
+  for (int ka = 0; ka < A; ++ka) {
+    float2 t[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) t[b] = z[b][ka];
+    dft<B, INV>(t);
+#pragma unroll
+    for (int kb = 0; kb < B; ++kb) v[ka + A * kb] = t[kb];
+  }
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void dft(float2* v) {
-  if constexpr (R == 2) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
     float2 a = v[0], b = v[1];
     v[0] = cadd(a, b);
     v[1] = csub(a, b);
@@ -154,8 +200,10 @@ __device__ __forceinline__ void dft(float2* v) {
     v[6] = csub(e2, t2);
     v[3] = cadd(e3, t3);
     v[7] = csub(e3, t3);
-  } else {
+  } else if constexpr (R == 3 || R == 5 || R == 7 || R == 9) {
     dft_odd<R, INV>(v);
+  } else {
+    dft_composite<R, INV>(v);
   }
 }
 

@@ -194,7 +194,7 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
 // -------------------------------------------------- kernel degree estimation
 // One CTA per (size s, axis, frame): s x s leading Bezout block of the DC slices
 // (poly.cpp:66-79), then sigma_min / sigma_max by one-sided Jacobi (poly.cpp:81-91).
-__global__ void __launch_bounds__(256) k_width_blocks(RecoverArgs a) {
+__global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
   extern __shared__ double2 shz[];
   __shared__ int flag;
   __shared__ double sv[CBP_MAX_WIDTH + 1];
@@ -295,7 +295,7 @@ cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     cfg = true;
   }
-  k_width_blocks<<<g, 256, sm, s>>>(a);
+  k_width_blocks<<<g, 512, sm, s>>>(a);
   k_width_pick<<<a.batch, 128, 0, s>>>(a);
   return cudaGetLastError();
 }
@@ -425,7 +425,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
     sm.G[j * n + k] = v;
   }
   __syncthreads();
-  herm_jacobi(sm.G, n, sm.V, n, n, sm.js);
+  herm_jacobi_cta(sm.G, n, sm.V, n, n, sm.js);
   __shared__ int kmin_s, k2_s;
   __shared__ double lmax_s, lmin_s;
   if (tid == 0) {
@@ -739,7 +739,7 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
     s.G[idx] = v;
   }
   __syncthreads();
-  herm_jacobi(s.G, n, s.V, n, n, s.js);
+  herm_jacobi_cta(s.G, n, s.V, n, n, s.js);
   __shared__ int kmin_s;
   __shared__ double lmax_s, lmin_s;
   if (threadIdx.x == 0) {
@@ -1097,13 +1097,13 @@ struct ConvResidArgs {
   int ntiles;
 };
 
-__device__ __forceinline__ double conv_at(const float* tile, int tw, const double* K, int t, int li, int lj) {
+__device__ __forceinline__ double conv_at(const double* tile, int tw, const double* K, int t, int li, int lj) {
   // out(i,j) = sum_{a,b} K[a][b] X[i-a][j-b]; tile holds X rows [i0-t+1, i0+VT_R), cols [j0-t+1, ...)
   double acc = 0.0;
   for (int a2 = 0; a2 < t; ++a2) {
-    const float* row = tile + (li + t - 1 - a2) * tw + (lj + t - 1);
+    const double* row = tile + (li + t - 1 - a2) * tw + (lj + t - 1);
     const double* kr = K + a2 * t;
-    for (int b2 = 0; b2 < t; ++b2) acc = fma(kr[b2], double(row[-b2]), acc);
+    for (int b2 = 0; b2 < t; ++b2) acc = fma(kr[b2], row[-b2], acc);
   }
   return acc;
 }
@@ -1132,8 +1132,8 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
   double* kw = shd;                      // t*t
   double* kw2 = kw + t * t;              // t*t (mode 1)
   const int tw = VT_C + t - 1, th = VT_R + t - 1;
-  float* tile = reinterpret_cast<float*>(kw2 + t * t);
-  float* tile2 = tile + th * tw;
+  double* tile = kw2 + t * t;  // converted once to FP64 (F2F throughput is far below DFMA)
+  double* tile2 = tile + th * tw;
   for (int i = threadIdx.x; i < t * t; i += blockDim.x) {
     kw[i] = K[i];
     if (a.mode == 1) kw2[i] = a.K2[i];
@@ -1144,8 +1144,8 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
     const int li = idx / tw, lj = idx - li * tw;
     const int gi = i0 - t + 1 + li, gj = j0 - t + 1 + lj;
     const bool in = gi >= 0 && gi < xr && gj >= 0 && gj < xc;
-    tile[idx] = in ? X[size_t(gi) * a.xld + gj] : 0.0f;
-    if (a.mode == 1) tile2[idx] = in ? Y[size_t(gi) * a.yld + gj] : 0.0f;
+    tile[idx] = in ? double(X[size_t(gi) * a.xld + gj]) : 0.0;
+    if (a.mode == 1) tile2[idx] = in ? double(Y[size_t(gi) * a.yld + gj]) : 0.0;
   }
   __syncthreads();
   double num = 0.0, den = 0.0;
@@ -1177,32 +1177,39 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
   }
 }
 
-// Per frame: fixed-order sum of the tile partials (zeros for tiles that exited early).
-__global__ void k_resid_reduce(const double2* part, int ntiles, int channels, cbp_kernel_slot* slots,
-                               double* out, int batch) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
+// Per frame: fixed-order (deterministic) block reduction of the tile partials.
+__global__ void __launch_bounds__(256) k_resid_reduce(const double2* part, int ntiles, int channels,
+                                                      cbp_kernel_slot* slots, double* out, int batch) {
+  const int b = blockIdx.x;
   if (slots && slots[b].status != 0) return;
   double num = 0.0, den = 0.0;
-  for (int c = 0; c < channels; ++c)
-    for (int i = 0; i < ntiles; ++i) {
-      const double2 v = part[(size_t(b) * channels + c) * ntiles + i];
-      num += v.x;
-      den += v.y;
-    }
+  const int total = channels * ntiles;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const double2 v = part[size_t(b) * total + i];
+    num += v.x;
+    den += v.y;
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  __shared__ double rn[8], rd[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) rn[warp] = num, rd[warp] = den;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  num = den = 0.0;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) num += rn[w], den += rd[w];
   if (!(den > 0.0)) {
-    if (slots) {
+    if (slots)
       slot_fail(slots + b, CBP_DEGENERATE_INPUT, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_ZERO_PUBLIC);
-    } else {
+    else
       out[b] = -1.0;
-    }
     return;
   }
-  const double r = sqrt(num / den);
+  const double res = sqrt(num / den);
   if (slots)
-    slots[b].residual = r;
+    slots[b].residual = res;
   else
-    out[b] = r;
+    out[b] = res;
 }
 
 cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_out, double* part,
@@ -1227,15 +1234,11 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.co = ra.cols;
   dim3 g(ntiles_max, ra.batch * ra.channels);
   const size_t sm = 2 * size_t(ra.t_max) * ra.t_max * sizeof(double) +
-                    2 * size_t(VT_R + ra.t_max - 1) * (VT_C + ra.t_max - 1) * sizeof(float);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cfg = true;
-  }
+                    size_t(VT_R + ra.t_max - 1) * (VT_C + ra.t_max - 1) * sizeof(double);
+  if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
+    return cudaErrorInvalidValue;
   k_conv_resid<<<g, 256, sm, s>>>(a);
-  k_resid_reduce<<<(ra.batch + 127) / 128, 128, 0, s>>>(a.part, ntiles_max, ra.channels, ra.slots, nullptr,
-                                                         ra.batch);
+  k_resid_reduce<<<ra.batch, 256, 0, s>>>(a.part, ntiles_max, ra.channels, ra.slots, nullptr, ra.batch);
   return cudaGetLastError();
 }
 
@@ -1262,14 +1265,11 @@ cudaError_t launch_validate_pair(const float* pub, const float* prv, int channel
   a.part = reinterpret_cast<double2*>(part);
   cudaMemsetAsync(part, 0, sizeof(double2) * size_t(nt) * channels, s);
   dim3 g(nt, channels);
-  const size_t sm = 2 * size_t(t) * t * sizeof(double) + 2 * size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(float);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cfg = true;
-  }
+  const size_t sm = 2 * size_t(t) * t * sizeof(double) + 2 * size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(double);
+  if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
+    return cudaErrorInvalidValue;
   k_conv_resid<<<g, 256, sm, s>>>(a);
-  k_resid_reduce<<<1, 32, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
+  k_resid_reduce<<<1, 256, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
   return cudaGetLastError();
 }
 
