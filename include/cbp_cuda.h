@@ -252,6 +252,12 @@ double cbp_coprimality_check(const double* k1, const double* k2, int t, int tria
 int cbp_generate_coprime_pair(int width, uint64_t seed, int max_retries, double margin_threshold,
                               int trials, double* k1, double* k2, double* margin);
 
+/* ---- device memory helpers (used by the C++ shim, include/cbp/) ---------------- */
+int cbp_device_alloc(cbp_ctx* ctx, size_t bytes, void** dev);
+void cbp_device_free(cbp_ctx* ctx, void* dev);
+int cbp_copy_to_device(cbp_ctx* ctx, void* dev, const void* host, size_t bytes);
+int cbp_copy_to_host(cbp_ctx* ctx, void* host, const void* dev, size_t bytes);
+
 /* ---- instrumentation ----------------------------------------------------------
  * Kernels enqueued by this context so far; optional CUDA-event timing of the three
  * deconvolution passes (A rows forward, B columns + filter, C rows inverse). */

@@ -385,6 +385,26 @@ int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, 
                     static_cast<cudaStream_t>(stream));
 }
 
+int cbp_device_alloc(cbp_ctx* ctx, size_t bytes, void** dev) {
+  if (!ctx || !dev) return CBP_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  return cuda_check(ctx, cudaMalloc(dev, bytes ? bytes : 16), "device allocation");
+}
+
+void cbp_device_free(cbp_ctx* ctx, void* dev) {
+  if (ctx && dev) cudaFree(dev);
+}
+
+int cbp_copy_to_device(cbp_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  return cuda_check(ctx, cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice), "copy to device");
+}
+
+int cbp_copy_to_host(cbp_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  return cuda_check(ctx, cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost), "copy to host");
+}
+
 int cbp_read_slots(cbp_ctx* ctx, const cbp_kernel_slot* slots_dev, int count,
                    cbp_kernel_slot* slots_host, void* stream) {
   if (!ctx) return CBP_INVALID_ARGUMENT;
