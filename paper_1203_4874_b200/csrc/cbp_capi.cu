@@ -76,6 +76,23 @@ const float2* stage_twiddles(cbp_ctx* ctx, int n, bool column) {
   return d;
 }
 
+// slot(u) of the compile-time column plan's DIF output order (null: no plan, natural
+// order); the Wiener table is stored in that order so pass B filters element-wise
+const short* column_slots(cbp_ctx* ctx, int n) {
+  std::vector<int> rad;
+  if (!ct_radices(n, true, rad)) return nullptr;
+  const int key = -(n + (1 << 24));  // distinct from the twiddle keys
+  auto it = ctx->tw.find(key);
+  if (it != ctx->tw.end()) return reinterpret_cast<const short*>(it->second);
+  std::vector<short> h(static_cast<size_t>(n));
+  for (int u = 0; u < n; ++u) h[u] = short(ct_pos(rad, u));
+  float2* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(short) + sizeof(float2)) != cudaSuccess) return nullptr;
+  cudaMemcpy(d, h.data(), h.size() * sizeof(short), cudaMemcpyHostToDevice);
+  ctx->tw[key] = d;
+  return reinterpret_cast<const short*>(d);
+}
+
 const float2* twiddles(cbp_ctx* ctx, int n) {
   auto it = ctx->tw.find(n);
   if (it != ctx->tw.end()) return it->second;
@@ -130,7 +147,9 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.plan_col = make_plan(a.Gr);
   if (a.plan_row.nst < 0 || a.plan_col.nst < 0)
     return set_error(ctx, CBP_UNSUPPORTED, "transform grid is not 2/3/5/7-smooth");
-  a.xp = (a.Hc + 3) & ~3;
+  a.xp = (a.Mb + 3) & ~3;  // XT column pitch
+  a.hp = (a.Gr + 3) & ~3;
+  a.hpos = column_slots(ctx, a.Gr);
   // rows per CTA for passes A/C: keep 2*rpc*L*8 bytes <= 64 KB, at most 8 rows
   int rpc = 8;
   while (rpc > 1 && size_t(2) * rpc * L * sizeof(float2) > 64 * 1024) rpc /= 2;
@@ -156,7 +175,7 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
                size_t out_plane_stride, cudaStream_t stream) {
   // Group whole frames so the half spectrum of a group (written by pass A, read and
   // rewritten by B, read by C) stays resident in the 126 MB L2.
-  const size_t plane_bytes = size_t(a.Mb) * a.xp * sizeof(float2);
+  const size_t plane_bytes = size_t(a.Hc) * a.xp * sizeof(float2);
   const int ch = std::max(a.channels, 1);
   static const size_t budget = [] {
     const char* e = getenv("CBP_L2_BUDGET_MB");
@@ -169,13 +188,13 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   float2* X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * group_planes));
   if (!X) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   a.X = X;
-  a.x_plane = size_t(a.Mb) * a.xp;
+  a.x_plane = size_t(a.Hc) * a.xp;
   a.in_plane = in_plane_stride;
   a.out_plane = out_plane_stride;
   // Wiener filter table(s) H[u][v] for the kernel slot(s) of this batch
   const int nslots = a.slot_per_frame ? std::max(frames, 1) : 1;
   a.s_frame = size_t(a.Hc) * CBP_MAX_WIDTH;
-  a.h_frame = size_t(a.Gr) * a.xp;
+  a.h_frame = size_t(a.Hc) * a.hp;
   a.S = static_cast<double2*>(workspace(ctx, WS_RED + 1, sizeof(double2) * a.s_frame * nslots));
   a.H = static_cast<float2*>(workspace(ctx, WS_RED + 2, sizeof(float2) * a.h_frame * nslots));
   if (!a.S || !a.H) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_rows_forward(DeblurArgs a) {
   // split into the half spectrum X[0..Gc/2] (fft.cpp:242-255 r2c)
   const int H = a.Hc;
   for (int idx = threadIdx.x; idx < nrows * H; idx += blockDim.x) {
-    const int s = idx / H, k = idx - s * H;
+    const int k = idx / nrows, s = idx - k * nrows;  // rows fastest: XT[k][r0 + s]
     float2 x;
     if (a.even) {
       const float2 zk = res[s * lp + (k == L ? 0 : k)];
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) k_rows_forward(DeblurArgs a) {
     } else {
       x = res[s * lp + k];
     }
-    a.X[size_t(p) * a.x_plane + size_t(r0 + s) * a.xp + k] = x;
+    a.X[size_t(p) * a.x_plane + size_t(k) * a.xp + r0 + s] = x;
   }
 }
 
@@ -100,11 +100,11 @@ __global__ void __launch_bounds__(256) k_cols_filter(DeblurArgs a) {
     S[idx] = make_float2(float(re), float(im));
   }
   for (int idx = threadIdx.x; idx < Gr * W; idx += blockDim.x) {
-    const int u = idx / W, s = idx - u * W;
+    const int s = idx / Gr, u = idx - s * Gr;  // column v = v0 + s is contiguous in XT
     const int v = v0 + s;
     float2 x = make_float2(0.f, 0.f);
-    if (u < a.Mb && v < a.Hc) x = X[size_t(u) * a.xp + v];
-    buf0[idx] = x;
+    if (u < a.Mb && v < a.Hc) x = X[size_t(v) * a.xp + u];
+    buf0[u * W + s] = x;
   }
   __syncthreads();
   float2* res = fft_run<false, true>(buf0, buf1, a.plan_col, W, 1, W, a.tw_col);
@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(256) k_cols_filter(DeblurArgs a) {
   __syncthreads();
   res = fft_run<true, true>(res, other, a.plan_col, W, 1, W, a.tw_col);
   for (int idx = threadIdx.x; idx < M * W; idx += blockDim.x) {
-    const int u = idx / W, s = idx - u * W;
+    const int s = idx / M, u = idx - s * M;
     const int v = v0 + s;
-    if (v < a.Hc) X[size_t(u) * a.xp + v] = res[idx];
+    if (v < a.Hc) X[size_t(v) * a.xp + u] = res[u * W + s];
   }
 }
 
@@ -155,20 +155,20 @@ __global__ void __launch_bounds__(256) k_rows_inverse(DeblurArgs a) {
   const int lp = L;
   float2* buf0 = smem;
   float2* buf1 = smem + size_t(rpc) * lp;
-  const float2* Y = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
+  const float2* Y = a.X + size_t(p) * a.x_plane + r0;  // XT[k][r0 + s]
   for (int idx = threadIdx.x; idx < rpc * L; idx += blockDim.x) {
     const int s = idx / L, k = idx - s * L;
     float2 z = make_float2(0.f, 0.f);
     if (s < nrows) {
-      const float2* row = Y + size_t(s) * a.xp;
+      const float2* row = Y + s;  // element k of row r0+s at row[k * xp]
       if (a.even) {  // inverse split (fft.cpp:257-270 c2r)
-        const float2 A = row[k];
-        const float2 B = cconj(row[L - k]);
+        const float2 A = row[size_t(k) * a.xp];
+        const float2 B = cconj(row[size_t(L - k) * a.xp]);
         const float2 e = cadd(A, B);
         const float2 o = cmul(csub(A, B), cconj(__ldg(&a.tw_post[k])));
         z = make_float2(e.x - o.y, e.y + o.x);  // e + i*o
       } else {
-        z = k <= L / 2 ? row[k] : cconj(row[L - k]);
+        z = k <= L / 2 ? row[size_t(k) * a.xp] : cconj(row[size_t(L - k) * a.xp]);
       }
     }
     buf0[s * lp + k] = z;

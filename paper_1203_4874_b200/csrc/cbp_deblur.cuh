@@ -14,9 +14,9 @@ struct DeblurArgs {
   float* out;  // latent planes
   size_t out_plane;
   int out_ld;
-  float2* X;  // half-spectrum workspace: plane p at X + p*x_plane, rows of xp
+  float2* X;  // transposed half spectrum XT[v][u]: plane p at X + p*x_plane, column v at v*xp
   size_t x_plane;
-  int xp;
+  int xp;     // pitch of one spectrum column (>= Mb, multiple of 4)
   int Mb, Nb;       // blurred plane extent
   int Gr, Gc, Hc;   // grid and half-spectrum width Gc/2+1
   int even;         // Gc even: half-length complex row transform
@@ -39,8 +39,10 @@ struct DeblurArgs {
   const float2* twst_col; // per-stage twiddles of the specialised column plan (or null)
   double2* S;             // per-slot column kernel transforms S[v][a] (k_wiener_s)
   size_t s_frame;         // S stride per slot
-  float2* H;              // per-slot Wiener filter H[u][v] (pitch xp), scaled by 1/(Gr*Gc)
+  float2* H;              // per-slot Wiener filter HT[v][slot(u)] (pitch hp), scaled by 1/(Gr*Gc)
   size_t h_frame;         // H stride per slot
+  int hp;                 // H column pitch (>= Gr, multiple of 4)
+  const short* hpos;      // slot(u) of the column plan's DIF output, or null (natural order)
 };
 
 int deblur_col_width(int Gr, int t_max);
@@ -50,6 +52,7 @@ cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaSt
 bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream_t stream);
 bool deblur_has_ct(int Gr, int Gc, int pass);
 bool ct_radices(int n, bool column, std::vector<int>& r);
+int ct_pos(const std::vector<int>& rad, int n);
 // Wiener filter tables of `frames` slots: S (column transforms) then H (cbp_deblur_ct.cu)
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s);
 

@@ -37,8 +37,14 @@ __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a
   return a.slot + (a.slot_per_frame ? p / a.channels : 0);
 }
 
+// The half spectrum lives transposed in HBM/L2: XT[v][u] (v < Hc columns, u < Mb rows,
+// pitch xp = Mb rounded to 4), so a column strip is contiguous for pass B and a group of
+// 4 rows is one 32-byte sector per frequency for passes A and C.
+
 // ------------------------------------------------------------ pass A (rows r2c)
-// Row s of a tile holds z[m] = (x[2m], x[2m+1]); forward DIF leaves Z[k] in slot pos(k).
+// Row s of a tile holds z[m] = (x[2m], x[2m+1]); the forward DIF leaves Z[k] in slot pos(k);
+// the r2c split handles the pair (k, L-k) in one thread: X[k] = e + W^k o,
+// X[L-k] = conj(e - W^k o), e = (Z[k] + conj Z[L-k])/2, o = -i (Z[k] - conj Z[L-k])/2.
 template <class P>
 __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
@@ -46,7 +52,7 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
   using R = typename P::R;
   using FFT = FftIP<L, RPC, L, 1, NT, false>;
   extern __shared__ __align__(16) float2 sm[];
-  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // slot of Z[k] after the DIF
+  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);
   for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
@@ -58,15 +64,17 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
     for (int s = 0; s < RPC; ++s) {
       const bool ok = r0 + s < a.Mb;
       const float* row = src + size_t(s) * a.in_ld;
+      float2* d = dst + s * L;
       if (v16) {
+        const int full = ok ? a.Nb / 4 : 0;  // whole 16-byte chunks inside the row
         for (int c = threadIdx.x; c < L / 2; c += NT) {
-          const int bytes = ok ? min(max((a.Nb - 4 * c) * 4, 0), 16) : 0;
-          cp_async16(dst + s * L + 2 * c, bytes ? row + 4 * c : a.in, bytes);
+          int bytes = c < full ? 16 : (ok ? min(max((a.Nb - 4 * c) * 4, 0), 16) : 0);
+          cp_async16(d + 2 * c, bytes ? row + 4 * c : a.in, bytes);
         }
       } else {
         for (int m = threadIdx.x; m < L; m += NT) {
           const int bytes = ok ? min(max((a.Nb - 2 * m) * 4, 0), 8) : 0;
-          cp_async8(dst + s * L + m, bytes ? row + 2 * m : a.in, bytes);
+          cp_async8(d + m, bytes ? row + 2 * m : a.in, bytes);
         }
       }
     }
@@ -83,19 +91,20 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
     __syncthreads();
     if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
-    float2* X = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
-#pragma unroll
-    for (int s = 0; s < RPC; ++s) {
-      if (r0 + s >= a.Mb) break;
+    float2* XT = a.X + size_t(p) * a.x_plane + r0;
+    constexpr int NPAIR = L / 2 + 1;
+    for (int idx = threadIdx.x; idx < NPAIR * RPC; idx += NT) {
+      const int k = idx / RPC, s = idx - k * RPC;
+      if (r0 + s >= a.Mb) continue;
       const float2* z = cur + s * L;
-      for (int k = threadIdx.x; k <= L; k += NT) {
-        const float2 zk = z[pos[k == L ? 0 : k]];
-        const float2 zc = cconj(z[pos[k == 0 ? 0 : L - k]]);
-        const float2 e = cscale(cadd(zk, zc), 0.5f);
-        const float2 d = csub(zk, zc);
-        const float2 o = make_float2(0.5f * d.y, -0.5f * d.x);  // -i/2 * d
-        X[size_t(s) * a.xp + k] = cadd(e, cmul(__ldg(&a.tw_post[k]), o));
-      }
+      const float2 zk = z[pos[k]];
+      const float2 zc = cconj(z[pos[k == 0 ? 0 : L - k]]);
+      const float2 e = cscale(cadd(zk, zc), 0.5f);
+      const float2 d = csub(zk, zc);
+      const float2 o = make_float2(0.5f * d.y, -0.5f * d.x);  // -i/2 * d
+      const float2 wo = cmul(__ldg(&a.tw_post[k]), o);
+      XT[size_t(k) * a.xp + s] = cadd(e, wo);
+      if (L - k != k) XT[size_t(L - k) * a.xp + s] = cconj(csub(e, wo));
     }
     __syncthreads();
   }
@@ -103,32 +112,31 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
 }
 
 // ----------------------------------------------- pass B (columns + Wiener filter)
-// The tile holds W columns as contiguous sequences (layout [column][row], pitch GP with
-// GP = 4 mod 16 so 4 columns x 4 rows hit distinct banks). Forward DIF leaves spectrum
-// row u in slot pos(u); the filter H (precomputed per kernel slot by k_wiener_h) is
-// applied there; the inverse DIT returns natural rows.
+// Column v of XT is contiguous: 16-byte copies into a [column][row] tile; the forward DIF
+// leaves spectrum row u in slot pos(u), where the filter table (k_wiener_h) already stores
+// H(u, v), so the filter is an element-wise product; the inverse DIT restores natural rows.
 template <class P>
 __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
-  constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;
+  constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;  // padded: sequences on distinct banks
   constexpr int NBUF = P::PIPE ? 2 : 1;
   using R = typename P::R;
   using FFT = FftIP<G, W, GP, 1, NT, false>;
   extern __shared__ __align__(16) float2 sm[];
-  float2* Hs = sm + NBUF * TILE;                           // filter strip, slot order
-  short* pos = reinterpret_cast<short*>(Hs + TILE);        // spectrum row u -> slot after the DIF
-  for (int i = threadIdx.x; i < G; i += NT) pos[i] = short(Pos<R>::get(i));
-  __syncthreads();
+  float2* Hs = sm + NBUF * TILE;
   const int strips = (a.Hc + W - 1) / W;
   const int total = planes * strips;
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / strips, v0 = (tile - p * strips) * W;
-    const float2* X = a.X + size_t(p) * a.x_plane + v0;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < G * W; idx += NT) {
-      const int u = idx / W, s = idx - u * W;
-      const int bytes = (u < a.Mb && v0 + s < a.Hc) ? 8 : 0;
-      cp_async8(dst + s * GP + u, bytes ? X + size_t(u) * a.xp + s : a.X, bytes);
+    const float2* XT = a.X + size_t(p) * a.x_plane;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+      const bool ok = v0 + s < a.Hc;
+      const float2* col = XT + size_t(v0 + s) * a.xp;
+      for (int c = threadIdx.x; c < GP / 2; c += NT) {
+        const int bytes = ok ? min(max((a.Mb - 2 * c) * 8, 0), 16) : 0;
+        cp_async16(dst + s * GP + 2 * c, bytes ? col + 2 * c : a.X, bytes);
+      }
     }
   };
   int tile = blockIdx.x;
@@ -142,12 +150,16 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
     const int status = slot->status;
     cp_async_wait<0>();
     __syncthreads();
-    // filter strip H[u][v0+s] -> Hs[s][pos(u)], in flight during the forward transform
-    if (status == 0) {
-      const float2* Ht = a.H + size_t(f) * a.h_frame + v0;
-      for (int idx = threadIdx.x; idx < G * W; idx += NT) {
-        const int u = idx / W, s = idx - u * W;
-        cp_async8(Hs + s * GP + pos[u], Ht + size_t(u) * a.xp + s, 8);
+    if (status == 0) {  // filter strip in flight during the forward transform
+      const float2* Ht = a.H + size_t(f) * a.h_frame;
+#pragma unroll
+      for (int s = 0; s < W; ++s) {
+        const bool ok = v0 + s < a.Hc;
+        const float2* hcol = Ht + size_t(v0 + s) * a.hp;
+        for (int c = threadIdx.x; c < GP / 2; c += NT) {
+          const int bytes = ok ? min(max((G - 2 * c) * 8, 0), 16) : 0;
+          cp_async16(Hs + s * GP + 2 * c, bytes ? hcol + 2 * c : a.H, bytes);
+        }
       }
     }
     cp_async_commit();
@@ -157,21 +169,28 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
     if (status == 0) {  // uniform over the CTA
       const int t = slot->width;
       if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
-      cp_async_wait<1>();  // the filter strip (the next tile's copies may still fly)
+      cp_async_wait<1>();
       __syncthreads();
-      if (!(a.dbg & 2))
-        for (int idx = threadIdx.x; idx < G * W; idx += NT) {
-          const int s = idx / G, sp = idx - s * G;
-          cur[s * GP + sp] = cmul(cur[s * GP + sp], Hs[s * GP + sp]);
+      if (!(a.dbg & 2)) {
+        float4* c4 = reinterpret_cast<float4*>(cur);
+        const float4* h4 = reinterpret_cast<const float4*>(Hs);
+        for (int i = threadIdx.x; i < TILE / 2; i += NT) {
+          const float4 x = c4[i], h = h4[i];
+          c4[i] = make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
+                              x.z * h.w + x.w * h.z);
         }
+      }
       __syncthreads();
       if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_col, R{});
       const int M = a.Mb - t + 1;
-      float2* X = a.X + size_t(p) * a.x_plane + v0;
-      const int wv = min(W, a.Hc - v0);
-      for (int idx = threadIdx.x; idx < M * W; idx += NT) {
-        const int u = idx / W, s = idx - u * W;
-        if (s < wv) X[size_t(u) * a.xp + s] = cur[s * GP + u];
+      float2* XT = a.X + size_t(p) * a.x_plane;
+#pragma unroll
+      for (int s = 0; s < W; ++s) {
+        if (v0 + s >= a.Hc) break;
+        float2* col = XT + size_t(v0 + s) * a.xp;
+        const float4* src = reinterpret_cast<const float4*>(cur + s * GP);
+        for (int c = threadIdx.x; c < M / 2; c += NT) reinterpret_cast<float4*>(col)[c] = src[c];
+        if ((M & 1) && threadIdx.x == 0) col[M - 1] = cur[s * GP + M - 1];
       }
     }
     __syncthreads();
@@ -180,12 +199,15 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
 }
 
 // ------------------------------------------------- pass C (rows c2r + crop)
+// Tile layout [k][s] (RPC rows interleaved): one frequency of RPC consecutive rows is one
+// 32-byte chunk of XT. The transform runs with consecutive threads on consecutive rows.
 template <class P>
 __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
-  constexpr int L = P::L, RPC = P::RPC, H = L + 1, HP = (L + 2) & ~1, TILE = RPC * HP;
+  constexpr int L = P::L, RPC = P::RPC, H = L + 1, TILE = ((H * RPC + 3) & ~3);
+  static_assert(RPC % 2 == 0, "16-byte copies carry two rows");
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, HP, 1, NT, false>;
+  using FFT = FftIP<L, RPC, 1, RPC, NT, true>;
   extern __shared__ __align__(16) float2 sm[];
   short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // slot of z[n] after the DIF
   for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
@@ -198,14 +220,13 @@ __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int pla
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     const int M = rows_of(p);
-    const float2* Y = a.X + size_t(p) * a.x_plane + size_t(r0) * a.xp;
-#pragma unroll
-    for (int s = 0; s < RPC; ++s) {
-      const bool ok = r0 + s < M;
-      for (int c = threadIdx.x; c < HP / 2; c += NT) {
-        const int bytes = ok ? min(max((H - 2 * c) * 8, 0), 16) : 0;
-        cp_async16(dst + s * HP + 2 * c, bytes ? Y + size_t(s) * a.xp + 2 * c : a.X, bytes);
-      }
+    const float2* XT = a.X + size_t(p) * a.x_plane + r0;
+    constexpr int HALF = RPC / 2;
+    for (int idx = threadIdx.x; idx < H * HALF; idx += NT) {
+      const int k = idx / HALF, j = idx - k * HALF;
+      const int rows_left = M - r0 - 2 * j;
+      const int bytes = rows_left >= 2 ? 16 : (rows_left == 1 ? 8 : 0);
+      cp_async16(dst + k * RPC + 2 * j, bytes ? XT + size_t(k) * a.xp + 2 * j : a.X, bytes);
     }
   };
   int tile = blockIdx.x;
@@ -222,19 +243,20 @@ __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int pla
     const int M = rows_of(p);
     const int nrows = min(RPC, M - r0);
     if (nrows > 0) {
-      // inverse split in place, one thread per pair (k, L-k) (fft.cpp:257-270 c2r)
+      // inverse split in place, one thread per pair (k, L-k) and row (fft.cpp:257-270 c2r)
       constexpr int NP = L / 2 + 1;
-#pragma unroll
-      for (int s = 0; s < RPC; ++s) {
-        float2* row = cur + s * HP;
-        for (int k = threadIdx.x; k < NP; k += NT) {
-          const float2 A = row[k], B = row[L - k];
-          const float2 e1 = cadd(A, cconj(B));
-          const float2 o1 = cmul(csub(A, cconj(B)), cconj(__ldg(&a.tw_post[k])));
+      for (int idx = threadIdx.x; idx < NP * RPC; idx += NT) {
+        const int k = idx / RPC, s = idx - k * RPC;
+        const float2 A = cur[k * RPC + s], B = cur[(L - k) * RPC + s];
+        const float2 w = cconj(__ldg(&a.tw_post[k]));
+        const float2 e1 = cadd(A, cconj(B));
+        const float2 o1 = cmul(csub(A, cconj(B)), w);
+        cur[k * RPC + s] = make_float2(e1.x - o1.y, e1.y + o1.x);
+        if (k != 0 && 2 * k != L) {
+          // conj(tw_post[L-k]) = -tw_post[k]: z[L-k] = (B + conj A) + i (B - conj A)(-conj w)
           const float2 e2 = cadd(B, cconj(A));
-          const float2 o2 = cmul(csub(B, cconj(A)), cconj(__ldg(&a.tw_post[L - k])));
-          row[k] = make_float2(e1.x - o1.y, e1.y + o1.x);
-          if (k != 0 && 2 * k != L) row[L - k] = make_float2(e2.x - o2.y, e2.y + o2.x);
+          const float2 o2 = cmul(csub(B, cconj(A)), make_float2(-w.x, w.y));
+          cur[(L - k) * RPC + s] = make_float2(e2.x - o2.y, e2.y + o2.x);
         }
       }
       __syncthreads();
@@ -245,11 +267,11 @@ __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int pla
         const int h = N / 2;
         for (int s = 0; s < nrows; ++s)
           for (int n = threadIdx.x; n < h; n += NT)
-            __stcs(reinterpret_cast<float2*>(dst + size_t(s) * a.out_ld) + n, cur[s * HP + pos[n]]);
+            __stcs(reinterpret_cast<float2*>(dst + size_t(s) * a.out_ld) + n, cur[pos[n] * RPC + s]);
       } else {
         for (int s = 0; s < nrows; ++s)
           for (int n = threadIdx.x; n < N; n += NT) {
-            const float2 z = cur[s * HP + pos[n >> 1]];
+            const float2 z = cur[pos[n >> 1] * RPC + s];
             __stcs(dst + size_t(s) * a.out_ld + n, (n & 1) ? z.y : z.x);
           }
       }
@@ -281,22 +303,23 @@ __global__ void k_wiener_s(DeblurArgs a, int frames) {
 }
 
 // H[f][u][v] = conj(K)/(|K|^2 + eps) / (Gr*Gc), K(u,v) = sum_a S[v][a] exp(-2 pi i u a / Gr)
-// in FP64 (decoder.cpp:209-211, fft.cpp:268); grid (ceil(Hc/32), ceil(Gr/8), frames).
+// in FP64 (decoder.cpp:209-211, fft.cpp:268); grid (ceil(Gr/32), ceil(Hc/8), frames):
+// lanes run along u so each warp writes within one table column.
 __global__ void __launch_bounds__(256) k_wiener_h(DeblurArgs a, int frames) {
-  __shared__ double2 Ss[32 * CBP_MAX_WIDTH];
+  __shared__ double2 Ss[8 * CBP_MAX_WIDTH];
   const int f = blockIdx.z;
   const cbp_kernel_slot* slot = a.slot + f;
   if (slot->status != 0) return;
   const int t = slot->width;
-  const int v0 = blockIdx.x * 32;
+  const int v0 = blockIdx.y * 8;
   const double2* S = a.S + size_t(f) * a.s_frame;
-  for (int i = threadIdx.x; i < 32 * t; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 8 * t; i += blockDim.x) {
     const int vv = i / t, ai = i - vv * t;
     Ss[i] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int vv = threadIdx.x & 31, v = v0 + vv;
-  const int u = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int vv = threadIdx.x >> 5, v = v0 + vv;
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   if (v >= a.Hc || u >= a.Gr) return;
   double2 acc = make_double2(0.0, 0.0);
   for (int ai = 0; ai < t; ++ai) {
@@ -305,14 +328,17 @@ __global__ void __launch_bounds__(256) k_wiener_h(DeblurArgs a, int frames) {
   }
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
   const double den = (acc.x * acc.x + acc.y * acc.y + slot->epsilon);
-  a.H[size_t(f) * a.h_frame + size_t(u) * a.xp + v] =
+  // transposed table HT[v][slot(u)]: slot(u) = pos(u) of the column plan (a.hpos), so pass B
+  // multiplies element-wise in its DIF output order
+  const int su = a.hpos ? int(a.hpos[u]) : u;
+  a.H[size_t(f) * a.h_frame + size_t(v) * a.hp + su] =
       make_float2(float(acc.x * sc / den), float(-acc.y * sc / den));
 }
 
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s) {
   dim3 g1((a.Hc * CBP_MAX_WIDTH + 255) / 256, frames);
   k_wiener_s<<<g1, 256, 0, s>>>(a, frames);
-  dim3 g2((a.Hc + 31) / 32, (a.Gr + 7) / 8, frames);
+  dim3 g2((a.Gr + 31) / 32, (a.Hc + 7) / 8, frames);
   k_wiener_h<<<g2, 256, 0, s>>>(a, frames);
   return cudaGetLastError();
 }
@@ -331,7 +357,7 @@ template <class P>
 void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
   constexpr int NB = P::PIPE ? 2 : 1;
   const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
-  const size_t smC = NB * size_t(P::RPC) * ((P::L + 2) & ~1) * sizeof(float2) + P::L * sizeof(short);
+  const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 3) & ~3) * sizeof(float2) + P::L * sizeof(short);
   static int gA = 0, gC = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -350,7 +376,7 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
 template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
   constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
-  const size_t sm = ((P::PIPE ? 2 : 1) + 1) * size_t(GP) * P::W * sizeof(float2) + P::G * sizeof(short);
+  const size_t sm = ((P::PIPE ? 2 : 1) + 1) * size_t(GP) * P::W * sizeof(float2);
   static int g = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -394,6 +420,19 @@ bool ct_radices(int n, bool column, std::vector<int>& r) {
     case 135: r = {27, 5}; return true;
   }
   return false;
+}
+
+// digit-reversal slot of element n for a radix list (host mirror of Pos<>::get)
+int ct_pos(const std::vector<int>& rad, int n) {
+  int pos = 0, N = 1;
+  for (int r : rad) N *= r;
+  for (size_t m = rad.size(); m-- > 0;) {  // Pos<R_1..R_m>: last radix first
+    const int r = rad[m];
+    N /= r;
+    pos += (n % r) * N;
+    n /= r;
+  }
+  return pos;
 }
 
 bool deblur_has_ct(int Gr, int Gc, int pass) {
