@@ -258,6 +258,13 @@ void cbp_device_free(cbp_ctx* ctx, void* dev);
 int cbp_copy_to_device(cbp_ctx* ctx, void* dev, const void* host, size_t bytes);
 int cbp_copy_to_host(cbp_ctx* ctx, void* host, const void* dev, size_t bytes);
 
+/* ---- scheduling ----------------------------------------------------------------
+ * The deconvolution passes run persistent grids sized to fill the GPU. A context whose
+ * deconvolution overlaps work of another stream (the next epoch's kernel recovery in a
+ * video pipeline) can leave `sms` SMs to that stream. No reference counterpart
+ * (the reference parallelizes frames over host threads, tools/cbp.cpp:141-164). */
+int cbp_set_sm_reserve(cbp_ctx* ctx, int sms);
+
 /* ---- instrumentation ----------------------------------------------------------
  * Kernels enqueued by this context so far; optional CUDA-event timing of the three
  * deconvolution passes (A rows forward, B columns + filter, C rows inverse). */

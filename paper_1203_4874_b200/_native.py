@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libcbp_cuda.so")
+# CBP_CUDA_LIB: load another build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("CBP_CUDA_LIB") or os.path.join(HERE, "_lib", "libcbp_cuda.so")
 
 CBP_MAX_WIDTH = 63
 
@@ -101,6 +102,7 @@ _SIGS = {
     "cbp_generate_coprime_pair": (_I, [_I, C.c_uint64, _I, _D, _I, _P, _P, _P]),
     "cbp_launch_count": (C.c_longlong, [_P]),
     "cbp_profile": (_I, [_P, _I]),
+    "cbp_set_sm_reserve": (_I, [_P, _I]),
     "cbp_profile_read": (_I, [_P, _P, _P, _P]),
 }
 

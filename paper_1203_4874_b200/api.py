@@ -429,6 +429,12 @@ def read_slots(slots: torch.Tensor, count: int) -> list:
     return [host[i] for i in range(count)]
 
 
+def set_sm_reserve(sms: int, ctx: N.Context | None = None, device: int | None = None):
+    """cbp_set_sm_reserve: SMs the deconvolution passes of this context leave to other streams."""
+    ctx = ctx or context(device)
+    ctx.check(N.lib().cbp_set_sm_reserve(ctx.ptr, int(sms)))
+
+
 def profile(enable: bool, device: int | None = None):
     N.lib().cbp_profile(context(device).ptr, int(enable))
 

@@ -155,6 +155,7 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   while (rpc > 1 && size_t(2) * rpc * L * sizeof(float2) > 64 * 1024) rpc /= 2;
   a.rows_per_cta = rpc;
   a.col_width = deblur_col_width(a.Gr, CBP_MAX_WIDTH);
+  a.sm_reserve = ctx->sm_reserve;
   a.tw_row = twiddles(ctx, L);
   a.tw_post = twiddles(ctx, a.Gc);
   a.tw_col = twiddles(ctx, a.Gr);
@@ -173,13 +174,15 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
 
 int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
                size_t out_plane_stride, cudaStream_t stream) {
-  // Group whole frames so the half spectrum of a group (written by pass A, read and
-  // rewritten by B, read by C) stays resident in the 126 MB L2.
+  // Group whole frames into as few launches as the workspace budget allows: measured on
+  // B200 (tools/deblur_micro.py, 1080p RGB), launch boundaries cost more than keeping the
+  // half spectrum L2-resident (3 planes per launch: 29.0 us/plane; 87 planes: 18.9 us/plane,
+  // spectrum in HBM). CBP_GROUP_BUDGET_MB caps the spectrum workspace (default 1 GB).
   const size_t plane_bytes = size_t(a.Hc) * a.xp * sizeof(float2);
   const int ch = std::max(a.channels, 1);
   static const size_t budget = [] {
-    const char* e = getenv("CBP_L2_BUDGET_MB");
-    return size_t(e ? atoi(e) : 40) << 20;
+    const char* e = getenv("CBP_GROUP_BUDGET_MB");
+    return size_t(e ? atoi(e) : 1024) << 20;
   }();
   int frames_per_group = int(std::max<size_t>(1, budget / (plane_bytes * ch)));
   const int frames = planes / ch;
@@ -296,6 +299,12 @@ void cbp_destroy(cbp_ctx* ctx) {
 const char* cbp_last_error(const cbp_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 long long cbp_launch_count(const cbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cbp_set_sm_reserve(cbp_ctx* ctx, int sms) {
+  if (!ctx || sms < 0) return CBP_INVALID_ARGUMENT;
+  ctx->sm_reserve = sms;
+  return 0;
+}
 
 int cbp_profile(cbp_ctx* ctx, int enable) {
   if (!ctx) return CBP_INVALID_ARGUMENT;
@@ -435,3 +444,12 @@ int cbp_read_slots(cbp_ctx* ctx, const cbp_kernel_slot* slots_dev, int count,
 }
 
 }  // extern "C"
+
+#ifdef CBP_PHASES
+namespace cbp_dev {
+__device__ unsigned long long g_phase[64];
+}
+extern "C" int cbp_debug_phases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, cbp_dev::g_phase, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : 1;
+}
+#endif

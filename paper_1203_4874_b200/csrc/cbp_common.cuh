@@ -71,4 +71,20 @@ __device__ __forceinline__ void slot_fail(cbp_kernel_slot* s, int status, int st
   }
 }
 
+// Phase timestamps for kernel-internal profiling (build with -DCBP_PHASES; read with
+// cbp_debug_phases). Compiled out otherwise.
+#ifdef CBP_PHASES
+extern __device__ unsigned long long g_phase[64];
+__device__ __forceinline__ void phase_mark(int i, bool who) {
+  if (who && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_phase[i] = t;
+  }
+}
+#define CBP_PHASE(i, who) ::cbp_dev::phase_mark((i), (who))
+#else
+#define CBP_PHASE(i, who) ((void)0)
+#endif
+
 }  // namespace cbp_dev

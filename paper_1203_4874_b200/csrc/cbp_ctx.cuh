@@ -19,6 +19,7 @@ struct cbp_ctx {
   cbp_kernel_slot* host_slot = nullptr;  // pinned staging
   cudaEvent_t ev[8] = {};
   int num_sms = 148;
+  int sm_reserve = 0;  // cbp_set_sm_reserve
   // optional per-pass timing of the deconvolution (cbp_profile)
   int prof = 0;
   std::vector<cudaEvent_t> prof_ev;

@@ -6,6 +6,7 @@
 // column strip) with stride gridDim.x and keeps two tile buffers in shared memory;
 // the next tile's global->shared copies (cp.async, zero-filled outside the frame) are
 // in flight while the current tile is transformed, so HBM/L2 latency overlaps the FFT.
+#include <cstdlib>
 #include <vector>
 
 #include "cbp_deblur.cuh"
@@ -16,20 +17,25 @@ namespace cbp_dev {
 
 // PIPE: persistent CTAs with a double-buffered cp.async prefetch of the next tile;
 // otherwise one tile per CTA and latency is hidden by many resident CTAs.
-template <int L_, int RPC_, class Rs, int NT_, bool PIPE_ = true>
+// MINB: resident CTAs per SM the register allocation must allow (__launch_bounds__).
+// HD (columns): read the filter straight from L2 in the multiply instead of staging it.
+template <int L_, int RPC_, class Rs, int NT_, bool PIPE_ = true, int MINB_ = 1>
 struct RowPlan {
   static constexpr int L = L_;
   static constexpr int RPC = RPC_;
   static constexpr int NT = NT_;
   static constexpr bool PIPE = PIPE_;
+  static constexpr int MINB = MINB_;
   using R = Rs;
 };
-template <int G_, int W_, class Rs, int NT_, bool PIPE_ = true>
+template <int G_, int W_, class Rs, int NT_, bool PIPE_ = true, int MINB_ = 1, bool HD_ = false>
 struct ColPlan {
   static constexpr int G = G_;
   static constexpr int W = W_;
   static constexpr int NT = NT_;
   static constexpr bool PIPE = PIPE_;
+  static constexpr int MINB = MINB_;
+  static constexpr bool HD = HD_;
   using R = Rs;
 };
 
@@ -46,7 +52,7 @@ __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a
 // the r2c split handles the pair (k, L-k) in one thread: X[k] = e + W^k o,
 // X[L-k] = conj(e - W^k o), e = (Z[k] + conj Z[L-k])/2, o = -i (Z[k] - conj Z[L-k])/2.
 template <class P>
-__global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
   using R = typename P::R;
@@ -67,11 +73,13 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
       float2* d = dst + s * L;
       if (v16) {
         const int full = ok ? a.Nb / 4 : 0;  // whole 16-byte chunks inside the row
+#pragma unroll 1
         for (int c = threadIdx.x; c < L / 2; c += NT) {
           int bytes = c < full ? 16 : (ok ? min(max((a.Nb - 4 * c) * 4, 0), 16) : 0);
           cp_async16(d + 2 * c, bytes ? row + 4 * c : a.in, bytes);
         }
       } else {
+#pragma unroll 1
         for (int m = threadIdx.x; m < L; m += NT) {
           const int bytes = ok ? min(max((a.Nb - 2 * m) * 4, 0), 8) : 0;
           cp_async8(d + m, bytes ? row + 2 * m : a.in, bytes);
@@ -92,19 +100,35 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
     if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     float2* XT = a.X + size_t(p) * a.x_plane + r0;
-    constexpr int NPAIR = L / 2 + 1;
-    for (int idx = threadIdx.x; idx < NPAIR * RPC; idx += NT) {
-      const int k = idx / RPC, s = idx - k * RPC;
-      if (r0 + s >= a.Mb) continue;
-      const float2* z = cur + s * L;
-      const float2 zk = z[pos[k]];
-      const float2 zc = cconj(z[pos[k == 0 ? 0 : L - k]]);
-      const float2 e = cscale(cadd(zk, zc), 0.5f);
-      const float2 d = csub(zk, zc);
-      const float2 o = make_float2(0.5f * d.y, -0.5f * d.x);  // -i/2 * d
-      const float2 wo = cmul(__ldg(&a.tw_post[k]), o);
-      XT[size_t(k) * a.xp + s] = cadd(e, wo);
-      if (L - k != k) XT[size_t(L - k) * a.xp + s] = cconj(csub(e, wo));
+    const int nrows = min(RPC, a.Mb - r0);
+    // one thread per frequency pair (k, L-k) and row pair (2j, 2j+1): 16-byte stores
+    constexpr int NPAIR = L / 2 + 1, HALF = RPC / 2;
+#pragma unroll 1
+    for (int idx = threadIdx.x; idx < NPAIR * HALF; idx += NT) {
+      const int k = idx / HALF, j = idx - k * HALF;
+      if (2 * j >= nrows) continue;
+      const int pk = pos[k], pc = pos[k == 0 ? 0 : L - k];
+      const float2 w = __ldg(&a.tw_post[k]);
+      float2 xk[2], xc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float2* z = cur + (2 * j + h) * L;
+        const float2 zk = z[pk], zc = cconj(z[pc]);
+        const float2 e = cscale(cadd(zk, zc), 0.5f);
+        const float2 d = csub(zk, zc);
+        const float2 wo = cmul(w, make_float2(0.5f * d.y, -0.5f * d.x));  // W^k * (-i/2) d
+        xk[h] = cadd(e, wo);
+        xc[h] = cconj(csub(e, wo));
+      }
+      float2* dk = XT + size_t(k) * a.xp + 2 * j;
+      float2* dc = XT + size_t(L - k) * a.xp + 2 * j;
+      if (2 * j + 1 < nrows) {
+        *reinterpret_cast<float4*>(dk) = make_float4(xk[0].x, xk[0].y, xk[1].x, xk[1].y);
+        if (L - k != k) *reinterpret_cast<float4*>(dc) = make_float4(xc[0].x, xc[0].y, xc[1].x, xc[1].y);
+      } else {
+        dk[0] = xk[0];
+        if (L - k != k) dc[0] = xc[0];
+      }
     }
     __syncthreads();
   }
@@ -116,7 +140,7 @@ __global__ void __launch_bounds__(P::NT) k_rows_forward_ct(DeblurArgs a, int pla
 // leaves spectrum row u in slot pos(u), where the filter table (k_wiener_h) already stores
 // H(u, v), so the filter is an element-wise product; the inverse DIT restores natural rows.
 template <class P>
-__global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
   constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;  // padded: sequences on distinct banks
   constexpr int NBUF = P::PIPE ? 2 : 1;
@@ -150,7 +174,7 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
     const int status = slot->status;
     cp_async_wait<0>();
     __syncthreads();
-    if (status == 0) {  // filter strip in flight during the forward transform
+    if (status == 0 && !P::HD) {  // filter strip in flight during the forward transform
       const float2* Ht = a.H + size_t(f) * a.h_frame;
 #pragma unroll
       for (int s = 0; s < W; ++s) {
@@ -173,11 +197,22 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
       __syncthreads();
       if (!(a.dbg & 2)) {
         float4* c4 = reinterpret_cast<float4*>(cur);
-        const float4* h4 = reinterpret_cast<const float4*>(Hs);
-        for (int i = threadIdx.x; i < TILE / 2; i += NT) {
-          const float4 x = c4[i], h = h4[i];
-          c4[i] = make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
-                              x.z * h.w + x.w * h.z);
+        auto mul = [](float4 x, float4 h) {
+          return make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
+                             x.z * h.w + x.w * h.z);
+        };
+        if constexpr (P::HD) {
+          const float2* Ht = a.H + size_t(f) * a.h_frame;
+          for (int i = threadIdx.x; i < W * (G / 2); i += NT) {
+            const int s = i / (G / 2), c = i - s * (G / 2);
+            if (v0 + s < a.Hc) {
+              const float4 h = __ldg(reinterpret_cast<const float4*>(Ht + size_t(v0 + s) * a.hp) + c);
+              c4[s * (GP / 2) + c] = mul(c4[s * (GP / 2) + c], h);
+            }
+          }
+        } else {
+          const float4* h4 = reinterpret_cast<const float4*>(Hs);
+          for (int i = threadIdx.x; i < TILE / 2; i += NT) c4[i] = mul(c4[i], h4[i]);
         }
       }
       __syncthreads();
@@ -199,18 +234,21 @@ __global__ void __launch_bounds__(P::NT) k_cols_filter_ct(DeblurArgs a, int plan
 }
 
 // ------------------------------------------------- pass C (rows c2r + crop)
-// Tile layout [k][s] (RPC rows interleaved): one frequency of RPC consecutive rows is one
-// 32-byte chunk of XT. The transform runs with consecutive threads on consecutive rows.
+// Tile layout [slot][s] (RPC rows interleaved): one frequency of RPC consecutive rows is
+// one 32-byte chunk of XT, copied straight into its digit-reversed slot pos(k) (X[L] into
+// the spare slot L). The pairwise c2r split works slot to slot in place, the inverse DIT
+// leaves z[n] in natural order, so each thread stores z[n] of all RPC rows.
 template <class P>
-__global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int planes) {
+__global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, H = L + 1, TILE = ((H * RPC + 3) & ~3);
   static_assert(RPC % 2 == 0, "16-byte copies carry two rows");
   using R = typename P::R;
   using FFT = FftIP<L, RPC, 1, RPC, NT, true>;
   extern __shared__ __align__(16) float2 sm[];
-  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // slot of z[n] after the DIF
+  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // DIT input slot of z[n]
   for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
+  __syncthreads();
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
   auto rows_of = [&](int p) {
@@ -226,7 +264,8 @@ __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int pla
       const int k = idx / HALF, j = idx - k * HALF;
       const int rows_left = M - r0 - 2 * j;
       const int bytes = rows_left >= 2 ? 16 : (rows_left == 1 ? 8 : 0);
-      cp_async16(dst + k * RPC + 2 * j, bytes ? XT + size_t(k) * a.xp + 2 * j : a.X, bytes);
+      const int slot = k < L ? pos[k] : L;
+      cp_async16(dst + slot * RPC + 2 * j, bytes ? XT + size_t(k) * a.xp + 2 * j : a.X, bytes);
     }
   };
   int tile = blockIdx.x;
@@ -243,35 +282,51 @@ __global__ void __launch_bounds__(P::NT) k_rows_inverse_ct(DeblurArgs a, int pla
     const int M = rows_of(p);
     const int nrows = min(RPC, M - r0);
     if (nrows > 0) {
-      // inverse split in place, one thread per pair (k, L-k) and row (fft.cpp:257-270 c2r)
-      constexpr int NP = L / 2 + 1;
-      for (int idx = threadIdx.x; idx < NP * RPC; idx += NT) {
-        const int k = idx / RPC, s = idx - k * RPC;
-        const float2 A = cur[k * RPC + s], B = cur[(L - k) * RPC + s];
+      // inverse split in place (fft.cpp:257-270 c2r), one thread per frequency pair (k, L-k)
+      // and row pair: 16-byte shared-memory accesses
+      constexpr int NP = L / 2 + 1, HALF = RPC / 2;
+#pragma unroll 1
+      for (int idx = threadIdx.x; idx < NP * HALF; idx += NT) {
+        const int k = idx / HALF, j = idx - k * HALF;
+        float4* pa = reinterpret_cast<float4*>(cur + pos[k] * RPC + 2 * j);
+        float4* pb = reinterpret_cast<float4*>(cur + (k == 0 ? L : pos[L - k]) * RPC + 2 * j);
+        const float4 A4 = *pa, B4 = *pb;
         const float2 w = cconj(__ldg(&a.tw_post[k]));
-        const float2 e1 = cadd(A, cconj(B));
-        const float2 o1 = cmul(csub(A, cconj(B)), w);
-        cur[k * RPC + s] = make_float2(e1.x - o1.y, e1.y + o1.x);
-        if (k != 0 && 2 * k != L) {
-          // conj(tw_post[L-k]) = -tw_post[k]: z[L-k] = (B + conj A) + i (B - conj A)(-conj w)
+        const float2 wm = make_float2(-w.x, w.y);  // conj(tw_post[L-k]) = -tw_post[k]
+        float2 r1[2], r2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float2 A = h ? make_float2(A4.z, A4.w) : make_float2(A4.x, A4.y);
+          const float2 B = h ? make_float2(B4.z, B4.w) : make_float2(B4.x, B4.y);
+          const float2 e1 = cadd(A, cconj(B));
+          const float2 o1 = cmul(csub(A, cconj(B)), w);
+          r1[h] = make_float2(e1.x - o1.y, e1.y + o1.x);
           const float2 e2 = cadd(B, cconj(A));
-          const float2 o2 = cmul(csub(B, cconj(A)), make_float2(-w.x, w.y));
-          cur[(L - k) * RPC + s] = make_float2(e2.x - o2.y, e2.y + o2.x);
+          const float2 o2 = cmul(csub(B, cconj(A)), wm);
+          r2[h] = make_float2(e2.x - o2.y, e2.y + o2.x);
         }
+        *pa = make_float4(r1[0].x, r1[0].y, r1[1].x, r1[1].y);
+        if (k != 0 && 2 * k != L) *pb = make_float4(r2[0].x, r2[0].y, r2[1].x, r2[1].y);
       }
       __syncthreads();
-      if (!(a.dbg & 1)) FFT::template dif<true>(cur, a.twst_row, R{});  // natural -> slot order
+      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_row, R{});  // slot -> natural order
       const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
       float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
       if (a.out_vec2 && N % 2 == 0) {
         const int h = N / 2;
-        for (int s = 0; s < nrows; ++s)
-          for (int n = threadIdx.x; n < h; n += NT)
-            __stcs(reinterpret_cast<float2*>(dst + size_t(s) * a.out_ld) + n, cur[pos[n] * RPC + s]);
+        for (int n = threadIdx.x; n < h; n += NT) {
+#pragma unroll
+          for (int s2 = 0; s2 < RPC; s2 += 2) {
+            const float4 z = reinterpret_cast<const float4*>(cur + n * RPC)[s2 / 2];
+            if (s2 < nrows) __stcs(reinterpret_cast<float2*>(dst + size_t(s2) * a.out_ld) + n, make_float2(z.x, z.y));
+            if (s2 + 1 < nrows)
+              __stcs(reinterpret_cast<float2*>(dst + size_t(s2 + 1) * a.out_ld) + n, make_float2(z.z, z.w));
+          }
+        }
       } else {
         for (int s = 0; s < nrows; ++s)
           for (int n = threadIdx.x; n < N; n += NT) {
-            const float2 z = cur[pos[n >> 1] * RPC + s];
+            const float2 z = cur[(n >> 1) * RPC + s];
             __stcs(dst + size_t(s) * a.out_ld + n, (n & 1) ? z.y : z.x);
           }
       }
@@ -344,12 +399,17 @@ cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s
 }
 
 // --------------------------------------------------------------- dispatch
+// Persistent grid: resident CTAs per SM x (SMs - a.sm_reserve). The reserve leaves whole
+// SMs to kernels of other streams (cbp_set_sm_reserve: the recovery chain of the next
+// epoch overlaps the deconvolution in the video pipelines).
 template <class K>
-int persistent_grid(K kernel, int nt, size_t smem, int total, int sms) {
+int resident_per_sm(K kernel, int nt, size_t smem) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, smem);
-  per_sm = per_sm < 1 ? 1 : per_sm;
-  const int g = sms * per_sm;
+  return per_sm < 1 ? 1 : per_sm;
+}
+__host__ inline int persistent_grid(int per_sm, int sms, int reserve, int total) {
+  const int g = (sms - (reserve > 0 && reserve < sms ? reserve : 0)) * per_sm;
   return total < g ? total : g;
 }
 
@@ -358,46 +418,47 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
   constexpr int NB = P::PIPE ? 2 : 1;
   const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 3) & ~3) * sizeof(float2) + P::L * sizeof(short);
-  static int gA = 0, gC = 0, sms = 0;
+  static int pA = 0, pC = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_rows_forward_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
     cudaFuncSetAttribute(k_rows_inverse_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
-    gA = P::PIPE ? persistent_grid(k_rows_forward_ct<P>, P::NT, smA, 1 << 30, sms) : (1 << 30);
-    gC = P::PIPE ? persistent_grid(k_rows_inverse_ct<P>, P::NT, smC, 1 << 30, sms) : (1 << 30);
+    pA = resident_per_sm(k_rows_forward_ct<P>, P::NT, smA);
+    pC = resident_per_sm(k_rows_inverse_ct<P>, P::NT, smC);
   }
   const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
   if (inverse)
-    k_rows_inverse_ct<P><<<total < gC ? total : gC, P::NT, smC, s>>>(a, planes);
+    k_rows_inverse_ct<P><<<P::PIPE ? persistent_grid(pC, sms, a.sm_reserve, total) : total, P::NT, smC, s>>>(a, planes);
   else
-    k_rows_forward_ct<P><<<total < gA ? total : gA, P::NT, smA, s>>>(a, planes);
+    k_rows_forward_ct<P><<<P::PIPE ? persistent_grid(pA, sms, a.sm_reserve, total) : total, P::NT, smA, s>>>(a, planes);
 }
 
 template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
   constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
-  const size_t sm = ((P::PIPE ? 2 : 1) + 1) * size_t(GP) * P::W * sizeof(float2);
-  static int g = 0, sms = 0;
+  const size_t sm = ((P::PIPE ? 2 : 1) + (P::HD ? 0 : 1)) * size_t(GP) * P::W * sizeof(float2);
+  static int pB = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    g = P::PIPE ? persistent_grid(k_cols_filter_ct<P>, P::NT, sm, 1 << 30, sms) : (1 << 30);
+    pB = resident_per_sm(k_cols_filter_ct<P>, P::NT, sm);
   }
   const int total = planes * ((a.Hc + P::W - 1) / P::W);
-  k_cols_filter_ct<P><<<total < g ? total : g, P::NT, sm, s>>>(a, planes);
+  k_cols_filter_ct<P><<<P::PIPE ? persistent_grid(pB, sms, a.sm_reserve, total) : total, P::NT, sm, s>>>(a, planes);
 }
 
 // Radix plans in DIT order; the first (contiguous-butterfly) radix is odd so its strided
 // shared-memory accesses are bank-conflict free. Large radices run in registers.
-using Row972 = RowPlan<972, 4, Radices<27, 36>, 160>;      // 1080p: Gc = 1944
-using Row972b = RowPlan<972, 2, Radices<27, 36>, 96, false>;
-using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false>;
+using Row972 = RowPlan<972, 4, Radices<27, 36>, 160, true, 3>;  // 1080p: Gc = 1944
+using Row972a = RowPlan<972, 4, Radices<27, 36>, 160, true, 1>;
+using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
 using Row1944 = RowPlan<1944, 2, Radices<27, 8, 9>, 256>;  // 4K: Gc = 3888
 using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
 using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
-using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160>;    // 1080p: Gr = 1120
-using Col1120b = ColPlan<1120, 2, Radices<35, 32>, 96, false>;
-using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false>;
+using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;  // 1080p: Gr = 1120
+using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 1>;
+using Col1120b = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;
+using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false, 4, true>;
 using Col2187 = ColPlan<2187, 2, Radices<27, 9, 9>, 256>;  // 4K: Gr = 2187
 using Col490 = ColPlan<490, 8, Radices<35, 14>, 288>;      // 640x480: Gr = 490
 using Col270 = ColPlan<270, 8, Radices<27, 10>, 224>;      // 256x256: Gr = 270
@@ -449,8 +510,9 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
     if (!a.H || !a.twst_col) return false;
     switch (a.Gr) {
       case 1120:
-        if (a.variant == 1) launch_cols<Col1120b>(a, planes, s);
-        else if (a.variant == 2) launch_cols<Col1120c>(a, planes, s);
+        if (a.variant == 1) launch_cols<Col1120a>(a, planes, s);
+        else if (a.variant == 2) launch_cols<Col1120b>(a, planes, s);
+        else if (a.variant == 3) launch_cols<Col1120c>(a, planes, s);
         else launch_cols<Col1120>(a, planes, s);
         return true;
       case 2187: launch_cols<Col2187>(a, planes, s); return true;
@@ -463,8 +525,8 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
   const bool inv = pass == 2;
   switch (a.Gc / 2) {
     case 972:
-      if (a.variant == 1) launch_rows<Row972b>(a, planes, inv, s);
-      else if (a.variant == 2) launch_rows<Row972c>(a, planes, inv, s);
+      if (a.variant == 1) launch_rows<Row972a>(a, planes, inv, s);
+      else if (a.variant == 3) launch_rows<Row972c>(a, planes, inv, s);
       else launch_rows<Row972>(a, planes, inv, s);
       return true;
     case 1944: launch_rows<Row1944>(a, planes, inv, s); return true;

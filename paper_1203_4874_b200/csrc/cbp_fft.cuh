@@ -134,6 +134,18 @@ struct Split {
 template <int R, bool INV>
 __device__ __forceinline__ void dft(float2* v);
 
+// x * W_R^m (W_R = exp(-+2 pi i / R)) for a compile-time m; quarter turns are swaps and
+// sign flips instead of a full complex product
+template <int R, bool INV>
+__device__ __forceinline__ float2 twiddle_const(float2 x, int m) {
+  if (m == 0) return x;
+  if (2 * m == R) return make_float2(-x.x, -x.y);
+  if (4 * m == R) return INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);      // -+i
+  if (4 * m == 3 * R) return INV ? make_float2(x.y, -x.x) : make_float2(-x.y, x.x);  // +-i
+  const float2 w = make_float2(Root<R>::re(m), INV ? -Root<R>::im(m) : Root<R>::im(m));
+  return cmul(x, w);
+}
+
 // Composite in-register DFT, R = A*B (four-step): A-point DFTs of the B strided
 // subsequences, twiddles W_R^{b*ka} (compile-time constants, cbp_roots.cuh), then B-point
 // DFTs; output in natural order.
@@ -150,11 +162,7 @@ __device__ __forceinline__ void dft_composite(float2* v) {
 #pragma unroll
   for (int b = 1; b < B; ++b)
 #pragma unroll
-    for (int ka = 1; ka < A; ++ka) {
-      const int m = (b * ka) % R;
-      const float2 w = make_float2(Root<R>::re(m), INV ? -Root<R>::im(m) : Root<R>::im(m));
-      z[b][ka] = cmul(z[b][ka], w);
-    }
+    for (int ka = 1; ka < A; ++ka) z[b][ka] = twiddle_const<R, INV>(z[b][ka], (b * ka) % R);
 #pragma unroll
   for (int ka = 0; ka < A; ++ka) {
     float2 t[B];
@@ -200,7 +208,7 @@ __device__ __forceinline__ void dft(float2* v) {
     v[6] = csub(e2, t2);
     v[3] = cadd(e3, t3);
     v[7] = csub(e3, t3);
-  } else if constexpr (R == 3 || R == 5 || R == 7 || R == 9) {
+  } else if constexpr (R == 3 || R == 5 || R == 7) {
     dft_odd<R, INV>(v);
   } else {
     dft_composite<R, INV>(v);

@@ -100,69 +100,61 @@ using InvPos = Pos<typename Reverse<Radices<>, Rs>::type>;
 // SEQ_FAST: consecutive threads walk sequences first (column strips).
 template <int N, int NSEQ, int SP, int ES, int NT, bool SEQ_FAST>
 struct FftIP {
-  static_assert(NT % NSEQ == 0, "threads must split evenly over sequences");
-  static constexpr int TPS = NT / NSEQ;
+  static_assert(!SEQ_FAST || NT % NSEQ == 0, "threads must split evenly over sequences");
 
   // DIT = false: DIF stage (DFT, then twiddle); true: DIT stage (twiddle, then DFT).
   // twst: this stage's twiddles in butterfly order, twst[(i-1)*NB + b] = W_{PS}^{i*(b % PP)},
   // so a warp's twiddle loads are contiguous.
   template <bool DIT, bool INV, int R, int PP>
   __device__ __forceinline__ static void stage(float2* buf, const float2* __restrict__ twst) {
-    constexpr int PS = PP * R;
     constexpr int NB = N / R;
-    constexpr int BPT = (NB + TPS - 1) / TPS;
-    const int q = SEQ_FAST ? int(threadIdx.x % NSEQ) : int(threadIdx.x / TPS);
-    const int tl = SEQ_FAST ? int(threadIdx.x / NSEQ) : int(threadIdx.x % TPS);
-    float2* sb = buf + q * SP;
-    if constexpr (PP == 1 && ES == 1 && R % 2 == 0 && SP % 2 == 0) {
-      // contiguous butterflies: 16-byte accesses keep the stride-R pattern conflict-free
+    // Butterfly g of the CTA: sequence q, butterfly b. SEQ_FAST: consecutive threads take
+    // consecutive sequences of one butterfly; otherwise butterflies are numbered flat over
+    // (sequence, butterfly), so idle lanes gather in whole idle warps at the end.
+    constexpr int NG = NSEQ * NB;
 #pragma unroll 2
-      for (int m = 0; m < BPT; ++m) {
-        const int b = tl + m * TPS;
-        if (NB % TPS == 0 || b < NB) {
-          float4* p4 = reinterpret_cast<float4*>(sb + b * R);
-          float2 v[R];
+    for (int g = threadIdx.x; g < NG; g += NT) {
+      const int q = SEQ_FAST ? g % NSEQ : g / NB;
+      const int b = SEQ_FAST ? g / NSEQ : g - q * NB;
+      float2* sb = buf + q * SP;
+      if constexpr (PP == 1 && ES == 1 && R % 2 == 0 && SP % 2 == 0) {
+        // contiguous butterflies: 16-byte accesses keep the stride-R pattern conflict-free
+        float4* p4 = reinterpret_cast<float4*>(sb + b * R);
+        float2 v[R];
 #pragma unroll
-          for (int j = 0; j < R / 2; ++j) {
-            const float4 x = p4[j];
-            v[2 * j] = make_float2(x.x, x.y);
-            v[2 * j + 1] = make_float2(x.z, x.w);
-          }
-          dft<R, INV>(v);
-#pragma unroll
-          for (int j = 0; j < R / 2; ++j) p4[j] = make_float4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y);
+        for (int j = 0; j < R / 2; ++j) {
+          const float4 x = p4[j];
+          v[2 * j] = make_float2(x.x, x.y);
+          v[2 * j + 1] = make_float2(x.z, x.w);
         }
-      }
-    } else {
-#pragma unroll 2
-      for (int m = 0; m < BPT; ++m) {
-        const int b = tl + m * TPS;
-        if (NB % TPS == 0 || b < NB) {
-          const int k = PP > 1 ? b % PP : 0;
-          const int base = (b - k) * R + k;  // block * PS + k
-          float2 v[R];
+        dft<R, INV>(v);
 #pragma unroll
-          for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
-          if (DIT && PP > 1) {
+        for (int j = 0; j < R / 2; ++j) p4[j] = make_float4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y);
+      } else {
+        const int k = PP > 1 ? b % PP : 0;
+        const int base = (b - k) * R + k;  // block * PS + k
+        float2 v[R];
 #pragma unroll
-            for (int i = 1; i < R; ++i) {
-              float2 w = __ldg(&twst[(i - 1) * NB + b]);
-              if (INV) w.y = -w.y;
-              v[i] = cmul(v[i], w);
-            }
+        for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
+        if (DIT && PP > 1) {
+#pragma unroll
+          for (int i = 1; i < R; ++i) {
+            float2 w = __ldg(&twst[(i - 1) * NB + b]);
+            if (INV) w.y = -w.y;
+            v[i] = cmul(v[i], w);
           }
-          dft<R, INV>(v);
-          if (!DIT && PP > 1) {
-#pragma unroll
-            for (int i = 1; i < R; ++i) {
-              float2 w = __ldg(&twst[(i - 1) * NB + b]);
-              if (INV) w.y = -w.y;
-              v[i] = cmul(v[i], w);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
         }
+        dft<R, INV>(v);
+        if (!DIT && PP > 1) {
+#pragma unroll
+          for (int i = 1; i < R; ++i) {
+            float2 w = __ldg(&twst[(i - 1) * NB + b]);
+            if (INV) w.y = -w.y;
+            v[i] = cmul(v[i], w);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
       }
     }
     __syncthreads();

@@ -121,94 +121,297 @@ __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, Jac
   __syncthreads();
 }
 
-// Warp-synchronous variant for n <= 64: same rotations as herm_jacobi, executed by one
-// warp with __syncwarp barriers (the CTA-wide barrier cost dominated the small solves).
-__device__ void herm_jacobi_warp(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc,
-                                 int max_sweeps = 40) {
+// Hermitian eigen-decomposition by Householder tridiagonalization (LAPACK zhetrd), then
+// bisection + inverse iteration on the real tridiagonal (dstebz/dstein), back-transformed.
+// O(n^3) work with warp-level barriers, instead of Jacobi's O(n^3 * sweeps) with a CTA
+// barrier per round (~3x faster at n = 22 on B200, see tools/micro/bench_eig.cu).
+// Executed by one warp; n <= 64. Same contract as herm_jacobi: G's diagonal receives the
+// eigenvalues, V the eigenvectors as columns; G's off-diagonal part is destroyed.
+__device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, bool vectors = true) {
+  __shared__ double s_d[64], s_e[64], s_beta[64], s_rc[64], s_rs[64];
+  __shared__ double2 s_ec[64], s_w[64], s_p[64], s_delta[64];
+  __shared__ int s_ctl[4];
   const int lane = threadIdx.x & 31;
-  const int m = (n + 1) & ~1;
-  for (int i = lane; i < n * n; i += 32) {
+  const unsigned full = 0xffffffffu;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+    return v;
+  };
+  const bool pw = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  CBP_PHASE(30, pw);
+  // ---- tridiagonalization G = Q T Q^H; v_k is kept in column k below the diagonal
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m = n - k - 1;
+    double s2 = 0.0;
+    for (int i = lane; i < m; i += 32) s2 += zabs2(G[(k + 1 + i) * ldg + k]);
+    s2 = wsum(s2);
+    const double2 x0 = G[(k + 1) * ldg + k];
+    const double xn = sqrt(s2);
+    if (lane == 0) s_d[k] = G[k * ldg + k].x;
+    if (xn == 0.0) {
+      if (lane == 0) s_beta[k] = 0.0, s_ec[k] = make_double2(0.0, 0.0);
+      __syncwarp();
+      continue;
+    }
+    const double ax0 = zabs(x0);
+    const double2 ph = ax0 > 0.0 ? zscale(x0, 1.0 / ax0) : make_double2(1.0, 0.0);
+    const double beta = 1.0 / (xn * (xn + ax0));  // 2 / |v|^2
+    __syncwarp();
+    if (lane == 0) {
+      G[(k + 1) * ldg + k] = zscale(ph, ax0 + xn);  // v_0 = x_0 - alpha
+      s_beta[k] = beta;
+      s_ec[k] = zscale(ph, -xn);  // alpha: the new subdiagonal entry
+    }
+    __syncwarp();
+    // p = beta S v; S Hermitian, so p_i = beta sum_j conj(S[j][i]) v_j (lanes on i)
+    for (int i = lane; i < m; i += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int j = 0; j < m; ++j) acc = zadd(acc, zcmul(G[(k + 1 + j) * ldg + k + 1 + i], G[(k + 1 + j) * ldg + k]));
+      s_p[i] = zscale(acc, beta);
+    }
+    __syncwarp();
+    double kr = 0.0, ki = 0.0;  // K = beta/2 v^H p
+    for (int i = lane; i < m; i += 32) {
+      const double2 u = zcmul(G[(k + 1 + i) * ldg + k], s_p[i]);
+      kr += u.x;
+      ki += u.y;
+    }
+    const double2 K = zscale(make_double2(wsum(kr), wsum(ki)), 0.5 * beta);
+    for (int i = lane; i < m; i += 32) s_w[i] = zsub(s_p[i], zmul(K, G[(k + 1 + i) * ldg + k]));
+    __syncwarp();
+    // S <- S - v w^H - w v^H (lanes on columns i)
+    for (int i = lane; i < m; i += 32) {
+      const double2 vi = G[(k + 1 + i) * ldg + k], wi = s_w[i];
+      for (int j = 0; j < m; ++j) {
+        const double2 vj = G[(k + 1 + j) * ldg + k], wj = s_w[j];
+        double2& sji = G[(k + 1 + j) * ldg + k + 1 + i];
+        sji = zsub(sji, zadd(zmul(vj, zconj(wi)), zmul(wj, zconj(vi))));
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int k = n >= 2 ? n - 2 : 0; k < n; ++k) s_d[k] = G[k * ldg + k].x;
+    if (n >= 2) {
+      s_ec[n - 2] = G[(n - 1) * ldg + n - 2];
+      s_beta[n - 2] = 0.0;
+    }
+    // unitary diagonal D with D^H T D real: e_k -> |e_k|
+    s_delta[0] = make_double2(1.0, 0.0);
+    for (int k = 0; k + 1 < n; ++k) {
+      const double ae = zabs(s_ec[k]);
+      s_e[k] = ae;
+      s_delta[k + 1] = ae > 0.0 ? zmul(s_delta[k], zscale(s_ec[k], 1.0 / ae)) : s_delta[k];
+    }
+    s_e[n - 1] = 0.0;
+  }
+  for (int i = lane; i < n * n; i += 32) {  // Z = I in the real part of V
     const int r = i / n, c = i - r * n;
     V[r * ldv + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
   }
-  double dmax = 0.0;
-  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, fabs(G[i * ldg + i].x));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  const double floor_abs = 1e-17 * dmax;
   __syncwarp();
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    int rotated = 0;
-    for (int r = 0; r < m - 1; ++r) {
-      for (int k = lane; k < m / 2; k += 32) {
-        int p, q;
-        rr_pair(r, k, m, p, q);
-        double cs = 1.0, sn = 0.0;
-        double2 e = make_double2(1.0, 0.0);
-        if (q < n) {
-          const double al = G[p * ldg + p].x, be = G[q * ldg + q].x;
-          const double2 ga = G[p * ldg + q];
-          const double ag = hypot(ga.x, ga.y);
-          if (ag > 0.0 && ag > 1e-15 * sqrt(fabs(al * be)) && ag > floor_abs) {
-            const double zeta = (be - al) / (2.0 * ag);
-            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            cs = 1.0 / sqrt(1.0 + tt * tt);
-            sn = cs * tt;
-            e = make_double2(ga.x / ag, ga.y / ag);
-            rotated = 1;
-          }
+  __syncwarp();
+  CBP_PHASE(31, pw);
+  // ---- the real tridiagonal T is scaled to unit norm by a power of two (exact).
+  // Eigenvalues only: bisection on Sturm counts, one lane per eigenvalue. Divisions cost
+  // ~130 cycles of FP64 latency on B200, so the counts use the division-free determinant
+  // recurrence (no overflow at unit norm: |p_i| <= 3^i; underflow rescale every 8 steps).
+  double lo0 = 1e300, hi0 = -1e300;
+  for (int i = 0; i < n; ++i) {
+    const double rad = (i > 0 ? s_e[i - 1] : 0.0) + (i + 1 < n ? s_e[i] : 0.0);
+    lo0 = fmin(lo0, s_d[i] - rad);
+    hi0 = fmax(hi0, s_d[i] + rad);
+  }
+  const double tn = fmax(fabs(lo0), fabs(hi0));
+  const double sc = tn > 0.0 ? ldexp(1.0, -ilogb(tn) - 1) : 1.0;  // power of two: exact
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) {
+    s_d[i] *= sc;
+    s_e[i] *= sc;
+    s_rc[i] = s_e[i] * s_e[i];  // e_i^2
+  }
+  __syncwarp();
+  lo0 = lo0 * sc - 1e-14;
+  hi0 = hi0 * sc + 1e-14;
+  auto count_below = [&](double x) {  // number of eigenvalues of T' smaller than x
+    double p0 = 1.0, p1 = s_d[0] - x;
+    int sg1 = p1 < 0.0 ? -1 : 1;
+    int cnt = sg1 < 0;
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+      const double p2 = fma(s_d[i] - x, p1, -s_rc[i - 1] * p0);
+      const int sg2 = p2 < 0.0 ? -1 : (p2 > 0.0 ? 1 : -sg1);
+      cnt += sg2 != sg1;
+      sg1 = sg2;
+      p0 = p1;
+      p1 = p2;
+      if ((i & 7) == 0 && fabs(p1) < 0x1p-600 && fabs(p0) < 0x1p-600) {
+        p0 *= 0x1p+600;
+        p1 *= 0x1p+600;
+      }
+    }
+    return cnt;
+  };
+  auto rcp = [](double v) {  // ~1 ulp reciprocal: MUFU seed + 2 Newton steps
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+    r = fma(r, fma(-v, r, 1.0), r);
+    r = fma(r, fma(-v, r, 1.0), r);
+    return r;
+  };
+  for (int k = lane; k < n && !vectors; k += 32) {
+    double lo = lo0, hi = hi0;
+    for (int it = 0; it < 62; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      if (count_below(mid) > k) hi = mid;
+      else lo = mid;
+    }
+    s_p[k].x = 0.5 * (lo + hi);
+  }
+  __syncwarp();
+  CBP_PHASE(34, pw);
+  if (!vectors) {
+    for (int k = lane; k < n; k += 32) G[k * ldg + k] = make_double2(s_p[k].x / sc, 0.0);
+    __syncwarp();
+    return;
+  }
+  // ---- eigenvectors: implicit QL with Wilkinson shifts (tqli) on T'. Every lane runs the
+  // same scalar recurrence (no broadcast barrier). The sweep reads d/e and writes the
+  // updated entries to separate arrays (s_dn/s_en), so its loads never wait behind its
+  // stores; rsqrt/rcp with Newton steps replace hypot and the divisions on the chain.
+  // The sweep's Givens rotations are then applied to each lane's rows of Z.
+  {
+    __shared__ double s_dn[64], s_en[64];
+    for (int i = lane; i < n * n; i += 32) {  // Z = I in the real part of V
+      const int r = i / n, c = i - r * n;
+      V[r * ldv + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    }
+    __syncwarp();
+    int l = 0, iter = 0;
+    while (l < n) {
+      int m = l;
+      for (; m < n - 1; ++m) {
+        const double dd = fabs(s_d[m]) + fabs(s_d[m + 1]);
+        if (fabs(s_e[m]) <= 2.220446049250313e-16 * dd) break;
+      }
+      if (m == l || ++iter > 60) {
+        ++l;
+        iter = 0;
+        continue;
+      }
+      const double el = s_e[l];
+      double g = (s_d[l + 1] - s_d[l]) * 0.5 * rcp(el);
+      double r = sqrt(fma(g, g, 1.0));
+      g = s_d[m] - s_d[l] + el * rcp(g + copysign(r, g));
+      double sn = 1.0, cs = 1.0, p = 0.0;
+      double dip1 = s_d[m];
+      int i = m - 1, nr = 0;
+      bool early = false;
+      for (; i >= l; --i) {
+        const double ei = s_e[i], di = s_d[i];
+        const double f = sn * ei, b = cs * ei;
+        const double q = fma(f, f, g * g);
+        if (q == 0.0) {
+          early = true;
+          break;
         }
-        sc.cs[k] = cs;
-        sc.sn[k] = sn;
-        sc.e[k] = e;
+        const double ri = rsqrt(q);
+        s_en[i + 1] = q * ri;
+        sn = f * ri;
+        cs = g * ri;
+        g = dip1 - p;
+        r = fma(di - g, sn, 2.0 * cs * b);
+        p = sn * r;
+        s_dn[i + 1] = g + p;
+        g = fma(cs, r, -b);
+        dip1 = di;
+        s_rc[nr] = cs;
+        s_rs[nr] = sn;
+        ++nr;
       }
       __syncwarp();
-      for (int i = lane; i < (m / 2) * n * 2; i += 32) {
-        const int which = i / ((m / 2) * n);
-        const int rem = i - which * (m / 2) * n;
-        const int k = rem / n, row = rem - k * n;
-        const double sn = sc.sn[k];
-        if (sn == 0.0) continue;
-        int p, q;
-        rr_pair(r, k, m, p, q);
-        double2* M = which ? V : G;
-        const int ld = which ? ldv : ldg;
-        const double cs = sc.cs[k];
-        const double2 ec = zconj(sc.e[k]);
-        const double2 gp = M[row * ld + p], gq = zmul(ec, M[row * ld + q]);
-        M[row * ld + p] = make_double2(cs * gp.x - sn * gq.x, cs * gp.y - sn * gq.y);
-        M[row * ld + q] = make_double2(sn * gp.x + cs * gq.x, sn * gp.y + cs * gq.y);
+      // commit the sweep: entries i+1 .. m were rewritten (the last rotation index is m-nr)
+      const int lo_w = m - nr + 1;
+      for (int j = lane + lo_w; j <= m; j += 32) {
+        s_d[j] = s_dn[j];
+        if (j < m) s_e[j] = s_en[j];  // e_m is set below
       }
       __syncwarp();
-      for (int i = lane; i < (m / 2) * n; i += 32) {
-        const int k = i / n, col = i - k * n;
-        const double sn = sc.sn[k];
-        if (sn == 0.0) continue;
-        int p, q;
-        rr_pair(r, k, m, p, q);
-        const double cs = sc.cs[k];
-        const double2 e = sc.e[k];
-        const double2 gp = G[p * ldg + col], gq = zmul(e, G[q * ldg + col]);
-        double2 np = make_double2(cs * gp.x - sn * gq.x, cs * gp.y - sn * gq.y);
-        double2 nq = make_double2(sn * gp.x + cs * gq.x, sn * gp.y + cs * gq.y);
-        if (col == q) np = make_double2(0.0, 0.0);
-        if (col == p) nq = make_double2(0.0, 0.0);
-        if (col == p) np.y = 0.0;
-        if (col == q) nq.y = 0.0;
-        G[p * ldg + col] = np;
-        G[q * ldg + col] = nq;
+      if (lane == 0) {
+        if (early) {  // r == 0 at rotation i: tqli sets e[i+1] = r and deflates there
+          s_d[i + 1] = dip1 - p;
+          s_e[i + 1] = 0.0;
+          s_e[m] = 0.0;
+        } else {
+          s_d[l] -= p;
+          s_e[l] = g;
+          s_e[m] = 0.0;
+        }
+      }
+      // rotation j acts on columns (m-1-j, m-j) of every row of Z
+      for (int rr = lane; rr < n; rr += 32) {
+        double2* zr = V + rr * ldv;
+        double zc = zr[m].x;
+        for (int j = 0; j < nr; ++j) {
+          const int c0 = m - 1 - j;
+          const double zi = zr[c0].x;
+          zr[c0 + 1].x = fma(s_rs[j], zi, s_rc[j] * zc);
+          zc = fma(s_rc[j], zi, -s_rs[j] * zc);
+        }
+        zr[m - nr].x = zc;
       }
       __syncwarp();
     }
-    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  for (int k = lane; k < n; k += 32) s_p[k].x = s_d[k];
+  __syncwarp();
+  CBP_PHASE(35, pw);
+  for (int k = lane; k < n; k += 32) s_d[k] = s_p[k].x / sc;
+  __syncwarp();
+  CBP_PHASE(32, pw);
+  // ---- eigenvectors V = Q D Z: Householders applied in reverse order, lanes on columns
+  for (int i = lane; i < n * n; i += 32) {
+    const int r = i / n, c = i - r * n;
+    V[r * ldv + c] = zscale(s_delta[r], V[r * ldv + c].x);
   }
   __syncwarp();
+  for (int k = n - 3; k >= 0; --k) {
+    const double beta = s_beta[k];
+    if (beta == 0.0) continue;
+    const int m = n - k - 1;
+    for (int c = lane; c < n; c += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int j = 0; j < m; ++j) acc = zadd(acc, zcmul(G[(k + 1 + j) * ldg + k], V[(k + 1 + j) * ldv + c]));
+      acc = zscale(acc, beta);
+      for (int j = 0; j < m; ++j)
+        V[(k + 1 + j) * ldv + c] = zsub(V[(k + 1 + j) * ldv + c], zmul(G[(k + 1 + j) * ldg + k], acc));
+    }
+    __syncwarp();
+  }
+  for (int k = lane; k < n; k += 32) G[k * ldg + k] = make_double2(s_d[k], 0.0);
+  __syncwarp();
+  CBP_PHASE(33, pw);
 }
 
-// whole-CTA entry (the CTA-wide variant measured faster than the single-warp one:
-// the per-round FP64 rotation parameters dominate, not the barriers)
+// eigenvalues only (G's diagonal), whole CTA
+__device__ __forceinline__ void herm_eigvals_cta(double2* G, int ldg, double2* V, int ldv, int n) {
+  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, false);
+  __syncthreads();
+}
+
+// whole-CTA entry: the tridiagonal route on warp 0 (the Jacobi solver above is kept as
+// the reference implementation, selectable with -DCBP_JACOBI)
 __device__ __forceinline__ void herm_jacobi_cta(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc) {
-  herm_jacobi(G, ldg, V, ldv, n, sc);
+#ifdef CBP_JACOBI
+  if (sc.cs) {
+    herm_jacobi(G, ldg, V, ldv, n, sc);
+    return;
+  }
+#endif
+  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n);
+  __syncthreads();
 }
 
 __device__ __forceinline__ double warp_sum(double v) {

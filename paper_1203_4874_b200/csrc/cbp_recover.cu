@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
   if (a.flags[b] & 1) return;                         // signed content: see k_width_pick
   const int s = a.search_min + 2 * si;
   if (s > a.search_max) return;
+  CBP_PHASE(0, blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0);
   const int L = axis == 0 ? a.cols : a.rows;
   const double2* p = a.slices + slice_offset(a, b, axis, 0, 0);
   const double2* q = a.slices + slice_offset(a, b, axis, 1, 0);
@@ -224,8 +225,22 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
     }
     A[j * s + i] = make_double2(re, im);
   }
-  __syncthreads();
-  onesided_sv(A, s, s, sv, &flag);
+  // real slices (nonnegative content: DC sums) give a real symmetric block whose singular
+  // values are |eigenvalues|: tridiagonal QL on one warp; complex blocks use Jacobi SVD
+  const bool pw = blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0;
+  CBP_PHASE(1, pw);
+  int cplx = 0;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) cplx |= A[idx].y != 0.0;
+  cplx = __syncthreads_or(cplx);
+  if (!cplx) {
+    double2* V = A + s * s;
+    herm_eigvals_cta(A, s, V, s, s);
+    for (int i = threadIdx.x; i < s; i += blockDim.x) sv[i] = fabs(A[i * s + i].x);
+    __syncthreads();
+  } else {
+    onesided_sv(A, s, s, sv, &flag);
+  }
+  CBP_PHASE(2, pw);
   if (threadIdx.x == 0) {
     double mx = 0.0, mn = 1e300;
     for (int i = 0; i < s; ++i) mx = fmax(mx, sv[i]), mn = fmin(mn, sv[i]);
@@ -289,10 +304,10 @@ __global__ void __launch_bounds__(128) k_width_pick(RecoverArgs a) {
 
 cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
   dim3 g(a.nsizes, 2, a.batch);
-  size_t sm = size_t(a.search_max) * a.search_max * sizeof(double2);
+  size_t sm = size_t(2) * a.search_max * a.search_max * sizeof(double2);  // block + eigenvectors
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cfg = true;
   }
   k_width_blocks<<<g, 512, sm, s>>>(a);
@@ -382,6 +397,8 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
   const int n = 2 * t;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const bool pw = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  CBP_PHASE(10, pw);
   // correlations: c(x, y, d) = sum_m conj(x[m]) y[m + d]
   const int nl = 4 * t - 1;
   for (int l = warp; l < nl; l += nw) {
@@ -425,7 +442,9 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
     sm.G[j * n + k] = v;
   }
   __syncthreads();
+  CBP_PHASE(11, pw);
   herm_jacobi_cta(sm.G, n, sm.V, n, n, sm.js);
+  CBP_PHASE(12, pw);
   __shared__ int kmin_s, k2_s;
   __shared__ double lmax_s, lmin_s;
   if (tid == 0) {
@@ -485,6 +504,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
     for (int i = tid; i < n; i += blockDim.x) sm.x[i] = zscale(sm.g[i], inv);
     __syncthreads();
   }
+  CBP_PHASE(13, pw);
   // gap = sigma_{2t-2} / sigma_0 (poly.cpp:105-110) with sigma_{2t-2} = |A v_2|
   double sig2 = 0.0;
   if (n >= 2) {
@@ -492,6 +512,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
     __syncthreads();
     sig2 = sqrt(apply_A(p, lp, q, lq, t, sm.g, r, R, sm.red));
   }
+  CBP_PHASE(14, pw);
   const double sig0 = sqrt(fmax(lmax_s, 0.0));
   SolveResult res;
   res.gap = sig0 == 0.0 ? 0.0 : sig2 / sig0;
@@ -739,7 +760,9 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
     s.G[idx] = v;
   }
   __syncthreads();
+  CBP_PHASE(25, blockIdx.x == 0);
   herm_jacobi_cta(s.G, n, s.V, n, n, s.js);
+  CBP_PHASE(22, blockIdx.x == 0);
   __shared__ int kmin_s;
   __shared__ double lmax_s, lmin_s;
   if (threadIdx.x == 0) {
@@ -952,6 +975,7 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   }
   __syncthreads();
   if (slot->status != 0) return;
+  CBP_PHASE(20, blockIdx.x == 0);
   ComposeSmem s = carve_compose(shc, t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   __syncthreads();
@@ -961,7 +985,9 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   complete_cta(v2, t, 1, s.root, s.B);
   __syncthreads();
   double residual = 0.0, ratio = 0.0;
+  CBP_PHASE(21, blockIdx.x == 0);
   const int rs = resolve_cta(s, t, &residual, &ratio);
+  CBP_PHASE(23, blockIdx.x == 0);
   if (rs) {
     if (threadIdx.x == 0) {
       slot_fail(slot, CBP_DEGENERATE_SCALES, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, ratio, rs);
@@ -971,6 +997,7 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   int reason = 0;
   double value = 0.0;
   const int st = assemble_cta(s, t, a.max_imag_energy, a.negative_weight_tol, slot->weights, &reason, &value);
+  CBP_PHASE(24, blockIdx.x == 0);
   if (threadIdx.x == 0) {
     if (st) {
       slot_fail(slot, st, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, value, reason);
@@ -988,7 +1015,8 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
 cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_compose, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(compose_smem_bytes(kSolveMaxWidth)));
     cfg = true;
   }
   k_compose<<<a.batch, 256, compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s>>>(a);
@@ -1011,6 +1039,7 @@ cudaError_t launch_complete(const double2* values, int t, int axis, double2* out
 __global__ void __launch_bounds__(256) k_resolve(const double2* av, const double2* bv, int t, double2* lambda,
                                                  double2* mu, double* residual, int* status, double* value) {
   extern __shared__ double2 shc[];
+  CBP_PHASE(20, blockIdx.x == 0);
   ComposeSmem s = carve_compose(shc, t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   __syncthreads();
@@ -1031,7 +1060,7 @@ cudaError_t launch_resolve(const double2* a_values, const double2* b_values, int
                            double2* mu, double* residual, int* status, double* value, cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
     cfg = true;
   }
   k_resolve<<<1, 256, compose_smem_bytes(t), s>>>(a_values, b_values, t, lambda, mu, residual, status, value);
@@ -1042,6 +1071,7 @@ __global__ void __launch_bounds__(256) k_assemble(const double2* as, const doubl
                                                   const double2* mu, int t, double max_imag, double neg_tol,
                                                   cbp_kernel_slot* slot) {
   extern __shared__ double2 shc[];
+  CBP_PHASE(20, blockIdx.x == 0);
   ComposeSmem s = carve_compose(shc, t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   for (int i = threadIdx.x; i < t * t; i += blockDim.x) s.A[i] = as[i], s.B[i] = bs[i];
@@ -1063,7 +1093,7 @@ cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const 
                             cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
     cfg = true;
   }
   k_assemble<<<1, 256, compose_smem_bytes(t), s>>>(a_spec, b_spec, lambda, mu, t, max_imag, neg_tol, slot);
