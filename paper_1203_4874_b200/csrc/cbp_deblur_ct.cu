@@ -376,10 +376,13 @@ __global__ void __launch_bounds__(256) k_wiener_h(DeblurArgs a, int frames) {
   const int vv = threadIdx.x >> 5, v = v0 + vv;
   const int u = blockIdx.x * 32 + (threadIdx.x & 31);
   if (v >= a.Hc || u >= a.Gr) return;
-  double2 acc = make_double2(0.0, 0.0);
+  // powers of W_Gr^u by recurrence (one sincos per thread; drift ~t ulp, far below the
+  // float2 the table is stored in)
+  const double2 wu = zroot(u, a.Gr);
+  double2 w = make_double2(1.0, 0.0), acc = make_double2(0.0, 0.0);
   for (int ai = 0; ai < t; ++ai) {
-    const double2 w = zroot(long(u) * ai, a.Gr);
     acc = zadd(acc, zmul(Ss[vv * t + ai], w));
+    w = zmul(w, wu);
   }
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
   const double den = (acc.x * acc.x + acc.y * acc.y + slot->epsilon);

@@ -138,7 +138,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.has_epsilon = cfg ? cfg->has_epsilon : 0;
   a.epsilon = cfg ? cfg->epsilon : 0.0;
   const size_t B = size_t(batch), T = size_t(t_max), L = size_t(a.lmax);
-  P.vtiles = want_validate ? validate_tiles(rows, cols) : 0;
+  P.vtiles = want_validate ? validate_tiles(rows, cols, 1) : 0;  // decode widths <= 31: 32-row tiles
   // carve one allocation (256-byte aligned pieces)
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -572,7 +572,7 @@ int cbp_validate_pair(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, 
   if ((st = check_kernel(ctx, k1, t))) return st;
   if ((st = check_kernel(ctx, k2, t))) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nt = validate_tiles(rows + t - 1, cols + t - 1);
+  const int nt = validate_tiles(rows + t - 1, cols + t - 1, t);
   char* base = static_cast<char*>(
       workspace(ctx, WS_RED, sizeof(double2) * (size_t(nt) * channels + 2) + 2 * sizeof(double) * t * t + 256));
   double* part = reinterpret_cast<double*>(base);

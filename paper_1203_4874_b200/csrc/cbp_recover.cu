@@ -1101,10 +1101,20 @@ cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const 
 }
 
 // ------------------------------------------------------- validation residual
-// Full 2-D convolution (poly.cpp:27-38) evaluated at output (i, j) from a shared tile.
-constexpr int VT_R = 16, VT_C = 64;
-
-int validate_tiles(int rows, int cols) { return ((rows + VT_R - 1) / VT_R) * ((cols + VT_C - 1) / VT_C); }
+// Full 2-D convolution (poly.cpp:27-38) of an FP64 shared tile. A thread owns 8 vertically
+// adjacent outputs of one column (the lanes of a warp take consecutive columns, so shared
+// loads are conflict-free) and walks each kernel column in chunks of 4 taps with an
+// 11-value register window: each tile load feeds 8 FMAs (the one-output-per-thread loop
+// was shared-memory bound at 2 loads per FMA). Taps are zero-padded to a multiple of 4.
+// Outputs per CTA: VT_R rows x 64 columns (8 rows per thread): 32 rows (256 threads), or
+// 8 rows (64 threads) for kernels wider than 40 taps, whose halo would not fit otherwise.
+constexpr int VT_C = 64;
+__host__ __device__ inline int conv_rows(int t) { return t > 40 ? 8 : 32; }
+__host__ __device__ inline int conv_pad(int t) { return (t + 3) & ~3; }
+int validate_tiles(int rows, int cols, int t) {
+  const int vr = conv_rows(t);
+  return ((rows + vr - 1) / vr) * ((cols + VT_C - 1) / VT_C);
+}
 
 // mode 0: a = conv(X, K) over the Ro x Co output, y = Y[i][j]; num += (a-y)^2, den += y^2.
 // mode 1: a = conv(X, K), y = conv(X2, K2); num += (a-y)^2, den += a^2.
@@ -1127,15 +1137,32 @@ struct ConvResidArgs {
   int ntiles;
 };
 
-__device__ __forceinline__ double conv_at(const double* tile, int tw, const double* K, int t, int li, int lj) {
-  // out(i,j) = sum_{a,b} K[a][b] X[i-a][j-b]; tile holds X rows [i0-t+1, i0+VT_R), cols [j0-t+1, ...)
-  double acc = 0.0;
-  for (int a2 = 0; a2 < t; ++a2) {
-    const double* row = tile + (li + t - 1 - a2) * tw + (lj + t - 1);
-    const double* kr = K + a2 * t;
-    for (int b2 = 0; b2 < t; ++b2) acc = fma(kr[b2], row[-b2], acc);
+// acc[q] = out(li0 + q, lj); tile[r][c] = X[i0 - tp + 1 + r][j0 - t + 1 + c] (pitch tw);
+// kt[b * tp + a] = K[a][b] (transposed, zero-padded rows a >= t)
+__device__ __forceinline__ void conv_col8(const double* tile, int tw, const double* kt, int t, int tp, int li0, int lj,
+                                          double acc[8]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int b2 = 0; b2 < t; ++b2) {
+    // X(i0 + li0 + x, j - b2) = col[x * tw]
+    const double* col = tile + (li0 + tp - 1) * tw + (lj + t - 1 - b2);
+    const double* kc = kt + b2 * tp;
+    double v[11];  // v[k] = col[(7 - c - k) * tw] for the chunk of taps a = c .. c+3
+#pragma unroll
+    for (int k = 0; k < 7; ++k) v[k + 4] = col[(7 - k) * tw];
+    for (int c = 0; c < tp; c += 4) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) v[k] = v[k + 4];
+#pragma unroll
+      for (int k = 7; k < 11; ++k) v[k] = col[(7 - c - k) * tw];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double w = kc[c + j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fma(w, v[7 - q + j], acc[q]);
+      }
+    }
   }
-  return acc;
 }
 
 __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
@@ -1150,6 +1177,7 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
     t = slot->width;
     K = slot->weights;
   }
+  const int tp = conv_pad(t), VT_R = conv_rows(t);
   // mode 0: X is the (rows-t+1) x (cols-t+1) latent, output is the rows x cols frame
   const int xr = a.mode == 0 ? a.xr - t + 1 : a.xr;
   const int xc = a.mode == 0 ? a.xc - t + 1 : a.xc;
@@ -1159,40 +1187,47 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
   const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - tr * tiles_c;
   const int i0 = tr * VT_R, j0 = tc * VT_C;
   if (i0 >= ro) return;
-  double* kw = shd;                      // t*t
-  double* kw2 = kw + t * t;              // t*t (mode 1)
-  const int tw = VT_C + t - 1, th = VT_R + t - 1;
-  double* tile = kw2 + t * t;  // converted once to FP64 (F2F throughput is far below DFMA)
+  double* kt = shd;           // t x tp (transposed)
+  double* kt2 = kt + t * tp;  // mode 1
+  const int tw = VT_C + t - 1, th = VT_R + tp - 1;
+  double* tile = kt2 + t * tp;  // converted once to FP64 (F2F throughput is far below DFMA)
   double* tile2 = tile + th * tw;
-  for (int i = threadIdx.x; i < t * t; i += blockDim.x) {
-    kw[i] = K[i];
-    if (a.mode == 1) kw2[i] = a.K2[i];
+  for (int i = threadIdx.x; i < t * tp; i += blockDim.x) {
+    const int bb = i / tp, aa = i - bb * tp;
+    kt[i] = aa < t ? K[aa * t + bb] : 0.0;
+    if (a.mode == 1) kt2[i] = aa < t ? a.K2[aa * t + bb] : 0.0;
   }
   const float* X = a.X + size_t(plane) * a.x_plane;
   const float* Y = a.Y + size_t(plane) * a.y_plane;
   for (int idx = threadIdx.x; idx < th * tw; idx += blockDim.x) {
     const int li = idx / tw, lj = idx - li * tw;
-    const int gi = i0 - t + 1 + li, gj = j0 - t + 1 + lj;
+    const int gi = i0 - tp + 1 + li, gj = j0 - t + 1 + lj;
     const bool in = gi >= 0 && gi < xr && gj >= 0 && gj < xc;
     tile[idx] = in ? double(X[size_t(gi) * a.xld + gj]) : 0.0;
     if (a.mode == 1) tile2[idx] = in ? double(Y[size_t(gi) * a.yld + gj]) : 0.0;
   }
   __syncthreads();
   double num = 0.0, den = 0.0;
-  for (int e = threadIdx.x; e < VT_R * VT_C; e += blockDim.x) {
-    const int li = e / VT_C, lj = e - li * VT_C;
-    const int gi = i0 + li, gj = j0 + lj;
-    if (gi >= ro || gj >= co) continue;
-    const double c1 = conv_at(tile, tw, kw, t, li, lj);
-    double y;
-    if (a.mode == 0) {
-      y = double(Y[size_t(gi) * a.yld + gj]);
-      den += y * y;
-    } else {
-      y = conv_at(tile2, tw, kw2, t, li, lj);
-      den += c1 * c1;
+  const int lj = threadIdx.x % VT_C, li0 = (threadIdx.x / VT_C) * 8;
+  const int gj = j0 + lj;
+  if (gj < co && i0 + li0 < ro) {
+    double c1[8], c2[8];
+    conv_col8(tile, tw, kt, t, tp, li0, lj, c1);
+    if (a.mode == 1) conv_col8(tile2, tw, kt2, t, tp, li0, lj, c2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int gi = i0 + li0 + q;
+      if (gi >= ro) break;
+      double y;
+      if (a.mode == 0) {
+        y = double(Y[size_t(gi) * a.yld + gj]);
+        den += y * y;
+      } else {
+        y = c2[q];
+        den += c1[q] * c1[q];
+      }
+      num += (c1[q] - y) * (c1[q] - y);
     }
-    num += (c1 - y) * (c1 - y);
   }
   num = warp_sum(num);
   den = warp_sum(den);
@@ -1205,6 +1240,11 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
     for (int w = 0; w < int(blockDim.x >> 5); ++w) sn += rn[w], sd += rd[w];
     a.part[size_t(plane) * a.ntiles + blockIdx.x] = make_double2(sn, sd);
   }
+}
+
+__host__ inline size_t conv_smem(int t, int mode) {
+  const int tp = conv_pad(t);
+  return (mode == 1 ? 2 : 1) * (size_t(t) * tp + size_t(conv_rows(t) + tp - 1) * (VT_C + t - 1)) * sizeof(double);
 }
 
 // Per frame: fixed-order (deterministic) block reduction of the tile partials.
@@ -1263,8 +1303,7 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.ro = ra.rows;
   a.co = ra.cols;
   dim3 g(ntiles_max, ra.batch * ra.channels);
-  const size_t sm = 2 * size_t(ra.t_max) * ra.t_max * sizeof(double) +
-                    size_t(VT_R + ra.t_max - 1) * (VT_C + ra.t_max - 1) * sizeof(double);
+  const size_t sm = conv_smem(std::min(ra.t_max, 31), 0);  // device-side widths are <= 31 (solver limit)
   if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
   k_conv_resid<<<g, 256, sm, s>>>(a);
@@ -1290,15 +1329,15 @@ cudaError_t launch_validate_pair(const float* pub, const float* prv, int channel
   a.mode = 1;
   a.ro = rows + t - 1;
   a.co = cols + t - 1;
-  const int nt = validate_tiles(a.ro, a.co);
+  const int nt = validate_tiles(a.ro, a.co, t);
   a.ntiles = nt;
   a.part = reinterpret_cast<double2*>(part);
   cudaMemsetAsync(part, 0, sizeof(double2) * size_t(nt) * channels, s);
   dim3 g(nt, channels);
-  const size_t sm = 2 * size_t(t) * t * sizeof(double) + 2 * size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(double);
+  const size_t sm = conv_smem(t, 1);
   if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
-  k_conv_resid<<<g, 256, sm, s>>>(a);
+  k_conv_resid<<<g, conv_rows(t) * VT_C / 8, sm, s>>>(a);
   k_resid_reduce<<<1, 256, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
   return cudaGetLastError();
 }
@@ -1307,16 +1346,18 @@ cudaError_t launch_validate_pair(const float* pub, const float* prv, int channel
 // encode_frame (encoder.cpp:96-99): conv2_full(plane, k) with the reference's
 // accumulation order (kernel column outer, kernel row inner; poly.cpp:32-36) and
 // unfused multiply/add, so the FP64 result is bit-identical to the CPU restatement.
+constexpr int ENC_R = 16, ENC_C = 64;
+
 __global__ void __launch_bounds__(256) k_encode(const float* latent, int rows, int cols, int ld, const double* k,
                                                 int t, float* out, int ld_out) {
   extern __shared__ double she[];
   const int plane = blockIdx.y;
   const int ro = rows + t - 1, co = cols + t - 1;
-  const int tiles_c = (co + VT_C - 1) / VT_C;
+  const int tiles_c = (co + ENC_C - 1) / ENC_C;
   const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - tr * tiles_c;
-  const int i0 = tr * VT_R, j0 = tc * VT_C;
+  const int i0 = tr * ENC_R, j0 = tc * ENC_C;
   double* kw = she;
-  const int tw = VT_C + t - 1, th = VT_R + t - 1;
+  const int tw = ENC_C + t - 1, th = ENC_R + t - 1;
   float* tile = reinterpret_cast<float*>(kw + t * t);
   for (int i = threadIdx.x; i < t * t; i += blockDim.x) kw[i] = k[i];
   const float* X = latent + size_t(plane) * rows * ld;
@@ -1327,8 +1368,8 @@ __global__ void __launch_bounds__(256) k_encode(const float* latent, int rows, i
   }
   __syncthreads();
   float* O = out + size_t(plane) * ro * ld_out;
-  for (int e = threadIdx.x; e < VT_R * VT_C; e += blockDim.x) {
-    const int li = e / VT_C, lj = e - li * VT_C;
+  for (int e = threadIdx.x; e < ENC_R * ENC_C; e += blockDim.x) {
+    const int li = e / ENC_C, lj = e - li * ENC_C;
     const int gi = i0 + li, gj = j0 + lj;
     if (gi >= ro || gj >= co) continue;
     double acc = 0.0;
@@ -1346,9 +1387,9 @@ __global__ void __launch_bounds__(256) k_encode(const float* latent, int rows, i
 
 cudaError_t launch_encode(const float* latent, int planes, int rows, int cols, int ld, const double* k, int t,
                           float* out, int ld_out, cudaStream_t s) {
-  const int nt = validate_tiles(rows + t - 1, cols + t - 1);
+  const int nt = ((rows + t - 1 + ENC_R - 1) / ENC_R) * ((cols + t - 1 + ENC_C - 1) / ENC_C);
   dim3 g(nt, planes);
-  const size_t sm = size_t(t) * t * sizeof(double) + size_t(VT_R + t - 1) * (VT_C + t - 1) * sizeof(float);
+  const size_t sm = size_t(t) * t * sizeof(double) + size_t(ENC_R + t - 1) * (ENC_C + t - 1) * sizeof(float);
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

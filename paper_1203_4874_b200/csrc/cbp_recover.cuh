@@ -52,7 +52,7 @@ cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s);
 // validation residual (decoder.cpp:367-376) of the latent against the public frame
 cudaError_t launch_validate(const RecoverArgs& a, const float* latent, int ld_out, double* part,
                             int ntiles_max, cudaStream_t s);
-int validate_tiles(int rows, int cols);
+int validate_tiles(int rows, int cols, int t);  // t: kernel width (sets the tile height)
 
 // Standalone batched cofactor solve for the stage-level C ABI entry.
 cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, int lq, int batch, int t,
