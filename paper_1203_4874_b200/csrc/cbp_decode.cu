@@ -126,7 +126,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.ld = ld;
   a.t_max = t_max;
   a.lmax = std::max(rows, cols);
-  a.nrb = (rows + 127) / 128;
+  a.nrb = (rows + 63) / 64;  // row blocks of rows_per_block(t) <= 64 + t - 1 rows
   a.search_min = smin;
   a.search_max = smax;
   a.nsizes = smax >= smin ? (smax - smin) / 2 + 1 : 0;

@@ -46,7 +46,7 @@ cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaS
 __device__ __forceinline__ int fold_width(const RecoverArgs& a, int b, int t_fixed) {
   return t_fixed > 0 ? t_fixed : a.slots[b].width;
 }
-__device__ __forceinline__ int rows_per_block(int t) { return t * ((128 + t - 1) / t); }
+__device__ __forceinline__ int rows_per_block(int t) { return t * ((64 + t - 1) / t); }
 
 // ---------------------------------------------------- polynomial evaluation
 // Z1 fold (fft.cpp:206-208): fold[r][n] = sum_{m = r mod t} luma[m][n]. Partial sums
@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256) k_fold_z1_part(RecoverArgs a, int t_fixed
   double* out = a.part + (((size_t(b) * 2 + q) * a.nrb + rb) * a.t_max) * a.cols + n;
   for (int r = 0; r < t; ++r) {
     double acc = 0.0;
+#pragma unroll 4
     for (int m = r0 + r; m < r1; m += t) acc += luma_at(base, plane, a.channels, size_t(m) * a.ld + n);
     out[size_t(r) * a.cols] = acc;
   }
@@ -131,20 +132,24 @@ __global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
   __syncthreads();
   const int m = blockIdx.x * 4 + warp;
   if (m >= a.rows) return;
-  for (int r = 0; r < t; ++r) acc[r * 32 + lane] = 0.0;
-  __syncwarp();
+
   const size_t plane = size_t(a.rows) * a.ld;
   const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane + size_t(m) * a.ld;
-  const int step = 32 % t;
-  int r = lane % t;
+  // lane -> (residue r, part h): it sums columns r + t*(h + nh*j) in a register (no shared
+  // read-modify-write chain); the nh parts of a residue are combined below
+  const int nh = t <= 32 ? 32 / t : 1;
   bool neg = false, bad = false;
-  for (int n = lane; n < a.cols; n += 32) {
-    const double x = luma_at(base, plane, a.channels, n);
-    neg |= x < 0.0;
-    bad |= !isfinite(x);
-    acc[r * 32 + lane] += x;
-    r += step;
-    if (r >= t) r -= t;
+  for (int rr = lane; rr < t * nh; rr += 32) {
+    const int r = rr % t, h = rr / t;
+    double racc = 0.0;
+#pragma unroll 4
+    for (int n = r + t * h; n < a.cols; n += t * nh) {
+      const double x = luma_at(base, plane, a.channels, n);
+      neg |= x < 0.0;
+      bad |= !isfinite(x);
+      racc += x;
+    }
+    acc[rr] = racc;
   }
   if (__any_sync(0xffffffffu, neg) && lane == 0) atomicOr(a.flags + b, 1);
   if (__any_sync(0xffffffffu, bad) && lane == 0)
@@ -152,7 +157,7 @@ __global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
   __syncwarp();
   for (int rr = lane; rr < t; rr += 32) {
     double s = 0.0;
-    for (int l = 0; l < 32; ++l) s += acc[rr * 32 + l];
+    for (int hh = 0; hh < nh; ++hh) s += acc[hh * t + rr];
     fold[rr] = s;
   }
   __syncwarp();
@@ -1244,7 +1249,8 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
 
 __host__ inline size_t conv_smem(int t, int mode) {
   const int tp = conv_pad(t);
-  return (mode == 1 ? 2 : 1) * (size_t(t) * tp + size_t(conv_rows(t) + tp - 1) * (VT_C + t - 1)) * sizeof(double);
+  // both weight blocks are always carved (the kernel lays the tile out after them)
+  return (size_t(2) * t * tp + (mode == 1 ? 2 : 1) * size_t(conv_rows(t) + tp - 1) * (VT_C + t - 1)) * sizeof(double);
 }
 
 // Per frame: fixed-order (deterministic) block reduction of the tile partials.
