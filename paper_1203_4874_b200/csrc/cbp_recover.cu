@@ -114,32 +114,26 @@ __global__ void __launch_bounds__(128) k_fold_z1_dft(RecoverArgs a, int t_fixed)
   }
 }
 
-// Z2 fold (fft.cpp:210-212) with one warp per row, then its DFT epilogue. Also flags
-// negative luma (decoder.cpp:52) and non-finite samples (image.cpp:33).
-// grid (ceil(rows/4), batch*2), block 128, smem 4 warps * t_max * 33 doubles + roots.
+// Z2 fold (fft.cpp:210-212), one 128-thread CTA per row: thread -> (residue r, part h) sums
+// columns r + t*(h + nh*j) in a register; the nh parts are combined in a fixed order, then
+// the t-point DFT epilogue. Also flags negative luma (decoder.cpp:52) and non-finite
+// samples (image.cpp:33). grid (rows, batch*2).
 __global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
-  extern __shared__ double sh[];
+  __shared__ double2 root[CBP_MAX_WIDTH];
+  __shared__ double acc[128 + CBP_MAX_WIDTH];
+  __shared__ double fold[CBP_MAX_WIDTH];
   const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
   cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0) return;
   const int t = fold_width(a, b, t_fixed);
   if (t <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* root = reinterpret_cast<double2*>(sh);
-  double* acc = sh + 2 * a.t_max + size_t(warp) * a.t_max * 33;
-  double* fold = acc + size_t(a.t_max) * 32;
   for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
-  __syncthreads();
-  const int m = blockIdx.x * 4 + warp;
-  if (m >= a.rows) return;
-
+  const int m = blockIdx.x;
   const size_t plane = size_t(a.rows) * a.ld;
   const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane + size_t(m) * a.ld;
-  // lane -> (residue r, part h): it sums columns r + t*(h + nh*j) in a register (no shared
-  // read-modify-write chain); the nh parts of a residue are combined below
-  const int nh = t <= 32 ? 32 / t : 1;
+  const int nh = t <= 128 ? 128 / t : 1;
   bool neg = false, bad = false;
-  for (int rr = lane; rr < t * nh; rr += 32) {
+  for (int rr = threadIdx.x; rr < t * nh; rr += blockDim.x) {
     const int r = rr % t, h = rr / t;
     double racc = 0.0;
 #pragma unroll 4
@@ -151,18 +145,20 @@ __global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
     }
     acc[rr] = racc;
   }
-  if (__any_sync(0xffffffffu, neg) && lane == 0) atomicOr(a.flags + b, 1);
-  if (__any_sync(0xffffffffu, bad) && lane == 0)
-    slot_fail(slot, CBP_RANGE_EXCEEDED, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_NONFINITE);
-  __syncwarp();
-  for (int rr = lane; rr < t; rr += 32) {
+  neg = __syncthreads_or(neg);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (neg) atomicOr(a.flags + b, 1);
+    if (bad) slot_fail(slot, CBP_RANGE_EXCEEDED, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_NONFINITE);
+  }
+  for (int rr = threadIdx.x; rr < t; rr += blockDim.x) {
     double s = 0.0;
     for (int hh = 0; hh < nh; ++hh) s += acc[hh * t + rr];
     fold[rr] = s;
   }
-  __syncwarp();
+  __syncthreads();
   double2* out = a.slices + slice_offset(a, b, 1, q, 0) + m;
-  for (int i = lane; i < t; i += 32) {
+  for (int i = threadIdx.x; i < t; i += blockDim.x) {
     double re = 0.0, im = 0.0;
     int idx = 0;
     for (int rr = 0; rr < t; ++rr) {
@@ -181,7 +177,6 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
     cudaFuncSetAttribute(k_fold_z1_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(k_fold_z2, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cfg = true;
   }
   dim3 g1((a.cols + 255) / 256, a.nrb, a.batch * 2);
@@ -189,9 +184,8 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
   dim3 g2((a.cols + 127) / 128, a.batch * 2);
   size_t sm2 = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
   k_fold_z1_dft<<<g2, 128, sm2, s>>>(b, t_fixed);
-  dim3 g3((a.rows + 3) / 4, a.batch * 2);
-  size_t sm3 = (2 * a.t_max + 4 * size_t(a.t_max) * 33) * sizeof(double);
-  k_fold_z2<<<g3, 128, sm3, s>>>(b, t_fixed);
+  dim3 g3(a.rows, a.batch * 2);
+  k_fold_z2<<<g3, 128, 0, s>>>(b, t_fixed);
   (void)tm;
   return cudaGetLastError();
 }
