@@ -84,7 +84,7 @@ __device__ __forceinline__ void phase_mark(int i, bool who) {
 }
 #define CBP_PHASE(i, who) ::cbp_dev::phase_mark((i), (who))
 #else
-#define CBP_PHASE(i, who) ((void)0)
+#define CBP_PHASE(i, who) ((void)(who))
 #endif
 
 }  // namespace cbp_dev

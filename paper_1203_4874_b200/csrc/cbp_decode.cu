@@ -155,6 +155,8 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   const size_t o_ratios = take(B * 2 * std::max(a.nsizes, 1) * sizeof(double));
   const size_t o_flags = take(B * sizeof(int));
   const size_t o_vpart = take(B * channels * std::max(P.vtiles, 1) * sizeof(double2) + 64);
+  const size_t o_roots = take(size_t(rows + cols) * sizeof(double2));
+  const size_t o_epart = take(signed_energy_doubles(batch, rows, cols) * sizeof(double));
   char* base = static_cast<char*>(workspace(ctx, WS_MISC, off));
   if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   a.part = reinterpret_cast<double*>(base + o_part);
@@ -166,6 +168,9 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.ratios = reinterpret_cast<double*>(base + o_ratios);
   a.flags = reinterpret_cast<int*>(base + o_flags);
   P.vpart = reinterpret_cast<double*>(base + o_vpart);
+  a.roots = reinterpret_cast<double2*>(base + o_roots);
+  a.epart = reinterpret_cast<double*>(base + o_epart);
+  a.epart_z2 = size_t(batch) * 2 * ((cols + 31) / 32) * (rows / 2 + 1);  // z1 part (cbp_signed.cu)
   return 0;
 }
 
@@ -235,6 +240,7 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
   cudaError_t e = launch_init_slots(a, hints, s);
   ctx->launches += (batch + HintChunk::kMax - 1) / HintChunk::kMax;
   if (e == cudaSuccess && need_est) e = launch_fold(a, 1, s);  // DC slices (decoder.cpp:58-64)
+  if (e == cudaSuccess && need_est) e = launch_signed_slices(a, s);  // signed content (65-82)
   if (e == cudaSuccess && need_est) e = launch_width(a, s);
   if (need_est) ctx->launches += 5;
   if (record_events) cudaEventRecord(ctx->ev[1], s);
@@ -352,6 +358,7 @@ int cbp_estimate_kernel_width(cbp_ctx* ctx, const float* pub_dev, const float* p
   P.a.slots = slots;
   cudaError_t e = launch_init_slots(P.a, nullptr, s);
   if (e == cudaSuccess) e = launch_fold(P.a, 1, s);
+  if (e == cudaSuccess) e = launch_signed_slices(P.a, s);
   if (e == cudaSuccess) e = launch_width(P.a, s);
   if ((st = cuda_check(ctx, e, "width launch"))) return st;
   cbp_kernel_slot* h = pinned<cbp_kernel_slot>(ctx, 1);

@@ -130,7 +130,6 @@ __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, Jac
 __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, bool vectors = true) {
   __shared__ double s_d[64], s_e[64], s_beta[64], s_rc[64], s_rs[64];
   __shared__ double2 s_ec[64], s_w[64], s_p[64], s_delta[64];
-  __shared__ int s_ctl[4];
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   auto wsum = [&](double v) {

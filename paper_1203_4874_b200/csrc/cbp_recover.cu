@@ -200,7 +200,6 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
   const int si = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
   const cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0 || slot->width > 0) return;  // failed or hinted
-  if (a.flags[b] & 1) return;                         // signed content: see k_width_pick
   const int s = a.search_min + 2 * si;
   if (s > a.search_max) return;
   CBP_PHASE(0, blockIdx.x == gridDim.x - 1 && blockIdx.y == 0 && blockIdx.z == 0);
@@ -267,10 +266,6 @@ __global__ void __launch_bounds__(128) k_width_pick(RecoverArgs a) {
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  if (a.flags[b] & 1) {  // signed content -> axis_spectrum_half path (decoder.cpp:65-82)
-    slot_fail(slot, CBP_UNSUPPORTED, CBP_STAGE_KERNEL_DEGREE_ESTIMATION, -1, -1, 0.0, CBP_REASON_SIGNED);
-    return;
-  }
   int w[2];
   bool cl[2];
   for (int axis = 0; axis < 2; ++axis) {

@@ -25,6 +25,9 @@ struct RecoverArgs {
   double2* scratch;   // [batch][2 axes][t_max][lmax + t_max] residual vectors
   // width search
   double* ratios;     // [batch][2][nsizes]
+  double2* roots;     // signed content: exp(-2 pi i k / rows) then exp(-2 pi i k / cols)
+  double* epart;      // signed content: per-tile energy partials, z1 then z2 (at epart_z2)
+  size_t epart_z2;
   int search_min, search_max, nsizes;
   double tau;
   int trust_hint;
@@ -47,6 +50,10 @@ cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaS
 // t_fixed > 0 folds with that t (1 = DC sums); otherwise with slots[b].width.
 cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s);
 cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s);
+// signed content (decoder.cpp:65-82): replaces the DC slices of frames with a negative
+// luma sample by the maximum-energy axis_spectrum_half slices (cbp_signed.cu)
+cudaError_t launch_signed_slices(const RecoverArgs& a, cudaStream_t s);
+size_t signed_energy_doubles(int batch, int rows, int cols);
 cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s);
 cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s);
 // validation residual (decoder.cpp:367-376) of the latent against the public frame

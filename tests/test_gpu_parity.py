@@ -97,6 +97,25 @@ def test_decode_frame_parity(oracle, api, rows, cols, ch, t, lo, hi, hint, trust
     assert krel(d.kernel_estimate, pair.k1) <= 1e-4
 
 
+@pytest.mark.parametrize("rows,cols,ch,t,lo,hi", [
+    (64, 64, 1, 5, 3, 9),
+    (61, 97, 3, 7, 3, 25),     # RGB, odd extents (prime factors 61, 97 in the axis DFTs)
+    (96, 128, 1, 9, 3, 25),
+])
+def test_decode_signed_content_parity(oracle, api, rows, cols, ch, t, lo, hi):
+    """Signed latents: width estimation takes the maximum-energy axis_spectrum_half slices
+    (decoder.cpp:65-82) instead of the DC sums."""
+    lat = oracle.random_frame(rows, cols, ch, oracle.frame_seed(3, rows + t)) - 0.5
+    pair = oracle.generate_coprime_pair(t, oracle.frame_seed(4, cols + t))
+    pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+    pub, prv = pub.astype(np.float32), prv.astype(np.float32)
+    w = api.estimate_kernel_width(torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda(), lo, hi, 1e-6)
+    ref_w = oracle.estimate_kernel_width(pub.astype(np.float64), prv.astype(np.float64), lo, hi, 1e-6)
+    assert w == ref_w == (t, False)
+    d, _ = check_decode(oracle, api, lat, pub, prv, lo, hi)
+    assert krel(d.kernel_estimate, pair.k1) <= 1e-4
+
+
 def test_decode_1080p_rgb_parity(oracle, api):
     """BASELINE config 3 frame at full size: 1920x1080 RGB, t = 11."""
     lat, pair, pub, prv = make(oracle, 1080, 1920, 3, 11, oracle.frame_seed(1, 0), oracle.frame_seed(2, 0))

@@ -559,3 +559,20 @@ def test_acceptance_1_reconstruction_subset(oracle):
             pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
             d = oracle.decode_frame(pub, prv, cfg=oracle.make_cfg(3, 9))
             assert oracle.psnr(lat, d.latent) >= 40.0 and d.validation_residual <= 1e-4
+
+
+def test_signed_content_width_and_decode(oracle):
+    """Signed latents (decoder.cpp:65-82): the maximum-energy axis_spectrum_half slices
+    carry the planted width; the decode reconstructs (the reference's planted-width and
+    round-trip checks, decoder_test.cpp:40-83, 311-331, on zero-mean content)."""
+    for rows, cols, t, hi in ((64, 64, 5, 9), (96, 128, 9, 25)):
+        lat = oracle.random_frame(rows, cols, 1, oracle.frame_seed(3, rows + t)) - 0.5
+        pair = oracle.generate_coprime_pair(t, oracle.frame_seed(4, cols + t))
+        pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+        assert oracle.estimate_kernel_width(pub, prv, 3, hi, 1e-6) == (t, False)
+        d = oracle.decode_frame(pub, prv, cfg=oracle.make_cfg(3, hi))
+        assert d.width_used == t and oracle.psnr(lat, d.latent) >= 40.0
+        # the spectra the slices come from: axis_spectrum_half == numpy rfft along the axis
+        luma = pub[0]
+        np.testing.assert_allclose(oracle.axis_spectrum_half(luma, 0), np.fft.rfft(luma, axis=0), rtol=0, atol=1e-10)
+        np.testing.assert_allclose(oracle.axis_spectrum_half(luma, 1), np.fft.rfft(luma, axis=1), rtol=0, atol=1e-10)
