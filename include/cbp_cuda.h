@@ -241,6 +241,33 @@ int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_
                         int channels, int rows, int cols, const int* recover, int width_hint,
                         const cbp_decode_cfg* cfg, float* latent, cbp_kernel_slot* slots_host);
 
+/* ---- quantized-stream tier (encoder.cpp:105-139) ---------------------------------
+ * Quantized frames are integer codes k (uint8 for bits = 8, uint16 for bits = 16) with
+ * value k / (2^bits - 1): the device form of the reference's u8/u16 frames.
+ * cbp_quantize_frames: k = round(clamp(x, 0, 1) * maxv) (quantize_frame, encoder.cpp:105-120);
+ *   CBP_RANGE_EXCEEDED ("samples outside [0,1]") if a sample lies outside [-1e-9, 1+1e-9].
+ *   Synchronizes (the range check is reported on the host).
+ * cbp_dequantize_frames: float(k / maxv) into FP32 frames (async).
+ * cbp_degrade_bits: k & ~(2^drop - 1) in place, drop in [0, bits) (degrade_bits,
+ *   encoder.cpp:124-139; async).
+ * cbp_decode_frames_q: cbp_decode_frames on quantized device frames (dequantized into
+ *   context workspaces first; same results as decoding the dequantized FP32 values).
+ * cbp_decode_run_host_q: cbp_decode_run_host with host codes: PCIe carries 1 or 2 bytes per
+ *   sample, dequantization runs on the device. */
+int cbp_quantize_frames(cbp_ctx* ctx, const float* in_dev, int planes, int rows, int cols, int ld, int bits,
+                        void* codes_dev, int ld_codes, void* stream);
+int cbp_dequantize_frames(cbp_ctx* ctx, const void* codes_dev, int bits, int planes, int rows, int cols,
+                          int ld_codes, float* out_dev, int ld, void* stream);
+int cbp_degrade_bits(cbp_ctx* ctx, void* codes_dev, int bits, int planes, int rows, int cols, int ld_codes,
+                     int drop, void* stream);
+int cbp_decode_frames_q(cbp_ctx* ctx, const void* pub_codes, const void* prv_codes, int bits, int batch,
+                        int channels, int rows, int cols, int ld_codes, const int* width_hints,
+                        const cbp_decode_cfg* cfg, float* latent_dev, int ld_out, cbp_decode_info* info,
+                        void* stream);
+int cbp_decode_run_host_q(cbp_ctx* ctx, const void* pub_codes, const void* prv_codes, int bits, int n_frames,
+                          int channels, int rows, int cols, const int* recover, int width_hint,
+                          const cbp_decode_cfg* cfg, float* latent, cbp_kernel_slot* slots_host);
+
 /* ---- reference-exact input generators (host; untimed) ------------------------
  * frame_seed / splitmix64 (rng.hpp:8-29), random_frame (synth.cpp:12-22: mt19937_64,
  * column-major draw, returned row-major FP32), coprimality_check and

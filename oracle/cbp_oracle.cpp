@@ -684,6 +684,23 @@ Frame quantize_frame(const Frame& f, int bits) {  // encoder.cpp:105-120
   return out;
 }
 
+Frame degrade_bits(const Frame& f, int drop) {  // encoder.cpp:124-139
+  validate_frame(f);
+  require(f.bit_depth != 0, Errc::not_quantized, "bit-precision degradation needs a quantized frame");
+  const int bits = f.bit_depth;
+  require(drop >= 0 && drop < bits, Errc::invalid_argument, "drop must lie in [0, bit width)");
+  if (drop == 0) return f;
+  const double maxv = double((1u << bits) - 1);
+  const std::uint32_t mask = ~((1u << drop) - 1u);
+  Frame out = f;
+  for (auto& plane : out.planes)
+    for (double& x : plane.v) {
+      const auto k = static_cast<std::uint32_t>(std::lround(x * maxv));
+      x = double(k & mask) / maxv;
+    }
+  return out;
+}
+
 // ------------------------------------------------------------- decoder.cpp
 namespace {
 using Clock = std::chrono::steady_clock;

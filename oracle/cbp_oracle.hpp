@@ -145,6 +145,7 @@ CoprimePair generate_coprime_pair(int width, uint64_t seed, int max_retries = 16
                                   double margin_threshold = 1e-6, int trials = 4);
 BlurredPair encode_frame(const Frame& latent, const CoprimePair& pair);
 Frame quantize_frame(const Frame& f, int bits);
+Frame degrade_bits(const Frame& f, int drop);
 
 // ---- decoder.hpp ----
 struct DecodeConfig {

@@ -184,6 +184,15 @@ def quantize(planes, bits: int) -> np.ndarray:
     return x
 
 
+def degrade_bits(planes, bits: int, drop: int) -> np.ndarray:
+    """encoder.cpp:124-139 on frames quantized to `bits` (values k / (2^bits - 1))."""
+    x = _f64(planes).copy()
+    if x.ndim == 2:
+        x = x[None]
+    _check(lib().orc_degrade_bits(_p(x), x.shape[0], x.shape[1], x.shape[2], bits, drop))
+    return x
+
+
 # ----------------------------------------------------------------------- poly
 def bezout_leading_block(p, q, size: int) -> np.ndarray:
     p = _c128(p); q = _c128(q)

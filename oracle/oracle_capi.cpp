@@ -134,6 +134,16 @@ int orc_quantize(double* planes, int channels, int rows, int cols, int bits) {
   });
 }
 
+// degrade_bits on frames quantized to `bits` (values k / (2^bits - 1))
+int orc_degrade_bits(double* planes, int channels, int rows, int cols, int bits, int drop) {
+  return guard([&] {
+    Frame f = frame_in(planes, channels, rows, cols);
+    f.bit_depth = bits;
+    Frame d = degrade_bits(f, drop);
+    for (int k = 0; k < channels; ++k) mat_out(d.planes[k], planes + size_t(k) * rows * cols);
+  });
+}
+
 int orc_bezout_leading_block(const double* p, int lp, const double* q, int lq, int size,
                              double* out) {
   return guard([&] { cmat_out(bezout_leading_block(cvec_in(p, lp), cvec_in(q, lq), size), out); });

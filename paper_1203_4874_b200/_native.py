@@ -95,6 +95,11 @@ _SIGS = {
     "cbp_encode_frames": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _I, _P]),
     "cbp_synth_frames": (_I, [_P, _P, _I, _I, _I, _I, C.c_uint64, _P]),
     "cbp_decode_run_host": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _P, _P]),
+    "cbp_decode_run_host_q": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P]),
+    "cbp_quantize_frames": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P]),
+    "cbp_dequantize_frames": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P]),
+    "cbp_degrade_bits": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "cbp_decode_frames_q": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P]),
     "cbp_frame_seed": (C.c_uint64, [C.c_uint64, _I]),
     "cbp_splitmix64": (C.c_uint64, [C.c_uint64]),
     "cbp_random_frame": (_I, [_I, _I, _I, C.c_uint64, _P]),

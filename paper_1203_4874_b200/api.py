@@ -169,6 +169,97 @@ def decode_frame(pub, prv, hint: int | None = None, cfg: DecodeCfg | None = None
     return decode_frames(pub, prv, None if hint is None else [hint], cfg)[0]
 
 
+# ------------------------------------------------------ quantized-stream tier
+_QDTYPE = {8: torch.uint8, 16: torch.uint16}
+
+
+def _bits_of(codes: torch.Tensor) -> int:
+    for bits, dt in _QDTYPE.items():
+        if codes.dtype == dt:
+            return bits
+    raise CbpError(1, "InvalidArgument: quantized frames must be uint8 or uint16 codes")
+
+
+def _dev_codes(x) -> torch.Tensor:
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    x = x.to(device=torch.device("cuda", torch.cuda.current_device()))
+    if x.dim() == 2:
+        x = x.unsqueeze(0)
+    return x.contiguous()
+
+
+def quantize_frames(frames, bits: int) -> torch.Tensor:
+    """cbp::quantize_frame (encoder.cpp:105-120) on the device: integer codes
+    k = round(clamp(x, 0, 1) * (2^bits - 1)) as uint8 / uint16; RangeExceeded outside [0, 1]."""
+    X = _dev_planes(frames)
+    if bits not in _QDTYPE:
+        raise CbpError(1, "InvalidArgument: quantization depth must be u8 or u16")
+    rows, cols = X.shape[-2:]
+    planes = X.numel() // (rows * cols)
+    out = torch.empty(X.shape, dtype=_QDTYPE[bits], device=X.device)
+    ctx = context(X.device.index)
+    ctx.check(N.lib().cbp_quantize_frames(ctx.ptr, C.c_void_p(X.data_ptr()), planes, rows, cols, cols, bits,
+                                          C.c_void_p(out.data_ptr()), cols, _stream_ptr(X.device)))
+    return out
+
+
+def dequantize_frames(codes) -> torch.Tensor:
+    """FP32 frames float(k / (2^bits - 1)) from uint8 / uint16 codes."""
+    Q = _dev_codes(codes)
+    bits = _bits_of(Q)
+    rows, cols = Q.shape[-2:]
+    planes = Q.numel() // (rows * cols)
+    out = torch.empty(Q.shape, dtype=torch.float32, device=Q.device)
+    ctx = context(Q.device.index)
+    ctx.check(N.lib().cbp_dequantize_frames(ctx.ptr, C.c_void_p(Q.data_ptr()), bits, planes, rows, cols, cols,
+                                            C.c_void_p(out.data_ptr()), cols, _stream_ptr(Q.device)))
+    return out
+
+
+def degrade_bits(codes, drop: int) -> torch.Tensor:
+    """cbp::degrade_bits (encoder.cpp:124-139) on codes: k & ~(2^drop - 1) (returns a copy)."""
+    Q = _dev_codes(codes).clone()
+    bits = _bits_of(Q)
+    rows, cols = Q.shape[-2:]
+    planes = Q.numel() // (rows * cols)
+    ctx = context(Q.device.index)
+    ctx.check(N.lib().cbp_degrade_bits(ctx.ptr, C.c_void_p(Q.data_ptr()), bits, planes, rows, cols, cols, int(drop),
+                                       _stream_ptr(Q.device)))
+    return Q
+
+
+def decode_frames_q(pub_codes, prv_codes, hints=None, cfg: DecodeCfg | None = None) -> list[DecodedFrame]:
+    """Batched decode_frame of quantized pairs (uint8 / uint16 codes, batch x ch x rows x cols)."""
+    P = _dev_codes(pub_codes)
+    Q = _dev_codes(prv_codes)
+    if P.dim() == 3:
+        P, Q = P.unsqueeze(0), Q.unsqueeze(0)
+    if P.shape != Q.shape or P.dtype != Q.dtype:
+        raise CbpError(13, "DimMismatch: pair frames disagree on dimensions")
+    bits = _bits_of(P)
+    B, ch, rows, cols = P.shape
+    cfg = cfg or make_cfg()
+    ctx = context(P.device.index)
+    out = torch.empty((B, ch, rows, cols), dtype=torch.float32, device=P.device)
+    hint_arr = None
+    if hints is not None:
+        hs = [hints] * B if np.isscalar(hints) else list(hints)
+        hint_arr = (C.c_int * B)(*[int(h) if h is not None else 0 for h in hs])
+    infos = (DecodeInfo * max(B, 1))()
+    ctx.check(N.lib().cbp_decode_frames_q(ctx.ptr, C.c_void_p(P.data_ptr()), C.c_void_p(Q.data_ptr()), bits, B, ch,
+                                          rows, cols, cols, hint_arr, C.byref(cfg), C.c_void_p(out.data_ptr()),
+                                          cols, infos, _stream_ptr(P.device)))
+    res = []
+    for b in range(B):
+        inf = infos[b]
+        t = inf.width_used
+        k = np.array(inf.kernel[: t * t]).reshape(t, t)
+        res.append(DecodedFrame(out[b, :, : rows - t + 1, : cols - t + 1], k, t, bool(inf.width_clamped),
+                                StageTimings(*list(inf.stage_ms)), inf.validation_residual, inf.epsilon_used))
+    return res
+
+
 def estimate_kernel_width(pub, prv, search_min: int, search_max: int, tau: float) -> tuple[int, bool]:
     """cbp::estimate_kernel_width (decoder.hpp:29-30) -> (width, clamped)."""
     P, _ = _as_batch(pub)
@@ -370,22 +461,28 @@ def generate_coprime_pair(width: int, seed: int, max_retries: int = 16, margin_t
 
 def decode_run_host(pub: torch.Tensor, prv: torch.Tensor, recover, cfg: DecodeCfg | None = None,
                     width_hint: int = 0, out: torch.Tensor | None = None, device: int | None = None):
-    """Host-buffer run decode (the end-to-end path): pub/prv are CPU float32 tensors
-    (n, channels, rows, cols), ideally pinned; returns (latent CPU tensor in the input
-    geometry, list of KernelSlot for the recovery frames)."""
-    assert pub.device.type == "cpu" and pub.dtype == torch.float32 and pub.is_contiguous()
+    """Host-buffer run decode (the end-to-end path): pub/prv are CPU float32 tensors, or
+    uint8 / uint16 quantized codes, (n, channels, rows, cols), ideally pinned; returns
+    (latent CPU float32 tensor in the input geometry, list of KernelSlot for the recovery
+    frames)."""
+    assert pub.device.type == "cpu" and pub.is_contiguous()
     n, ch, rows, cols = pub.shape
     rec = np.ascontiguousarray(np.asarray(recover, np.int32))
     cfg = cfg or make_cfg()
     if out is None:
-        out = torch.empty_like(pub, pin_memory=pub.is_pinned())
+        out = torch.empty(pub.shape, dtype=torch.float32, pin_memory=pub.is_pinned())
     nrec = int((rec != 0).sum())
     slots = (KernelSlot * max(nrec, 1))()
     ctx = context(device)
-    ctx.check(N.lib().cbp_decode_run_host(ctx.ptr, C.c_void_p(pub.data_ptr()),
-                                          C.c_void_p(prv.data_ptr()) if prv is not None else None, n, ch, rows,
-                                          cols, rec.ctypes.data_as(C.c_void_p), int(width_hint), C.byref(cfg),
-                                          C.c_void_p(out.data_ptr()), slots))
+    prv_p = C.c_void_p(prv.data_ptr()) if prv is not None else None
+    if pub.dtype == torch.float32:
+        ctx.check(N.lib().cbp_decode_run_host(ctx.ptr, C.c_void_p(pub.data_ptr()), prv_p, n, ch, rows, cols,
+                                              rec.ctypes.data_as(C.c_void_p), int(width_hint), C.byref(cfg),
+                                              C.c_void_p(out.data_ptr()), slots))
+    else:  # quantized codes: 1 or 2 bytes per sample over PCIe, dequantized on the device
+        ctx.check(N.lib().cbp_decode_run_host_q(ctx.ptr, C.c_void_p(pub.data_ptr()), prv_p, _bits_of(pub), n, ch,
+                                                rows, cols, rec.ctypes.data_as(C.c_void_p), int(width_hint),
+                                                C.byref(cfg), C.c_void_p(out.data_ptr()), slots))
     return out, [slots[i] for i in range(nrec)]
 
 

@@ -42,6 +42,10 @@ enum Workspace {
   WS_PRV = 8,
   WS_OUT = 9,
   WS_RED = 10,    // validation partial sums
+  // 11, 12: Wiener filter tables (WS_RED + 1, WS_RED + 2)
+  WS_QPUB = 13,   // dequantized frames (cbp_decode_frames_q)
+  WS_QPRV = 14,
+  WS_QCODES = 15, // host-pipeline code rings (cbp_decode_run_host_q)
 };
 
 const char* errc_name(int status);

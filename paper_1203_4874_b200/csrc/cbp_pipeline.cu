@@ -47,10 +47,21 @@ int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv
 int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels, int rows, int cols,
                              int ld, const cbp_kernel_slot* slot_dev, float* latent_dev, int ld_out, void* stream);
 
-int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames, int channels, int rows,
-                        int cols, const int* recover, int width_hint, const cbp_decode_cfg* cfg, float* latent,
-                        cbp_kernel_slot* slots_host) {
+int cbp_dequantize_frames(cbp_ctx* ctx, const void* codes_dev, int bits, int planes, int rows, int cols,
+                          int ld_codes, float* out_dev, int ld, void* stream);
+
+}  // extern "C"
+
+namespace {
+
+// bits = 0: FP32 host frames; 8 / 16: quantized codes (uint8 / uint16), copied as codes and
+// dequantized on the device (cbp_quant.cu), so PCIe carries 1 or 2 bytes per sample.
+int run_host(cbp_ctx* ctx, const void* pub, const void* prv, int bits, int n_frames, int channels, int rows,
+             int cols, const int* recover, int width_hint, const cbp_decode_cfg* cfg, float* latent,
+             cbp_kernel_slot* slots_host) {
   if (!ctx || !pub || !recover || !cfg || !latent) return CBP_INVALID_ARGUMENT;
+  if (bits != 0 && bits != 8 && bits != 16)
+    return set_error(ctx, CBP_INVALID_ARGUMENT, "quantization depth must be u8 or u16");
   if (n_frames <= 0) return 0;
   if (!recover[0]) return set_error(ctx, CBP_INVALID_ARGUMENT, "the first frame of a run must recover the kernel");
   int n_rec = 0;
@@ -58,22 +69,34 @@ int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_
   if (n_rec > 0 && !prv) return set_error(ctx, CBP_INVALID_ARGUMENT, "recovery frames need the private stream");
   Pipe& P = pipe_of(ctx);
   const size_t frame = size_t(channels) * rows * cols;
+  const size_t esz = bits == 0 ? sizeof(float) : bits == 8 ? 1 : 2;
   float* dpub = static_cast<float*>(workspace(ctx, WS_PUB, sizeof(float) * frame * kRing));
   float* dprv = static_cast<float*>(workspace(ctx, WS_PRV, sizeof(float) * frame * kRing));
   float* dout = static_cast<float*>(workspace(ctx, WS_OUT, sizeof(float) * frame * kRing));
+  char* codes = bits ? static_cast<char*>(workspace(ctx, WS_QCODES, esz * frame * kRing * 2)) : nullptr;
   cbp_kernel_slot* slots = static_cast<cbp_kernel_slot*>(workspace(ctx, WS_SOLVE, sizeof(cbp_kernel_slot) * n_rec));
-  if (!dpub || !dprv || !dout || !slots) return set_error(ctx, CBP_CUDA_ERROR, "pipeline allocation failed");
+  if (!dpub || !dprv || !dout || !slots || (bits && !codes))
+    return set_error(ctx, CBP_CUDA_ERROR, "pipeline allocation failed");
+  const char* hpub = static_cast<const char*>(pub);
+  const char* hprv = static_cast<const char*>(prv);
   int rec = -1;
   const int hint = width_hint;
   for (int j = 0; j < n_frames; ++j) {
     const int r = j % kRing;
     if (j >= kRing) cudaStreamWaitEvent(P.h2d, P.out[r], 0);  // ring slot drained
-    cudaMemcpyAsync(dpub + r * frame, pub + j * frame, sizeof(float) * frame, cudaMemcpyHostToDevice, P.h2d);
-    if (recover[j])
-      cudaMemcpyAsync(dprv + r * frame, prv + j * frame, sizeof(float) * frame, cudaMemcpyHostToDevice, P.h2d);
+    char* cpub = bits ? codes + esz * frame * r : reinterpret_cast<char*>(dpub + r * frame);
+    char* cprv = bits ? codes + esz * frame * (kRing + r) : reinterpret_cast<char*>(dprv + r * frame);
+    cudaMemcpyAsync(cpub, hpub + esz * frame * j, esz * frame, cudaMemcpyHostToDevice, P.h2d);
+    if (recover[j]) cudaMemcpyAsync(cprv, hprv + esz * frame * j, esz * frame, cudaMemcpyHostToDevice, P.h2d);
     cudaEventRecord(P.in[r], P.h2d);
     cudaStreamWaitEvent(P.comp, P.in[r], 0);
-    int st;
+    int st = 0;
+    if (bits) {
+      st = cbp_dequantize_frames(ctx, cpub, bits, channels, rows, cols, cols, dpub + r * frame, cols, P.comp);
+      if (!st && recover[j])
+        st = cbp_dequantize_frames(ctx, cprv, bits, channels, rows, cols, cols, dprv + r * frame, cols, P.comp);
+      if (st) return st;
+    }
     if (recover[j]) {
       ++rec;
       st = cbp_decode_frames_async(ctx, dpub + r * frame, dprv + r * frame, 1, channels, rows, cols, cols,
@@ -97,6 +120,25 @@ int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_
   for (int k = 0; k < n_rec; ++k)
     if (hs[k].status) return set_error(ctx, hs[k].status, "recovery frame " + std::to_string(k) + " failed");
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames, int channels, int rows,
+                        int cols, const int* recover, int width_hint, const cbp_decode_cfg* cfg, float* latent,
+                        cbp_kernel_slot* slots_host) {
+  return run_host(ctx, pub, prv, 0, n_frames, channels, rows, cols, recover, width_hint, cfg, latent, slots_host);
+}
+
+int cbp_decode_run_host_q(cbp_ctx* ctx, const void* pub_codes, const void* prv_codes, int bits, int n_frames,
+                          int channels, int rows, int cols, const int* recover, int width_hint,
+                          const cbp_decode_cfg* cfg, float* latent, cbp_kernel_slot* slots_host) {
+  if (bits != 8 && bits != 16) return ctx ? set_error(ctx, CBP_INVALID_ARGUMENT, "quantization depth must be u8 or u16")
+                                          : CBP_INVALID_ARGUMENT;
+  return run_host(ctx, pub_codes, prv_codes, bits, n_frames, channels, rows, cols, recover, width_hint, cfg, latent,
+                  slots_host);
 }
 
 }  // extern "C"

@@ -407,3 +407,87 @@ def test_acceptance_1_on_gpu(oracle, api):
             assert d.width_used == t
             assert oracle.psnr(lat, d.latent.cpu().numpy().astype(np.float64)) >= 40.0
             assert d.validation_residual <= 1e-4
+
+
+# ------------------------------------------------------------ quantized-stream tier
+def test_quantize_degrade_on_device(oracle, api):
+    """Device codes match the reference's quantize_frame / degrade_bits (encoder_test.cpp:170-215)."""
+    half = torch.full((1, 2, 2), 0.5, device="cuda")
+    assert int(api.quantize_frames(half, 8)[0, 0, 0]) == 128
+    assert int(api.quantize_frames(half, 16)[0, 0, 0]) == 32768
+    for bad in (1.1, -0.5):
+        with pytest.raises(api.CbpError) as e:
+            api.quantize_frames(torch.full((1, 2, 2), bad, device="cuda"), 8)
+        assert e.value.status == 7 and "samples outside [0,1]" in str(e.value)
+    x = oracle.random_frame(37, 53, 3, oracle.frame_seed(7, 1)).astype(np.float32)
+    for bits in (8, 16):
+        codes = api.quantize_frames(torch.from_numpy(x).cuda(), bits).cpu().numpy().astype(np.int64)
+        ref = oracle.quantize(x.astype(np.float64), bits) * ((1 << bits) - 1)
+        assert np.array_equal(codes, np.rint(ref).astype(np.int64))
+        for drop in (0, 1, 3, bits - 1):
+            got = api.degrade_bits(api.quantize_frames(torch.from_numpy(x).cuda(), bits), drop)
+            deg = oracle.degrade_bits(ref / ((1 << bits) - 1), bits, drop) * ((1 << bits) - 1)
+            assert np.array_equal(got.cpu().numpy().astype(np.int64), np.rint(deg).astype(np.int64))
+        deq = api.dequantize_frames(api.quantize_frames(torch.from_numpy(x).cuda(), bits)).cpu().numpy()
+        assert np.array_equal(deq, (ref / ((1 << bits) - 1)).astype(np.float32))
+    with pytest.raises(api.CbpError):
+        api.degrade_bits(api.quantize_frames(half, 8), 8)
+
+
+@pytest.mark.parametrize("bits,ch", [(16, 1), (8, 3)])
+def test_decode_quantized_parity(oracle, api, bits, ch):
+    """decoder_test.cpp:427-439 (u16 decode) through device codes: decode of the codes equals
+    the oracle decode of the same dequantized FP32 values."""
+    rows, cols, t = 64, 64, 5
+    lat, pair, pub, prv = make(oracle, rows, cols, ch, t, oracle.frame_seed(1, 77), oracle.frame_seed(2, 77))
+    qp = api.quantize_frames(torch.from_numpy(pub).cuda(), bits)
+    qq = api.quantize_frames(torch.from_numpy(prv).cuda(), bits)
+    d = api.decode_frames_q(qp, qq, hints=[t], cfg=api.make_cfg(3, 9, trust_hint=True))[0]
+    fp = api.dequantize_frames(qp).cpu().numpy().astype(np.float64)
+    fq = api.dequantize_frames(qq).cpu().numpy().astype(np.float64)
+    ref = oracle.decode_frame(fp, fq, hint=t, cfg=oracle.make_cfg(3, 9, trust_hint=True))
+    assert d.width_used == ref.width_used == t
+    assert krel(d.kernel_estimate, ref.kernel) <= KREL
+    got = d.latent.cpu().numpy().astype(np.float64)
+    assert np.abs(got - ref.latent).max() <= LMAX
+    if bits == 16:
+        assert oracle.psnr(lat, got) >= 40.0  # decoder_test.cpp:437
+
+
+def test_acceptance_8_bit_degradation(oracle, api):
+    """acceptance.cpp:366-403: u8 pairs, low bits dropped 0/2/4/6, trusted hint and open
+    plausibility gates: PSNR must not rise as bits are dropped."""
+    cfg = api.make_cfg(3, 9, trust_hint=True, max_imag_energy=float("inf"), negative_weight_tol=float("inf"))
+    for seed in (1, 2, 3, 5, 7):
+        lat = oracle.random_frame(48, 48, 1, oracle.frame_seed(800, seed))
+        pair = oracle.generate_coprime_pair(3, oracle.frame_seed(801, seed))
+        pub, prv = oracle.encode_frame(lat, pair.k1, pair.k2)
+        qp = api.quantize_frames(torch.from_numpy(pub.astype(np.float32)).cuda(), 8)
+        qq = api.quantize_frames(torch.from_numpy(prv.astype(np.float32)).cuda(), 8)
+        prev = float("inf")
+        for drop in (0, 2, 4, 6):
+            d = api.decode_frames_q(api.degrade_bits(qp, drop), api.degrade_bits(qq, drop), hints=[3], cfg=cfg)[0]
+            q = oracle.psnr(lat, d.latent.cpu().numpy().astype(np.float64))
+            assert q <= prev + 1e-9
+            prev = q
+
+
+def test_host_pipeline_quantized_matches_fp32(oracle, api):
+    """cbp_decode_run_host_q (codes over PCIe) gives the same latents as the FP32 host
+    pipeline fed the dequantized values."""
+    rows, cols, t, n = 64, 80, 5, 5
+    lat = np.stack([oracle.random_frame(rows, cols, 3, oracle.frame_seed(9, 10 + i)) for i in range(n)])
+    pair = oracle.generate_coprime_pair(t, oracle.frame_seed(9, 2))
+    pubs, prvs = zip(*[oracle.encode_frame(lat[i], pair.k1, pair.k2) for i in range(n)])
+    pub = torch.from_numpy(np.stack(pubs).astype(np.float32))
+    prv = torch.from_numpy(np.stack(prvs).astype(np.float32))
+    codes_p = api.quantize_frames(pub.cuda(), 16).cpu()
+    codes_q = api.quantize_frames(prv.cuda(), 16).cpu()
+    rec = [1, 0, 0, 0, 0]
+    cfg = api.make_cfg(3, 9)
+    out_q, _ = api.decode_run_host(codes_p.pin_memory(), codes_q.pin_memory(), rec, cfg)
+    fp = api.dequantize_frames(codes_p.cuda()).cpu()
+    fq = api.dequantize_frames(codes_q.cuda()).cpu()
+    out_f, _ = api.decode_run_host(fp.pin_memory(), fq.pin_memory(), rec, cfg)
+    m, nn = rows, cols  # blurred extent minus t-1 = latent extent
+    assert torch.equal(out_q[..., :m, :nn], out_f[..., :m, :nn])

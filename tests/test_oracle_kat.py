@@ -576,3 +576,26 @@ def test_signed_content_width_and_decode(oracle):
         luma = pub[0]
         np.testing.assert_allclose(oracle.axis_spectrum_half(luma, 0), np.fft.rfft(luma, axis=0), rtol=0, atol=1e-10)
         np.testing.assert_allclose(oracle.axis_spectrum_half(luma, 1), np.fft.rfft(luma, axis=1), rtol=0, atol=1e-10)
+
+
+def test_quantize_and_degrade_kats(oracle):
+    """encoder_test.cpp:170-215: rounding to the nearest level, idempotence, half-level error
+    bound, range check, degrade_bits masking."""
+    half = np.full((1, 2, 2), 0.5)
+    assert oracle.quantize(half, 8)[0, 0, 0] == 128.0 / 255.0
+    assert oracle.quantize(half, 16)[0, 0, 0] == 32768.0 / 65535.0
+    f = oracle.random_mat(6, 6, 91)
+    once = oracle.quantize(f, 8)
+    assert np.array_equal(once, oracle.quantize(once, 8))
+    g = oracle.random_mat(16, 16, 92)
+    assert np.abs(oracle.quantize(g, 16)[0] - g).max() <= 0.5 / 65535.0 + 1e-15
+    for bad in (1.1, -0.5):
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.quantize(np.full((1, 2, 2), bad), 8)
+        assert e.value.status == 7  # 1 + Errc::range_exceeded
+    assert oracle.quantize(np.full((1, 2, 2), 1.0 + 5e-10), 8)[0, 0, 0] == 1.0
+    assert oracle.degrade_bits(np.full((1, 1, 1), 183.0 / 255.0), 8, 3)[0, 0, 0] == 176.0 / 255.0
+    assert oracle.degrade_bits(np.full((1, 1, 1), 258.0 / 65535.0), 16, 8)[0, 0, 0] == 256.0 / 65535.0
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.degrade_bits(np.full((1, 1, 1), 0.5), 8, 8)
+    assert e.value.status == 1  # 1 + Errc::invalid_argument: drop outside [0, bits)
