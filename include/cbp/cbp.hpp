@@ -63,6 +63,8 @@ inline void require(bool ok, Errc code, const std::string& what) {
 // ------------------------------------------------------------ image.hpp:10-32
 enum class BitDepth { f32, u16, u8 };
 int bit_depth_bits(BitDepth d);
+const char* bit_depth_name(BitDepth d);              // "float32", "u16", "u8"
+BitDepth bit_depth_from_name(const std::string& s);  // InvalidArgument for other names
 
 struct Frame {
   std::vector<ImagePlane> planes;

@@ -131,6 +131,17 @@ const char* errc_name(Errc c) { return cbp_errc_name(int(c) + 1); }  // error.cp
 
 int bit_depth_bits(BitDepth d) { return d == BitDepth::u16 ? 16 : d == BitDepth::u8 ? 8 : 0; }
 
+const char* bit_depth_name(BitDepth d) {  // image.cpp:5-12
+  return d == BitDepth::u16 ? "u16" : d == BitDepth::u8 ? "u8" : "float32";
+}
+
+BitDepth bit_depth_from_name(const std::string& s) {  // image.cpp:14-19
+  if (s == "float32") return BitDepth::f32;
+  if (s == "u16") return BitDepth::u16;
+  if (s == "u8") return BitDepth::u8;
+  fail(Errc::invalid_argument, "unknown bit depth '" + s + "'");
+}
+
 void validate_frame(const Frame& f) {  // image.cpp:30-39
   require(f.channels() == 1 || f.channels() == 3, Errc::dim_mismatch, "frame must have 1 or 3 planes");
   for (const auto& p : f.planes) {

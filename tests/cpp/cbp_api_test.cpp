@@ -4,6 +4,9 @@
 // __graft_entry__.build(); run by tests/test_cpp_api.py on a GPU box.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iterator>
 #include <random>
 #include <string>
 
@@ -12,6 +15,7 @@
 #include "cbp/fft.hpp"
 #include "cbp/metrics.hpp"
 #include "cbp/poly.hpp"
+#include "cbp/stream_io.hpp"
 #include "cbp/synth.hpp"
 
 using namespace cbp;
@@ -36,6 +40,8 @@ static int g_fail = 0, g_pass = 0;
     }                                                                            \
     CHECK(threw);                                                                \
   } while (0)
+
+namespace fs = std::filesystem;
 
 namespace {
 // tests/support.hpp:31-39
@@ -75,7 +81,41 @@ DecodeConfig small_search(int lo = 3, int hi = 9) {
 }
 }  // namespace
 
-int main() {
+// public/private streams of `n` encoded frames (the `cbp encode` layout, tools/cbp.cpp:60-114)
+void write_pair_streams(const fs::path& dir, int n, int rows, int cols, int ch, int t, BitDepth depth,
+                        std::vector<Frame>* latents = nullptr) {
+  std::vector<Frame> pub, prv;
+  std::string id;
+  for (int i = 0; i < n; ++i) {
+    const Frame lat = random_frame(rows, cols, ch, frame_seed(11, i));
+    BlurredPair bp = encode_frame(lat, generate_coprime_pair(t, frame_seed(12, i)));
+    if (depth != BitDepth::f32) {
+      bp.public_frame = quantize_frame(bp.public_frame, depth);
+      bp.private_frame = quantize_frame(bp.private_frame, depth);
+    }
+    if (i == 0) id = bp.pair_id;
+    pub.push_back(bp.public_frame);
+    prv.push_back(bp.private_frame);
+    if (latents) latents->push_back(lat);
+  }
+  StreamManifest m;
+  m.frame_count = n;
+  m.width = pub.front().cols();
+  m.height = pub.front().rows();
+  m.bit_depth = depth;
+  m.pair_id = id;
+  m.kernel_width_hint = t;
+  m.role = StreamRole::Public;
+  write_stream(pub, m, dir / "public");
+  m.role = StreamRole::Private;
+  write_stream(prv, m, dir / "private");
+}
+
+int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "--write-streams") {  // fixture for the cbp-decode CLI test
+    write_pair_streams(argv[2], 3, 40, 48, 3, 5, BitDepth::u16);
+    return 0;
+  }
   // decoder_test.cpp:311-331 round trip on a midsize scene
   {
     const Mat latent = random_mat(64, 64, 137);
@@ -198,6 +238,36 @@ int main() {
     const CoprimePair a = generate_coprime_pair(9, 42), b = generate_coprime_pair(9, 42);
     CHECK(a.coprimality_margin > 1e-6 && max_abs_diff(a.k1.weights, b.k1.weights) == 0.0);
     CHECK_THROWS_CODE(generate_coprime_pair(4, 1), Errc::invalid_argument);
+  }
+  // disk-to-disk decode (tools/cbp.cpp:130-207): f32 and u16 streams, sidecars, exit codes
+  for (BitDepth depth : {BitDepth::f32, BitDepth::u16}) {
+    const fs::path dir = fs::temp_directory_path() / ("cbp_dec_" + std::to_string(int(depth)));
+    fs::remove_all(dir);
+    std::vector<Frame> lat;
+    write_pair_streams(dir, 4, 48, 56, depth == BitDepth::f32 ? 1 : 3, 5, depth, &lat);
+    DecodeStreamOptions o;
+    o.pub = dir / "public";
+    o.prv = dir / "private";
+    o.out = dir / "latent";
+    o.width_min = 3;
+    o.width_max = 9;
+    o.batch = 3;  // two device batches
+    o.trust_hint = depth != BitDepth::f32;  // quantization noise swamps the width search (acceptance.cpp:379)
+    o.verbose = false;
+    CHECK(decode_stream(o) == 0);
+    auto [back, m] = read_stream(o.out);
+    CHECK(m.role == StreamRole::Latent && m.frame_count == 4 && m.bit_depth == BitDepth::f32);
+    for (int i = 0; i < 4; ++i) CHECK(psnr(lat[size_t(i)], back[size_t(i)]) >= 40.0);
+    char side[64];
+    std::snprintf(side, sizeof(side), "frame_%06d.json", 3);
+    std::ifstream sf(o.out / side);
+    const std::string text((std::istreambuf_iterator<char>(sf)), std::istreambuf_iterator<char>());
+    CHECK(text.find("\"width_used\": 5") != std::string::npos && text.find("\"total_ms\"") != std::string::npos);
+    o.max_residual = 1e-30;  // every residual above it: status 4
+    CHECK(decode_stream(o) == 4);
+    o.prv = o.pub;  // two public streams do not pair
+    CHECK_THROWS_CODE(decode_stream(o), Errc::pair_mismatch);
+    fs::remove_all(dir);
   }
   std::printf("cbp_api_test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
