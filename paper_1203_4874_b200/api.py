@@ -82,9 +82,12 @@ def spectral_deblur(blurred, kernel, epsilon: float, out: torch.Tensor | None = 
     shaped like the input with rows-t+1 x cols-t+1 planes.
     """
     ndim = blurred.dim() if isinstance(blurred, torch.Tensor) else np.ndim(blurred)
-    x = _dev_planes(blurred)
+    x = blurred if _pitched_ok(blurred) else _dev_planes(blurred)
     x4 = x.unsqueeze(0) if x.dim() == 3 else x
+    if x4.dim() == 2:
+        x4 = x4.unsqueeze(0).unsqueeze(0)
     B, ch, rows, cols = x4.shape
+    ld = x4.stride(-2)
     k = np.ascontiguousarray(np.asarray(kernel, dtype=np.float64))
     if k.ndim != 2 or k.shape[0] != k.shape[1]:
         raise CbpError(13, "DimMismatch: kernel weights must be width x width")
@@ -93,9 +96,11 @@ def spectral_deblur(blurred, kernel, epsilon: float, out: torch.Tensor | None = 
     M, Nc = rows - t + 1, cols - t + 1
     if out is None:  # output planes keep the input geometry; the top-left M x N is written
         out = torch.empty((B, ch, rows, cols), dtype=torch.float32, device=x4.device)
-    ctx.check(N.lib().cbp_spectral_deblur(ctx.ptr, C.c_void_p(x4.data_ptr()), B, ch, rows, cols, cols,
+    if not _pitched_ok(out) or out.shape[-2] != rows:
+        raise CbpError(13, "DimMismatch: out must be float32 planes of the input geometry")
+    ctx.check(N.lib().cbp_spectral_deblur(ctx.ptr, C.c_void_p(x4.data_ptr()), B, ch, rows, cols, ld,
                                           k.ctypes.data_as(C.c_void_p), t, float(epsilon),
-                                          C.c_void_p(out.data_ptr()), out.shape[-1],
+                                          C.c_void_p(out.data_ptr()), out.stride(-2),
                                           _stream_ptr(x4.device)))
     out = out[..., :M, :Nc]
     if ndim == 2:
@@ -126,6 +131,22 @@ class DecodedFrame:
     stage_timings: StageTimings = field(default_factory=StageTimings)
     validation_residual: float = 0.0
     epsilon_used: float = 0.0
+
+
+def _pitched_ok(x) -> bool:
+    """A CUDA float32 tensor the C ABI can read in place: unit column stride and planes of
+    rows x ld (ld = row stride >= cols, e.g. a [..., :cols] view of pitched rows)."""
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 and x.dim() >= 2):
+        return False
+    rows, ld = x.shape[-2], x.stride(-2)
+    if x.stride(-1) != 1 or ld < x.shape[-1]:
+        return False
+    expect = rows * ld
+    for d in range(x.dim() - 3, -1, -1):
+        if x.shape[d] > 1 and x.stride(d) != expect:
+            return False
+        expect *= x.shape[d]
+    return True
 
 
 def _as_batch(x) -> tuple[torch.Tensor, int]:
