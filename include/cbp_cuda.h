@@ -177,6 +177,15 @@ int cbp_spectral_deblur(cbp_ctx* ctx, const float* blurred_dev, int batch, int c
 
 /* Same, with kernel, width and epsilon read on the device from a slot written by
  * cbp_decode_frames_async (a failed slot leaves its outputs untouched). */
+/* As cbp_decode_frames_async, and records `slot_ready_event` (a cudaEvent_t) on `stream` as
+ * soon as the slots hold their final kernel, width and epsilon, before the batch's own
+ * deconvolution and validation residual: a pipeline can start cbp_spectral_deblur_slot on
+ * the following frames while those finish (the residual and any validation failure land
+ * in the slot when `stream` completes). */
+int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch,
+                               int channels, int rows, int cols, int ld, const int* width_hints,
+                               const cbp_decode_cfg* cfg, float* latent_dev, int ld_out,
+                               cbp_kernel_slot* slots_dev, void* stream, void* slot_ready_event);
 int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,
                              int rows, int cols, int ld, const cbp_kernel_slot* slot_dev,
                              float* latent_dev, int ld_out, void* stream);

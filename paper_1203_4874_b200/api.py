@@ -512,7 +512,8 @@ def launch_count(device: int | None = None) -> int:
 
 
 def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, out: torch.Tensor,
-                        slots: torch.Tensor, hints=None, ctx: N.Context | None = None, stream=None):
+                        slots: torch.Tensor, hints=None, ctx: N.Context | None = None, stream=None,
+                        slot_ready: "torch.cuda.Event | None" = None):
     """cbp_decode_frames_async on device tensors (batch, ch, rows, cols); ``slots`` is a
     uint8 device tensor of batch * sizeof(KernelSlot) bytes receiving the per-frame state.
     ``ctx`` / ``stream`` select the context (workspaces) and CUDA stream (default: the
@@ -523,6 +524,13 @@ def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, ou
     if hints is not None:
         hint_arr = (C.c_int * B)(*[int(h) for h in hints])
     st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
+    if slot_ready is not None:  # recorded as soon as the kernels are final (cbp_decode_frames_async_ev)
+        ev = C.c_void_p(slot_ready.cuda_event)
+        ctx.check(N.lib().cbp_decode_frames_async_ev(ctx.ptr, C.c_void_p(pub.data_ptr()),
+                                                     C.c_void_p(prv.data_ptr()), B, ch, rows, cols, pub.stride(-2),
+                                                     hint_arr, C.byref(cfg), C.c_void_p(out.data_ptr()),
+                                                     out.stride(-2), C.c_void_p(slots.data_ptr()), st, ev))
+        return
     ctx.check(N.lib().cbp_decode_frames_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(prv.data_ptr()), B,
                                               ch, rows, cols, pub.stride(-2), hint_arr, C.byref(cfg),
                                               C.c_void_p(out.data_ptr()), out.stride(-2),

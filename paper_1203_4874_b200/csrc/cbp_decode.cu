@@ -252,6 +252,9 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
   if (record_events) cudaEventRecord(ctx->ev[3], s);
   if (e == cudaSuccess) e = launch_compose(a, s);
   if ((st = cuda_check(ctx, e, "recovery launch"))) return st;
+  // kernels, widths and epsilons are final here; the frame's own deconvolution and the
+  // validation residual follow on this stream, consumers of the slots need not wait for them
+  if (ctx->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(ctx->slot_event), s);
   DeblurArgs d;
   if ((st = deblur_setup(ctx, rows, cols, d))) return st;
   d.in = pub;
@@ -298,6 +301,18 @@ int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv
   if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
   return enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg, latent_dev,
                         ld_out, slots_dev, static_cast<cudaStream_t>(stream), false);
+}
+
+int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels,
+                               int rows, int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg,
+                               float* latent_dev, int ld_out, cbp_kernel_slot* slots_dev, void* stream,
+                               void* slot_ready_event) {
+  if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
+  ctx->slot_event = slot_ready_event;
+  const int st = enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg,
+                                latent_dev, ld_out, slots_dev, static_cast<cudaStream_t>(stream), false);
+  ctx->slot_event = nullptr;
+  return st;
 }
 
 int cbp_decode_frames(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels, int rows,

@@ -222,6 +222,37 @@ def test_slot_chaining_equals_spectral_deblur(oracle, api):
     assert torch.equal(out[1:, :, :96, :128], ref)
 
 
+def test_slot_ready_event_pipeline(oracle, api):
+    """cbp_decode_frames_async_ev: a second stream waiting on the slot-ready event deblurs the
+    following frames with the final kernel while the recovery frame's own deconvolution and
+    validation run on the first stream; results equal the serial chain."""
+    pair = oracle.generate_coprime_pair(7, 14)
+    frames = [oracle.encode_frame(oracle.random_frame(96, 128, 1, 40 + i), pair.k1, pair.k2) for i in range(4)]
+    P = torch.from_numpy(np.stack([f[0] for f in frames]).astype(np.float32)).cuda()
+    Q = torch.from_numpy(np.stack([f[1] for f in frames]).astype(np.float32)).cuda()
+    cfg = api.make_cfg(3, 9)
+    s_rec, s_deb = torch.cuda.Stream(), torch.cuda.Stream()
+    ready = torch.cuda.Event()
+    ready.record(s_rec)  # materialise the event handle
+    from paper_1203_4874_b200 import _native
+    ctx_rec = _native.Context(0)
+    out = torch.zeros_like(P)
+    slots = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    api.decode_frames_async(P[0:1], Q[0:1], cfg, out[0:1], slots[0], ctx=ctx_rec, stream=s_rec, slot_ready=ready)
+    s_deb.wait_event(ready)
+    api.spectral_deblur_slot(P[1:], slots[0].data_ptr(), out[1:], stream=s_deb)
+    torch.cuda.synchronize()
+    ref = torch.zeros_like(P)
+    slots2 = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    api.decode_frames_async(P[0:1], Q[0:1], cfg, ref[0:1], slots2[0])
+    api.spectral_deblur_slot(P[1:], slots2[0].data_ptr(), ref[1:])
+    torch.cuda.synchronize()
+    a, b = api.read_slots(slots, 1)[0], api.read_slots(slots2, 1)[0]
+    assert a.status == b.status == 0 and a.width == b.width == 7 and a.residual == b.residual
+    assert torch.equal(out[..., :90, :122], ref[..., :90, :122])
+
+
 def test_host_pipeline_equals_device_path(oracle, api):
     pair = oracle.generate_coprime_pair(5, 31)
     frames = [oracle.encode_frame(oracle.random_frame(60, 70, 1, 40 + i), pair.k1, pair.k2) for i in range(5)]
