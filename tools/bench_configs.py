@@ -1,0 +1,152 @@
+"""Device-side numbers for the other BASELINE.json configs; bench.py measures
+the headline config c3. Synthetic inputs as in bench.py (device-synthesised latents, device
+encode with reference-exact kernel pairs); CUDA-event timing after warm-up. Prints one JSON
+object per config.
+
+  c1  256x256 gray, t=7, search 3..25: decode_frame latency (device-resident, and through the
+      C++-style host path with H2D/D2H: cbp_decode_run_host of one frame)
+  c2  640x480 gray, t=9: 1 decode_frame + 299 spectral_deblur with the device-resident kernel
+  c4  3840x2160 gray, t=15, kernel recovery on every frame (trusted hint / estimated width)
+  c5  64 streams of 1080p gray, t=11, re-estimated every 30 frames (per-GPU frames/s)
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1203_4874_b200 import api, _native
+
+HBM = 6534.1e9
+
+
+def pitched(n, ch, rows, cols):
+    ldp = (cols + 3) // 4 * 4
+    return torch.empty((n, ch, rows, ldp), dtype=torch.float32, device="cuda")[..., :cols]
+
+
+def make_pairs(n, ch, rows, cols, t, seed, shared_kernel=True):
+    """n encoded frames; one kernel pair (shared) or one per frame."""
+    Mb, Nb = rows + t - 1, cols + t - 1
+    pub, prv = pitched(n, ch, Mb, Nb), pitched(n, ch, Mb, Nb)
+    for i in range(n):
+        pair = api.generate_coprime_pair(t, api.frame_seed(2, seed if shared_kernel else seed * 1000 + i))
+        lat = api.synth_frames(ch, rows, cols, seed=api.frame_seed(1, seed * 1000 + i)).view(1, ch, rows, cols)
+        p, q = api.encode_frame(lat, pair.k1, pair.k2)
+        pub[i].copy_(p[0])
+        prv[i].copy_(q[0])
+    return pub, prv
+
+
+def timed(fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps  # ms per call
+
+
+def c1():
+    rows = cols = 256
+    t = 7
+    pub, prv = make_pairs(1, 1, rows, cols, t, 1)
+    out = torch.empty_like(pub)
+    slots = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    cfg = api.make_cfg(3, 25)
+    ms = timed(lambda: api.decode_frames_async(pub, prv, cfg, out, slots[0]), 20)
+    sl = api.read_slots(slots, 1)[0]
+    hp = pub.contiguous().cpu().pin_memory()
+    hq = prv.contiguous().cpu().pin_memory()
+    ho = torch.empty_like(hp).pin_memory()
+    host = timed(lambda: api.decode_run_host(hp, hq, [1], cfg, out=ho), 10)
+    return {"config": "c1: 256x256 gray, t=7, search 3..25, single frame", "width": sl.width,
+            "decode_latency_ms_device": ms, "decode_latency_ms_host_buffers": host}
+
+
+def epoch_fps(ch, rows, cols, t, epoch, seed, label, pool=3):
+    """1 decode + (epoch-1) slot deblurs per epoch, epochs cycled from a pool (the bench.py step)."""
+    Mb, Nb = rows + t - 1, cols + t - 1
+    pubs, prvs = [], []
+    for e in range(pool):
+        p, q = make_pairs(epoch, ch, rows, cols, t, seed + e)
+        pubs.append(p)
+        prvs.append(q)
+    outs = [pitched(epoch, ch, Mb, Nb) for _ in range(pool)]
+    slots = torch.zeros((pool, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    cfg = api.make_cfg(9, 25)
+    state = {"i": 0}
+
+    def step():
+        e = state["i"] % pool
+        state["i"] += 1
+        api.decode_frames_async(pubs[e][0:1], prvs[e][0:1], cfg, outs[e][0:1], slots[e])
+        api.spectral_deblur_slot(pubs[e][1:], slots[e].data_ptr(), outs[e][1:])
+
+    ms = timed(step, 6)
+    sl = api.read_slots(slots, pool)
+    assert all(s.status == 0 and s.width == t for s in sl), [(s.status, s.width) for s in sl]
+    fps = epoch / (ms / 1e3)
+    byts = ch * (Mb * Nb + rows * cols) * 4
+    return {"config": label, "frames_per_s": fps, "ms_per_epoch": ms,
+            "hbm_roofline_frac": fps * byts / HBM, "bytes_per_frame": byts}
+
+
+def c4(trust):
+    rows, cols, t, B = 2160, 3840, 15, 4
+    pub, prv = make_pairs(B, 1, rows, cols, t, 7, shared_kernel=False)
+    out = torch.empty_like(pub)
+    slots = torch.zeros((B, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    cfg = api.make_cfg(9, 25, trust_hint=trust)
+    hints = [t] * B if trust else None
+    ms = timed(lambda: api.decode_frames_async(pub, prv, cfg, out, slots, hints=hints), 5)
+    sl = api.read_slots(slots, B)
+    assert all(s.status == 0 and s.width == t for s in sl), [(s.status, s.width) for s in sl]
+    Mb, Nb = rows + t - 1, cols + t - 1
+    fps = B / (ms / 1e3)
+    return {"config": f"c4: 3840x2160 gray, t=15, per-frame recovery ({'trusted hint' if trust else 'estimated width'})",
+            "frames_per_s": fps, "ms_per_batch_of_4": ms, "hbm_roofline_frac": fps * (2 * Mb * Nb + rows * cols) * 4 / HBM}
+
+
+def c5():
+    """64 streams x 1080p gray, epochs of 30 frames: per epoch, one batched recovery of the
+    64 streams' first frames, then 29 x 64 slot deblurs (each stream its own kernel)."""
+    S, rows, cols, t, epoch = 64, 1080, 1920, 11, 30
+    Mb, Nb = rows + t - 1, cols + t - 1
+    rec_pub, rec_prv = make_pairs(S, 1, rows, cols, t, 11, shared_kernel=False)
+    frames, _ = make_pairs(8, 1, rows, cols, t, 12)  # deblur inputs (content does not change the work)
+    out_rec = torch.empty_like(rec_pub)
+    out = pitched(8, 1, Mb, Nb)
+    slots = torch.zeros((S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    cfg = api.make_cfg(9, 25)
+
+    def ep():
+        api.decode_frames_async(rec_pub, rec_prv, cfg, out_rec, slots)
+        for s in range(S):  # 29 frames of stream s with its kernel, 8 frames per call
+            for f0 in range(0, epoch - 1, 8):
+                n = min(8, epoch - 1 - f0)
+                api.spectral_deblur_slot(frames[:n], slots[s].data_ptr(), out[:n])
+
+    ms = timed(ep, 2, warm=1)
+    sl = api.read_slots(slots, S)
+    ok = sum(1 for s in sl if s.status == 0 and s.width == t)
+    fps = S * epoch / (ms / 1e3)
+    return {"config": "c5: 64 streams x 1080p gray, t=11, re-estimated every 30 frames (1 GPU)",
+            "frames_per_s": fps, "ms_per_epoch_64_streams": ms, "streams_recovered": ok,
+            "hbm_roofline_frac": fps * (Mb * Nb + rows * cols) * 4 / HBM}
+
+
+if __name__ == "__main__":
+    torch.cuda.set_device(0)
+    res = [c1(),
+           epoch_fps(1, 480, 640, 9, 300, 3, "c2: 640x480 gray, t=9, kernel recovered once, 300 frames", pool=2),
+           epoch_fps(3, 1080, 1920, 11, 30, 5, "c3 (serial, one stream): 1080p RGB, t=11, 1 decode + 29 deblur"),
+           c4(True), c4(False), c5()]
+    for r in res:
+        print(json.dumps(r), flush=True)
