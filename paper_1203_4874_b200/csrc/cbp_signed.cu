@@ -11,6 +11,8 @@
 // order; only the picked frequency's slices are then formed, written over the DC slices
 // so k_width_blocks / k_width_pick run unchanged (complex blocks take the Jacobi SVD path).
 // Frames without a negative sample exit at the first instruction.
+#include <algorithm>
+
 #include "cbp_recover.cuh"
 
 namespace cbp_dev {
@@ -42,13 +44,26 @@ __global__ void k_spec_roots(RecoverArgs a) {
 
 // z1: F_q(i, n) = sum_m W_M^{i m} luma_q(m, n), i <= M/2. Per tile: partial energies
 // sum_n |F|^2 for the tile's 32 frequencies. grid (ceil(N/32), ceil(H1/32), batch*2).
+__device__ __forceinline__ bool any_signed(const RecoverArgs& a) {
+  for (int b = 0; b < a.batch; ++b)
+    if (signed_frame(a, b)) return true;
+  return false;
+}
+
+// Persistent grid over tiles (x fastest, then y, then frame*2+stream): a batch without
+// signed frames costs one flag scan per CTA instead of ~10^4 empty CTAs.
 __global__ void __launch_bounds__(256) k_spec_energy_z1(RecoverArgs a) {
-  const int b = blockIdx.z >> 1, q = blockIdx.z & 1;
-  if (!signed_frame(a, b)) return;
+  if (!any_signed(a)) return;
+  const int M = a.rows, N = a.cols, H1 = M / 2 + 1;
+  const int tx = (N + TS - 1) / TS, ty = (H1 + TS - 1) / TS;
+  for (int tile = blockIdx.x; tile < tx * ty * a.batch * 2; tile += gridDim.x) {
+  const int bz = tile / (tx * ty), rem = tile - bz * (tx * ty);
+  const int by = rem / tx, bx = rem - by * tx;
+  const int b = bz >> 1, q = bz & 1;
+  if (!signed_frame(a, b)) continue;
   __shared__ double Ls[TS][TS + 1];
   __shared__ double2 Ws[TS][TS + 1];
-  const int M = a.rows, N = a.cols, H1 = M / 2 + 1;
-  const int n0 = blockIdx.x * TS, i0 = blockIdx.y * TS;
+  const int n0 = bx * TS, i0 = by * TS;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t plane = size_t(M) * a.ld;
   const float* base = stream_base(a, b, q);
@@ -82,20 +97,26 @@ __global__ void __launch_bounds__(256) k_spec_energy_z1(RecoverArgs a) {
     double e = zabs2(acc[k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-    if (lane == 0 && i < H1) a.epart[((size_t(b) * 2 + q) * ntn + blockIdx.x) * H1 + i] = e;
+    if (lane == 0 && i < H1) a.epart[((size_t(b) * 2 + q) * ntn + bx) * H1 + i] = e;
+  }
   }
 }
 
 // z2: F_q(m, j) = sum_n luma_q(m, n) W_N^{j n}, j <= N/2. Per tile: partial energies
 // sum_m |F|^2 for the tile's 32 frequencies. grid (ceil(H2/32), ceil(M/32), batch*2).
 __global__ void __launch_bounds__(256) k_spec_energy_z2(RecoverArgs a) {
-  const int b = blockIdx.z >> 1, q = blockIdx.z & 1;
-  if (!signed_frame(a, b)) return;
+  if (!any_signed(a)) return;
+  const int M = a.rows, N = a.cols, H2 = N / 2 + 1;
+  const int tx = (H2 + TS - 1) / TS, ty = (M + TS - 1) / TS;
+  for (int tile = blockIdx.x; tile < tx * ty * a.batch * 2; tile += gridDim.x) {
+  const int bz = tile / (tx * ty), rem = tile - bz * (tx * ty);
+  const int by = rem / tx, bx = rem - by * tx;
+  const int b = bz >> 1, q = bz & 1;
+  if (!signed_frame(a, b)) continue;
   __shared__ double Ls[TS][TS + 1];
   __shared__ double2 Ws[TS][TS + 1];
   __shared__ double Es[8][TS];
-  const int M = a.rows, N = a.cols, H2 = N / 2 + 1;
-  const int j0 = blockIdx.x * TS, m0 = blockIdx.y * TS;
+  const int j0 = bx * TS, m0 = by * TS;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t plane = size_t(M) * a.ld;
   const float* base = stream_base(a, b, q);
@@ -128,7 +149,9 @@ __global__ void __launch_bounds__(256) k_spec_energy_z2(RecoverArgs a) {
   if (w == 0 && j0 + lane < H2) {
     double e = 0.0;
     for (int ww = 0; ww < 8; ++ww) e += Es[ww][lane];
-    a.epart[((size_t(b) * 2 + q) * ntm + blockIdx.y) * H2 + j0 + lane] = e;
+    a.epart[((size_t(b) * 2 + q) * ntm + by) * H2 + j0 + lane] = e;
+  }
+  __syncthreads();  // Es is rewritten by the next tile
   }
 }
 
@@ -210,10 +233,10 @@ size_t signed_energy_doubles(int batch, int rows, int cols) {
 cudaError_t launch_signed_slices(const RecoverArgs& a, cudaStream_t s) {
   const int M = a.rows, N = a.cols;
   k_spec_roots<<<(std::max(M, N) + 255) / 256, 256, 0, s>>>(a);
-  dim3 g1((N + TS - 1) / TS, (M / 2 + 1 + TS - 1) / TS, a.batch * 2);
-  k_spec_energy_z1<<<g1, 256, 0, s>>>(a);
-  dim3 g2((N / 2 + 1 + TS - 1) / TS, (M + TS - 1) / TS, a.batch * 2);
-  k_spec_energy_z2<<<g2, 256, 0, s>>>(a);
+  const int t1 = ((N + TS - 1) / TS) * ((M / 2 + 1 + TS - 1) / TS) * a.batch * 2;
+  const int t2 = ((N / 2 + 1 + TS - 1) / TS) * ((M + TS - 1) / TS) * a.batch * 2;
+  k_spec_energy_z1<<<std::min(t1, 148 * 4), 256, 0, s>>>(a);
+  k_spec_energy_z2<<<std::min(t2, 148 * 4), 256, 0, s>>>(a);
   k_spec_pick<<<dim3(a.batch, 2), 512, 0, s>>>(a);
   return cudaGetLastError();
 }
