@@ -127,7 +127,12 @@ __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, Jac
 // barrier per round (~3x faster at n = 22 on B200, see tools/micro/bench_eig.cu).
 // Executed by one warp; n <= 64. Same contract as herm_jacobi: G's diagonal receives the
 // eigenvalues, V the eigenvectors as columns; G's off-diagonal part is destroyed.
-__device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, bool vectors = true) {
+// mode: EIG_VALUES (eigenvalues only, bisection), EIG_QL (eigenvectors by implicit QL: exactly
+// orthogonal, robust for dense clusters of tiny eigenvalues), EIG_INVIT (eigenvectors by
+// inverse iteration: faster when the spectrum is well separated)
+enum EigMode { EIG_VALUES = 0, EIG_QL = 1, EIG_INVIT = 2 };
+__device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, int mode) {
+  const bool vectors = mode != EIG_VALUES;
   __shared__ double s_d[64], s_e[64], s_beta[64], s_rc[64], s_rs[64];
   __shared__ double2 s_ec[64], s_w[64], s_p[64], s_delta[64];
   const int lane = threadIdx.x & 31;
@@ -276,6 +281,7 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, b
     __syncwarp();
     return;
   }
+  if (mode == EIG_QL) {
   // ---- eigenvectors: implicit QL with Wilkinson shifts (tqli) on T'. Every lane runs the
   // same scalar recurrence (no broadcast barrier). The sweep reads d/e and writes the
   // updated entries to separate arrays (s_dn/s_en), so its loads never wait behind its
@@ -366,6 +372,95 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, b
   }
   for (int k = lane; k < n; k += 32) s_p[k].x = s_d[k];
   __syncwarp();
+  } else {
+  // ---- eigenvectors by inverse iteration, one lane per eigenvalue: bisection to full precision,
+  // then three inverse-iteration steps (tridiagonal LU with partial pivoting) with
+  // Rayleigh-quotient shifts. Eigenvalues closer than 1e-8 |T'| form a cluster that one
+  // lane handles in turn, orthogonalizing each member against the previous ones (LAPACK
+  // stein's scheme with a tighter cluster threshold: separated eigenvectors come out
+  // orthogonal to ~1e-8 and accurate to ~1e-16 / gap).
+  for (int k = lane; k < n; k += 32) {
+    double lo = lo0, hi = hi0;
+    for (int it = 0; it < 62; ++it) {  // to full precision: the shifts must resolve close pairs
+      const double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi) break;
+      if (count_below(mid) > k) hi = mid;
+      else lo = mid;
+    }
+    s_p[k].x = 0.5 * (lo + hi);  // ascending in k
+  }
+  __syncwarp();
+  __shared__ int s_cl[65], s_ncl;
+  if (lane == 0) {
+    int nc = 0;
+    for (int k = 0; k < n; ++k)
+      if (k == 0 || s_p[k].x - s_p[k - 1].x > 1e-8) s_cl[nc++] = k;
+    s_cl[nc] = n;
+    s_ncl = nc;
+  }
+  __syncwarp();
+  for (int cl = lane; cl < s_ncl; cl += 32) {
+    const int k0 = s_cl[cl], k1 = s_cl[cl + 1];
+    for (int k = k0; k < k1; ++k) {
+      double lam = s_p[k].x, rq = lam;
+      double y[64];
+      unsigned h = 0x9e3779b9u * unsigned(k + 1);
+      for (int i = 0; i < n; ++i) {  // pseudo-random start vector
+        h ^= h << 13, h ^= h >> 17, h ^= h << 5;
+        y[i] = double(h & 0xffff) * (1.0 / 65536.0) - 0.5;
+      }
+      for (int it = 0; it < 3; ++it) {
+        double u0[64], u1[64], u2[64];
+        double a0 = s_d[0] - lam, bn = n > 1 ? s_e[0] : 0.0;
+        for (int i = 0; i + 1 < n; ++i) {
+          const double cv = s_e[i], dl = s_d[i + 1] - lam, el = i + 2 < n ? s_e[i + 1] : 0.0;
+          if (fabs(a0) >= fabs(cv)) {
+            const double aa = fabs(a0) < 1e-16 ? copysign(1e-16, a0) : a0;  // pivot floor eps |T'|
+            const double m = cv * rcp(aa);
+            u0[i] = aa, u1[i] = bn, u2[i] = 0.0;
+            y[i + 1] -= m * y[i];
+            a0 = dl - m * bn;
+            bn = el;
+          } else {
+            const double m = a0 * rcp(cv);
+            u0[i] = cv, u1[i] = dl, u2[i] = el;
+            const double tt = y[i];
+            y[i] = y[i + 1];
+            y[i + 1] = tt - m * y[i];
+            a0 = bn - m * dl;
+            bn = -m * el;
+          }
+        }
+        u0[n - 1] = fabs(a0) < 1e-16 ? copysign(1e-16, a0) : a0;
+        u1[n - 1] = u2[n - 1] = 0.0;
+        for (int i = n - 1; i >= 0; --i) {
+          double v = y[i];
+          if (i + 1 < n) v -= u1[i] * y[i + 1];
+          if (i + 2 < n) v -= u2[i] * y[i + 2];
+          y[i] = v * rcp(u0[i]);
+        }
+        for (int j = k0; j < k; ++j) {  // earlier members of this cluster
+          double dot = 0.0;
+          for (int i = 0; i < n; ++i) dot = fma(V[i * ldv + j].x, y[i], dot);
+          for (int i = 0; i < n; ++i) y[i] = fma(-dot, V[i * ldv + j].x, y[i]);
+        }
+        double nrm = 0.0;
+        for (int i = 0; i < n; ++i) nrm = fma(y[i], y[i], nrm);
+        const double inv = rsqrt(nrm);
+        rq = 0.0;
+        for (int i = 0; i < n; ++i) {
+          y[i] *= inv;
+          rq = fma(s_d[i] * y[i], y[i], rq);
+          if (i > 0) rq = fma(2.0 * s_e[i - 1] * y[i - 1], y[i], rq);
+        }
+        if (k1 - k0 == 1 && fabs(rq - lam) < 1e-6) lam = rq;  // Rayleigh shift (isolated only)
+      }
+      s_p[k].x = k1 - k0 == 1 ? rq : s_p[k].x;
+      for (int i = 0; i < n; ++i) V[i * ldv + k] = make_double2(y[i], 0.0);
+    }
+  }
+  __syncwarp();
+  }
   CBP_PHASE(35, pw);
   for (int k = lane; k < n; k += 32) s_d[k] = s_p[k].x / sc;
   __syncwarp();
@@ -396,20 +491,22 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, b
 
 // eigenvalues only (G's diagonal), whole CTA
 __device__ __forceinline__ void herm_eigvals_cta(double2* G, int ldg, double2* V, int ldv, int n) {
-  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, false);
+  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, EIG_VALUES);
   __syncthreads();
 }
 
 // whole-CTA entry: the tridiagonal route on warp 0 (the Jacobi solver above is kept as
 // the reference implementation, selectable with -DCBP_JACOBI)
-__device__ __forceinline__ void herm_jacobi_cta(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc) {
+__device__ __forceinline__ void herm_jacobi_cta(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc,
+                                                int mode = EIG_QL) {
 #ifdef CBP_JACOBI
   if (sc.cs) {
     herm_jacobi(G, ldg, V, ldv, n, sc);
     return;
   }
 #endif
-  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n);
+  (void)sc;
+  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, mode);
   __syncthreads();
 }
 

@@ -437,7 +437,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
   }
   __syncthreads();
   CBP_PHASE(11, pw);
-  herm_jacobi_cta(sm.G, n, sm.V, n, n, sm.js);
+  herm_jacobi_cta(sm.G, n, sm.V, n, n, sm.js, EIG_QL);  // smooth p, q: dense tiny eigenvalues
   CBP_PHASE(12, pw);
   __shared__ int kmin_s, k2_s;
   __shared__ double lmax_s, lmin_s;
@@ -755,7 +755,7 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
   }
   __syncthreads();
   CBP_PHASE(25, blockIdx.x == 0);
-  herm_jacobi_cta(s.G, n, s.V, n, n, s.js);
+  herm_jacobi_cta(s.G, n, s.V, n, n, s.js, EIG_INVIT);  // resolve Gram: separated spectrum
   CBP_PHASE(22, blockIdx.x == 0);
   __shared__ int kmin_s;
   __shared__ double lmax_s, lmin_s;

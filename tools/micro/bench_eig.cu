@@ -16,7 +16,7 @@ __global__ void keig(const double2* G0, double2* Gout, double2* V, int n, unsign
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) G[i] = G0[i];
   __syncthreads();
   unsigned long long t0 = clock64();
-  herm_jacobi_cta(G, n, Vs, n, n, JacobiScratch{});
+  herm_jacobi_cta(G, n, Vs, n, n, JacobiScratch{}, EIG_MODE);
   unsigned long long t1 = clock64();
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) Gout[i] = G[i], V[i] = Vs[i];
   if (threadIdx.x == 0) t[0] = t1 - t0;

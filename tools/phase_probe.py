@@ -4,8 +4,9 @@ import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1203_4874_b200 import api, _native
-pair = api.generate_coprime_pair(11, api.frame_seed(2, 0))
-lat = api.synth_frames(3, 1080, 1920, seed=1).view(1, 3, 1080, 1920)
+R, Cc, CH, T = (int(x) for x in os.environ.get("PROBE", "1080,1920,3,11").split(","))
+pair = api.generate_coprime_pair(T, api.frame_seed(2, 0))
+lat = api.synth_frames(CH, R, Cc, seed=1).view(1, CH, R, Cc)
 pub, prv = api.encode_frame(lat, pair.k1, pair.k2)
 out = torch.empty_like(pub)
 slots = torch.zeros(api.SLOT_BYTES, dtype=torch.uint8, device="cuda")
