@@ -138,7 +138,8 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.has_epsilon = cfg ? cfg->has_epsilon : 0;
   a.epsilon = cfg ? cfg->epsilon : 0.0;
   const size_t B = size_t(batch), T = size_t(t_max), L = size_t(a.lmax);
-  P.vtiles = want_validate ? validate_tiles(rows, cols, 1) : 0;  // decode widths <= 31: 32-row tiles
+  // decode widths are <= min(t_max, 31): the tile count is largest for the widest kernel
+  P.vtiles = want_validate ? validate_tiles(rows, cols, std::min(t_max, 31)) : 0;
   // carve one allocation (256-byte aligned pieces)
   size_t off = 0;
   auto take = [&](size_t bytes) {

@@ -3,6 +3,8 @@
 // Every stage keeps the reference's FP64 arithmetic (decoder.cpp, poly.cpp, fft.cpp);
 // inputs are the FP32 frames as stored in HBM.
 #include "cbp_linalg.cuh"
+#include <type_traits>
+
 #include "cbp_recover.cuh"
 
 namespace cbp_dev {
@@ -1103,7 +1105,9 @@ cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const 
 // Outputs per CTA: VT_R rows x 64 columns (8 rows per thread): 32 rows (256 threads), or
 // 8 rows (64 threads) for kernels wider than 40 taps, whose halo would not fit otherwise.
 constexpr int VT_C = 64;
-__host__ __device__ inline int conv_rows(int t) { return t > 40 ? 8 : 32; }
+// outputs per thread (a column strip) and output rows per CTA (4 row groups of 64 threads)
+__host__ __device__ inline int conv_out(int) { return 8; }
+__host__ __device__ inline int conv_rows(int t) { return t > 40 ? 8 : 4 * conv_out(t); }
 __host__ __device__ inline int conv_pad(int t) { return (t + 3) & ~3; }
 int validate_tiles(int rows, int cols, int t) {
   const int vr = conv_rows(t);
@@ -1159,7 +1163,48 @@ __device__ __forceinline__ void conv_col8(const double* tile, int tw, const doub
   }
 }
 
-__global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
+// Fully unrolled variant for a compile-time padded width TP: the (OUT + TP - 1)-value
+// window of one kernel column lives in registers without shifts, each load feeds up to
+// OUT FMAs.
+template <int OUT, int TP>
+__device__ __forceinline__ void conv_colT(const double* tile, int tw, const double* kt, int t, int li0, int lj,
+                                          double* acc) {
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) acc[q] = 0.0;
+  for (int b2 = 0; b2 < t; ++b2) {
+    const double* col = tile + (li0 + TP - 1) * tw + (lj + t - 1 - b2);  // X(i0 + li0 + x, .) = col[x * tw]
+    const double* kc = kt + b2 * TP;
+    double v[OUT + TP - 1];  // v[k] = col[(OUT - 1 - k) * tw]
+#pragma unroll
+    for (int k = 0; k < OUT + TP - 1; ++k) v[k] = col[(OUT - 1 - k) * tw];
+#pragma unroll
+    for (int j = 0; j < TP; ++j) {
+      const double w = kc[j];
+#pragma unroll
+      for (int q = 0; q < OUT; ++q) acc[q] = fma(w, v[OUT - 1 - q + j], acc[q]);
+    }
+  }
+}
+
+template <int OUT>
+__device__ __forceinline__ void conv_dispatch(const double* tile, int tw, const double* kt, int t, int tp, int li0,
+                                              int lj, double* acc) {
+  {
+    switch (tp) {
+      case 4: return conv_colT<8, 4>(tile, tw, kt, t, li0, lj, acc);
+      case 8: return conv_colT<8, 8>(tile, tw, kt, t, li0, lj, acc);
+      case 12: return conv_colT<8, 12>(tile, tw, kt, t, li0, lj, acc);
+      case 16: return conv_colT<8, 16>(tile, tw, kt, t, li0, lj, acc);
+      case 20: return conv_colT<8, 20>(tile, tw, kt, t, li0, lj, acc);
+      case 24: return conv_colT<8, 24>(tile, tw, kt, t, li0, lj, acc);
+      case 28: return conv_colT<8, 28>(tile, tw, kt, t, li0, lj, acc);
+      case 32: return conv_colT<8, 32>(tile, tw, kt, t, li0, lj, acc);
+      default: return conv_col8(tile, tw, kt, t, tp, li0, lj, acc);  // t > 32
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
   extern __shared__ double shd[];
   const int plane = blockIdx.y;
   const int frame = plane / a.channels;
@@ -1202,27 +1247,31 @@ __global__ void __launch_bounds__(256) k_conv_resid(ConvResidArgs a) {
   }
   __syncthreads();
   double num = 0.0, den = 0.0;
-  const int lj = threadIdx.x % VT_C, li0 = (threadIdx.x / VT_C) * 8;
-  const int gj = j0 + lj;
-  if (gj < co && i0 + li0 < ro) {
-    double c1[8], c2[8];
-    conv_col8(tile, tw, kt, t, tp, li0, lj, c1);
-    if (a.mode == 1) conv_col8(tile2, tw, kt2, t, tp, li0, lj, c2);
+  auto accumulate = [&](auto out_tag) {
+    constexpr int OUT = decltype(out_tag)::value;
+    const int lj = threadIdx.x % VT_C, li0 = (threadIdx.x / VT_C) * OUT;
+    const int gj = j0 + lj;
+    if (gj < co && i0 + li0 < ro) {
+      double c1[OUT], c2[OUT];
+      conv_dispatch<OUT>(tile, tw, kt, t, tp, li0, lj, c1);
+      if (a.mode == 1) conv_dispatch<OUT>(tile2, tw, kt2, t, tp, li0, lj, c2);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int gi = i0 + li0 + q;
-      if (gi >= ro) break;
-      double y;
-      if (a.mode == 0) {
-        y = double(Y[size_t(gi) * a.yld + gj]);
-        den += y * y;
-      } else {
-        y = c2[q];
-        den += c1[q] * c1[q];
+      for (int q = 0; q < OUT; ++q) {
+        const int gi = i0 + li0 + q;
+        if (gi >= ro) break;
+        double y;
+        if (a.mode == 0) {
+          y = double(Y[size_t(gi) * a.yld + gj]);
+          den += y * y;
+        } else {
+          y = c2[q];
+          den += c1[q] * c1[q];
+        }
+        num += (c1[q] - y) * (c1[q] - y);
       }
-      num += (c1[q] - y) * (c1[q] - y);
     }
-  }
+  };
+  accumulate(std::integral_constant<int, 8>{});
   num = warp_sum(num);
   den = warp_sum(den);
   __shared__ double rn[8], rd[8];
@@ -1298,7 +1347,8 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.ro = ra.rows;
   a.co = ra.cols;
   dim3 g(ntiles_max, ra.batch * ra.channels);
-  const size_t sm = conv_smem(std::min(ra.t_max, 31), 0);  // device-side widths are <= 31 (solver limit)
+  size_t sm = 0;  // the device-side width is <= min(t_max, 31) (solver limit); tile heights vary with t
+  for (int t = 1; t <= std::min(ra.t_max, 31); ++t) sm = std::max(sm, conv_smem(t, 0));
   if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
   k_conv_resid<<<g, 256, sm, s>>>(a);
@@ -1332,7 +1382,7 @@ cudaError_t launch_validate_pair(const float* pub, const float* prv, int channel
   const size_t sm = conv_smem(t, 1);
   if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
-  k_conv_resid<<<g, conv_rows(t) * VT_C / 8, sm, s>>>(a);
+  k_conv_resid<<<g, conv_rows(t) / conv_out(t) * VT_C, sm, s>>>(a);
   k_resid_reduce<<<1, 256, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
   return cudaGetLastError();
 }
