@@ -1238,12 +1238,28 @@ __global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
   }
   const float* X = a.X + size_t(plane) * a.x_plane;
   const float* Y = a.Y + size_t(plane) * a.y_plane;
-  for (int idx = threadIdx.x; idx < th * tw; idx += blockDim.x) {
-    const int li = idx / tw, lj = idx - li * tw;
-    const int gi = i0 - tp + 1 + li, gj = j0 - t + 1 + lj;
-    const bool in = gi >= 0 && gi < xr && gj >= 0 && gj < xc;
-    tile[idx] = in ? double(X[size_t(gi) * a.xld + gj]) : 0.0;
-    if (a.mode == 1) tile2[idx] = in ? double(Y[size_t(gi) * a.yld + gj]) : 0.0;
+  // tile loads in batches of 8 independent loads per thread (memory-level parallelism:
+  // the one-at-a-time loop was long-scoreboard bound)
+  constexpr int LB = 8;
+  for (int base = threadIdx.x; base < th * tw; base += LB * blockDim.x) {
+    float xv[LB], yv[LB];
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int idx = base + u * blockDim.x;
+      const int li = idx / tw, lj = idx - li * tw;
+      const int gi = i0 - tp + 1 + li, gj = j0 - t + 1 + lj;
+      const bool in = idx < th * tw && gi >= 0 && gi < xr && gj >= 0 && gj < xc;
+      xv[u] = in ? __ldg(X + size_t(gi) * a.xld + gj) : 0.f;
+      yv[u] = (in && a.mode == 1) ? __ldg(Y + size_t(gi) * a.yld + gj) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < th * tw) {
+        tile[idx] = double(xv[u]);
+        if (a.mode == 1) tile2[idx] = double(yv[u]);
+      }
+    }
   }
   __syncthreads();
   double num = 0.0, den = 0.0;
@@ -1253,6 +1269,14 @@ __global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
     const int gj = j0 + lj;
     if (gj < co && i0 + li0 < ro) {
       double c1[OUT], c2[OUT];
+      float yq[OUT];  // mode 0: the compared samples, loaded before the convolution
+      if (a.mode == 0) {
+#pragma unroll
+        for (int q = 0; q < OUT; ++q) {
+          const int gi = i0 + li0 + q;
+          yq[q] = gi < ro ? __ldg(Y + size_t(gi) * a.yld + gj) : 0.f;
+        }
+      }
       conv_dispatch<OUT>(tile, tw, kt, t, tp, li0, lj, c1);
       if (a.mode == 1) conv_dispatch<OUT>(tile2, tw, kt2, t, tp, li0, lj, c2);
 #pragma unroll
@@ -1261,7 +1285,7 @@ __global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
         if (gi >= ro) break;
         double y;
         if (a.mode == 0) {
-          y = double(Y[size_t(gi) * a.yld + gj]);
+          y = double(yq[q]);
           den += y * y;
         } else {
           y = c2[q];
