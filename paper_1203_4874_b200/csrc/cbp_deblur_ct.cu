@@ -233,6 +233,109 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a,
   cp_async_wait<0>();
 }
 
+// Pass B with bulk copies (TMA engine): one thread moves each column strip in (a single
+// copy per column, completion on an mbarrier), the filter strip likewise, and the filtered
+// columns back out (bulk stores, drained before the buffer is refilled). Needs an even
+// Mb (16-byte multiple column runs); the rows Mb..G-1 of the tile are zeroed by threads.
+template <class P>
+__global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs a, int planes) {
+  constexpr int NT = P::NT;
+  constexpr int G = P::G, W = P::W, GP = ((G + 11) / 16) * 16 + 4, TILE = GP * W;
+  constexpr int HB = ((G + 1) / 2) * 2;  // filter run: G rounded up to an even count (16-byte multiple)
+  using R = typename P::R;
+  using FFT = FftIP<G, W, GP, 1, NT, false>;
+  static_assert(P::PIPE && !P::HD, "bulk pass B keeps two tile buffers and a staged filter strip");
+  extern __shared__ __align__(16) float2 sm[];
+  float2* Hs = sm + 2 * TILE;
+  __shared__ __align__(8) unsigned long long bar[3];  // tile buffers 0, 1; filter strip
+  const int strips = (a.Hc + W - 1) / W;
+  const int total = planes * strips;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  // zero the padding rows (and absent columns) of buffer `b` for tile `tile`
+  auto pad = [&](int tile, float2* dst) {
+    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    (void)p;
+    for (int s = 0; s < W; ++s) {
+      const int lo = v0 + s < a.Hc ? a.Mb : 0;
+      for (int u = lo + threadIdx.x; u < G; u += NT) dst[s * GP + u] = make_float2(0.f, 0.f);
+    }
+  };
+  auto issue = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
+    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const float2* XT = a.X + size_t(p) * a.x_plane;
+    const int nc = min(W, a.Hc - v0);
+    fence_proxy_async();
+    mbar_expect_tx(b, unsigned(nc) * unsigned(a.Mb) * 8u);
+    for (int s = 0; s < nc; ++s) bulk_g2s(dst + s * GP, XT + size_t(v0 + s) * a.xp, unsigned(a.Mb) * 8u, b);
+  };
+  unsigned ph[2] = {0u, 0u}, phh = 0u;
+  int tile = blockIdx.x;
+  if (tile < total) {
+    pad(tile, sm);
+    if (threadIdx.x == 0) issue(tile, sm, &bar[0]);
+  }
+  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+    const int cb = it & 1;
+    float2* cur = sm + cb * TILE;
+    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const int f = a.slot_per_frame ? p / a.channels : 0;
+    const cbp_kernel_slot* slot = a.slot + f;
+    const int status = slot->status;
+    mbar_wait(&bar[cb], ph[cb]);
+    ph[cb] ^= 1u;
+    __syncthreads();  // tile data and zero padding visible to all threads
+    const int nc = min(W, a.Hc - v0);
+    if (status == 0 && threadIdx.x == 0) {  // filter strip in flight during the forward transform
+      const float2* Ht = a.H + size_t(f) * a.h_frame;
+      fence_proxy_async();
+      mbar_expect_tx(&bar[2], unsigned(nc) * unsigned(HB) * 8u);
+      for (int s = 0; s < nc; ++s) bulk_g2s(Hs + s * GP, Ht + size_t(v0 + s) * a.hp, unsigned(HB) * 8u, &bar[2]);
+    }
+    const int next = tile + gridDim.x;
+    if (next < total) {  // prefetch into the other buffer (its last bulk stores drained first)
+      float2* nb = sm + (cb ^ 1) * TILE;
+      pad(next, nb);
+      if (threadIdx.x == 0) {
+        bulk_wait_read();
+        issue(next, nb, &bar[cb ^ 1]);
+      }
+    }
+    if (status == 0) {  // uniform over the CTA
+      const int t = slot->width;
+      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
+      mbar_wait(&bar[2], phh);
+      phh ^= 1u;
+      __syncthreads();
+      if (!(a.dbg & 2)) {
+        float4* c4 = reinterpret_cast<float4*>(cur);
+        const float4* h4 = reinterpret_cast<const float4*>(Hs);
+        for (int i = threadIdx.x; i < TILE / 2; i += NT) {
+          const float4 x = c4[i], h = h4[i];
+          c4[i] = make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
+                              x.z * h.w + x.w * h.z);
+        }
+      }
+      __syncthreads();
+      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_col, R{});
+      const int M = a.Mb - t + 1;  // even: Mb even, t odd
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        float2* XT = a.X + size_t(p) * a.x_plane;
+        for (int s = 0; s < nc; ++s) bulk_s2g(XT + size_t(v0 + s) * a.xp, cur + s * GP, unsigned(M) * 8u);
+        bulk_commit();
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // ------------------------------------------------- pass C (rows c2r + crop)
 // Tile layout [slot][s] (RPC rows interleaved): one frequency of RPC consecutive rows is
 // one 32-byte chunk of XT, copied straight into its digit-reversed slot pos(k) (X[L] into
@@ -440,13 +543,24 @@ template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
   constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
   const size_t sm = ((P::PIPE ? 2 : 1) + (P::HD ? 0 : 1)) * size_t(GP) * P::W * sizeof(float2);
-  static int pB = 0, sms = 0;
+  static int pB = 0, pT = 0, sms = 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     pB = resident_per_sm(k_cols_filter_ct<P>, P::NT, sm);
+    if constexpr (P::PIPE && !P::HD) {
+      cudaFuncSetAttribute(k_cols_filter_bulk<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+      pT = resident_per_sm(k_cols_filter_bulk<P>, P::NT, sm);
+    }
   }
   const int total = planes * ((a.Hc + P::W - 1) / P::W);
+  if constexpr (P::PIPE && !P::HD) {
+    static const bool bulk = !getenv("CBP_NO_BULK");
+    if (bulk && a.Mb % 2 == 0) {  // column runs of Mb complex values are 16-byte multiples
+      k_cols_filter_bulk<P><<<persistent_grid(pT, sms, a.sm_reserve, total), P::NT, sm, s>>>(a, planes);
+      return;
+    }
+  }
   k_cols_filter_ct<P><<<P::PIPE ? persistent_grid(pB, sms, a.sm_reserve, total) : total, P::NT, sm, s>>>(a, planes);
 }
 
