@@ -51,18 +51,41 @@ __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a
 // Row s of a tile holds z[m] = (x[2m], x[2m+1]); the forward DIF leaves Z[k] in slot pos(k);
 // the r2c split handles the pair (k, L-k) in one thread: X[k] = e + W^k o,
 // X[L-k] = conj(e - W^k o), e = (Z[k] + conj Z[L-k])/2, o = -i (Z[k] - conj Z[L-k])/2.
-template <class P>
+// BULK: the input rows arrive by bulk copies (one per row, TMA engine, completion on an
+// mbarrier; rows 16-byte aligned with a pitch >= Nb rounded to 4); threads then zero the
+// row tails Nb..2L-1 and the rows beyond Mb.
+template <class P, bool BULK = false>
 __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
   using R = typename P::R;
   using FFT = FftIP<L, RPC, L, 1, NT, false>;
+  static_assert(!BULK || (P::PIPE && L % 2 == 0), "bulk rows need two buffers and 16-byte row starts");
   extern __shared__ __align__(16) float2 sm[];
   short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);
   for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
   const bool v16 = a.in_vec4 && (L % 2 == 0);
+  __shared__ __align__(8) unsigned long long bar[2];
+  unsigned ph[2] = {0u, 0u};
+  const unsigned row_bytes = unsigned((a.Nb + 3) & ~3) * 4u;  // 16-byte multiple, within the pitch
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+  }
+  auto issue_bulk = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    const float* src = a.in + size_t(p) * a.in_plane + size_t(r0) * a.in_ld;
+    const int nr = min(RPC, a.Mb - r0);
+    fence_proxy_async();
+    mbar_expect_tx(b, unsigned(nr) * row_bytes);
+    for (int s = 0; s < nr; ++s) bulk_g2s(dst + s * L, src + size_t(s) * a.in_ld, row_bytes, b);
+  };
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     const float* src = a.in + size_t(p) * a.in_plane + size_t(r0) * a.in_ld;
@@ -88,14 +111,31 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     }
   };
   int tile = blockIdx.x;
-  if (tile < total) issue(tile, sm);
-  cp_async_commit();
+  if constexpr (BULK) {
+    if (tile < total && threadIdx.x == 0) issue_bulk(tile, sm, &bar[0]);
+  } else {
+    if (tile < total) issue(tile, sm);
+    cp_async_commit();
+  }
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
     float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int next = tile + gridDim.x;
-    if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (BULK) {
+      const int cb = it & 1;
+      if (next < total && threadIdx.x == 0) issue_bulk(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
+      mbar_wait(&bar[cb], ph[cb]);
+      ph[cb] ^= 1u;
+      const int r0t = (tile - (tile / groups) * groups) * RPC;
+      float* cf = reinterpret_cast<float*>(cur);
+      for (int s = 0; s < RPC; ++s) {  // zero the tails (and the rows past the frame)
+        const int lo = r0t + s < a.Mb ? a.Nb : 0;
+        for (int x = lo + threadIdx.x; x < 2 * L; x += NT) cf[s * 2 * L + x] = 0.f;
+      }
+    } else {
+      if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+      cp_async_commit();
+      cp_async_wait<1>();
+    }
     __syncthreads();
     if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
@@ -132,7 +172,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     }
     __syncthreads();
   }
-  cp_async_wait<0>();
+  if constexpr (!BULK) cp_async_wait<0>();
 }
 
 // ----------------------------------------------- pass B (columns + Wiener filter)
@@ -524,19 +564,33 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
   constexpr int NB = P::PIPE ? 2 : 1;
   const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 3) & ~3) * sizeof(float2) + P::L * sizeof(short);
-  static int pA = 0, pC = 0, sms = 0;
+  static int pA = 0, pC = 0, pAb = 0, sms = 0;
+  constexpr bool kBulk = P::PIPE && P::L % 2 == 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_rows_forward_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
     cudaFuncSetAttribute(k_rows_inverse_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
     pA = resident_per_sm(k_rows_forward_ct<P>, P::NT, smA);
     pC = resident_per_sm(k_rows_inverse_ct<P>, P::NT, smC);
+    if constexpr (kBulk) {
+      cudaFuncSetAttribute(k_rows_forward_ct<P, kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
+      pAb = resident_per_sm(k_rows_forward_ct<P, kBulk>, P::NT, smA);
+    }
   }
   const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
-  if (inverse)
+  if (inverse) {
     k_rows_inverse_ct<P><<<P::PIPE ? persistent_grid(pC, sms, a.sm_reserve, total) : total, P::NT, smC, s>>>(a, planes);
-  else
-    k_rows_forward_ct<P><<<P::PIPE ? persistent_grid(pA, sms, a.sm_reserve, total) : total, P::NT, smA, s>>>(a, planes);
+    return;
+  }
+  if constexpr (kBulk) {
+    static const bool bulk = !getenv("CBP_NO_BULK");
+    // 16-byte aligned rows whose pitch holds Nb rounded up to 4 floats
+    if (bulk && a.in_vec4 && a.in_ld >= ((a.Nb + 3) & ~3)) {
+      k_rows_forward_ct<P, kBulk><<<persistent_grid(pAb, sms, a.sm_reserve, total), P::NT, smA, s>>>(a, planes);
+      return;
+    }
+  }
+  k_rows_forward_ct<P><<<P::PIPE ? persistent_grid(pA, sms, a.sm_reserve, total) : total, P::NT, smA, s>>>(a, planes);
 }
 
 template <class P>
