@@ -7,12 +7,23 @@
 // the next tile's global->shared copies (cp.async, zero-filled outside the frame) are
 // in flight while the current tile is transformed, so HBM/L2 latency overlaps the FFT.
 #include <cstdlib>
+#include <cstring>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "cbp_deblur.cuh"
 #include "cbp_fft_ct.cuh"
 
 namespace cbp_dev {
+
+template <class Rs>
+struct RadixCount;
+template <int... Rs>
+struct RadixCount<Radices<Rs...>> {
+  static constexpr int value = sizeof...(Rs);
+};
 
 
 // PIPE: persistent CTAs with a double-buffered cp.async prefetch of the next tile;
@@ -381,15 +392,18 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
 // one 32-byte chunk of XT, copied straight into its digit-reversed slot pos(k) (X[L] into
 // the spare slot L). The pairwise c2r split works slot to slot in place, the inverse DIT
 // leaves z[n] in natural order, so each thread stores z[n] of all RPC rows.
-template <class P>
-__global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a, int planes) {
+template <class P, bool TMA = false>
+__global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a, int planes,
+                                                                     const __grid_constant__ CUtensorMap tmap) {
   constexpr int NT = P::NT;
-  constexpr int L = P::L, RPC = P::RPC, H = L + 1, TILE = ((H * RPC + 3) & ~3);
+  constexpr int L = P::L, RPC = P::RPC, H = L + 1, TILE = ((H * RPC + 15) & ~15);  // 128-byte buffers
   static_assert(RPC % 2 == 0, "16-byte copies carry two rows");
   using R = typename P::R;
   using FFT = FftIP<L, RPC, 1, RPC, NT, true>;
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm_c[];  // TMA tile destinations: 128-byte aligned
+  float2* const sm = sm_c;
   short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // DIT input slot of z[n]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + (P::PIPE ? 2 : 1) * TILE + (L + 3) / 4);
   for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
   __syncthreads();
   const int groups = (a.Mb + RPC - 1) / RPC;
@@ -411,15 +425,57 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
       cp_async16(dst + slot * RPC + 2 * j, bytes ? XT + size_t(k) * a.xp + 2 * j : a.X, bytes);
     }
   };
+  // TMA: one tensor copy per tile. The map views XT as (row u, digit d_1, ..., digit d_m,
+  // plane), the frequency k split into the radix digits of the column order, so the box
+  // lands with frequency k in slot pos(k) (a digit reversal is a transpose of the digit
+  // axes); X[L] goes to the spare slot by a bulk copy (clipped to the pitch).
+  unsigned ph[2] = {0u, 0u};
+  constexpr int NRAD = RadixCount<R>::value;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+  }
+  auto issue_tma = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
+    const int p = tile / groups, r0 = (tile - p * groups) * RPC;
+    const unsigned tail = unsigned(min(RPC, a.xp - r0)) * 8u;
+    fence_proxy_async();
+    mbar_expect_tx(b, unsigned(RPC) * L * 8u + tail);
+    const unsigned d = smem_u32(dst), bb = smem_u32(b);
+    const unsigned long long tm = reinterpret_cast<unsigned long long>(&tmap);
+    if constexpr (NRAD == 2)
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+          ::"r"(d), "l"(tm), "r"(r0), "r"(0), "r"(0), "r"(p), "r"(bb) : "memory");
+    else
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+          ::"r"(d), "l"(tm), "r"(r0), "r"(0), "r"(0), "r"(0), "r"(p), "r"(bb) : "memory");
+    bulk_g2s(dst + L * RPC, a.X + size_t(p) * a.x_plane + size_t(L) * a.xp + r0, tail, b);
+  };
   int tile = blockIdx.x;
-  if (tile < total) issue(tile, sm);
-  cp_async_commit();
+  if constexpr (TMA) {
+    if (tile < total && threadIdx.x == 0) issue_tma(tile, sm, &bar[0]);
+  } else {
+    if (tile < total) issue(tile, sm);
+    cp_async_commit();
+  }
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
     float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int next = tile + gridDim.x;
-    if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (TMA) {
+      const int cb = it & 1;
+      if (next < total && threadIdx.x == 0) issue_tma(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
+      mbar_wait(&bar[cb], ph[cb]);
+      ph[cb] ^= 1u;
+    } else {
+      if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
+      cp_async_commit();
+      cp_async_wait<1>();
+    }
     __syncthreads();
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     const int M = rows_of(p);
@@ -476,7 +532,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
     }
     __syncthreads();
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
 }
 
 // --------------------------------------------- Wiener filter tables (per slot)
@@ -559,12 +615,58 @@ __host__ inline int persistent_grid(int per_sm, int sms, int reserve, int total)
   return total < g ? total : g;
 }
 
+// Tensor map for pass C's tile loads: XT viewed as (u, d_1, ..., d_m, plane) with frequency
+// k = sum_i d_i N/(R_1...R_i), i.e. the slot order of the DIT input; box (RPC, R_1, ..., R_m, 1).
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool ct_radices(int n, bool column, std::vector<int>& r);
+
+template <class P>
+bool rows_inverse_tmap(const DeblurArgs& a, int planes, CUtensorMap* map) {
+  std::vector<int> rad;
+  ct_radices(P::L, false, rad);
+  auto enc = tmap_encoder();
+  if (!enc || rad.size() + 2 > 5 || (a.xp * 8) % 16 || (size_t(a.x_plane) * 8) % 16 ||
+      reinterpret_cast<uintptr_t>(a.X) % 16)
+    return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5];
+  const int rank = int(rad.size()) + 2;
+  dims[0] = cuuint64_t(a.Mb);
+  box[0] = P::RPC;
+  size_t step = P::L;  // frequency stride of digit i: N / (R_1 ... R_i)
+  for (size_t i = 0; i < rad.size(); ++i) {
+    step /= rad[i];
+    dims[i + 1] = cuuint64_t(rad[i]);
+    box[i + 1] = cuuint32_t(rad[i]);
+    strides[i] = cuuint64_t(step * a.xp * 8);
+  }
+  dims[rank - 1] = cuuint64_t(planes);
+  box[rank - 1] = 1;
+  strides[rank - 2] = cuuint64_t(size_t(a.x_plane) * 8);
+  for (int i = 0; i < rank; ++i) estr[i] = 1;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank), const_cast<float2*>(a.X), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class P>
 void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
   constexpr int NB = P::PIPE ? 2 : 1;
   const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
-  const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 3) & ~3) * sizeof(float2) + P::L * sizeof(short);
-  static int pA = 0, pC = 0, pAb = 0, sms = 0;
+  const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 15) & ~15) * sizeof(float2) +
+                     size_t((P::L + 3) / 4) * sizeof(float2) + 2 * sizeof(unsigned long long);
+  static int pA = 0, pC = 0, pAb = 0, pCt = 0, sms = 0;
   constexpr bool kBulk = P::PIPE && P::L % 2 == 0;
   if (!sms) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -576,10 +678,24 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
       cudaFuncSetAttribute(k_rows_forward_ct<P, kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
       pAb = resident_per_sm(k_rows_forward_ct<P, kBulk>, P::NT, smA);
     }
+    if constexpr (P::PIPE) {
+      cudaFuncSetAttribute(k_rows_inverse_ct<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
+      pCt = resident_per_sm(k_rows_inverse_ct<P, true>, P::NT, smC);
+    }
   }
   const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
   if (inverse) {
-    k_rows_inverse_ct<P><<<P::PIPE ? persistent_grid(pC, sms, a.sm_reserve, total) : total, P::NT, smC, s>>>(a, planes);
+    CUtensorMap map;
+    if constexpr (P::PIPE) {
+      static const bool tma = !getenv("CBP_NO_BULK");
+      if (tma && rows_inverse_tmap<P>(a, planes, &map)) {
+        k_rows_inverse_ct<P, true><<<persistent_grid(pCt, sms, a.sm_reserve, total), P::NT, smC, s>>>(a, planes, map);
+        return;
+      }
+    }
+    memset(&map, 0, sizeof(map));
+    k_rows_inverse_ct<P><<<P::PIPE ? persistent_grid(pC, sms, a.sm_reserve, total) : total, P::NT, smC, s>>>(a, planes,
+                                                                                                              map);
     return;
   }
   if constexpr (kBulk) {
