@@ -214,7 +214,8 @@ def run_reference(args, world, rank):
 
 
 # --------------------------------------------------------------- B200 arm
-SM_RESERVE = 16
+SM_RESERVE = int(os.environ.get("CBP_BENCH_SM_RESERVE", "16"))
+REC_STREAMS = int(os.environ.get("CBP_BENCH_REC_STREAMS", "2"))  # recoveries in flight
 
 
 def run_b200(args, world, rank, local):
@@ -247,45 +248,50 @@ def run_b200(args, world, rank, local):
     cfg = api.make_cfg(9, 25, 1e-6, validate=True)
     torch.cuda.synchronize(dev)
 
-    # Recovery (decode_frame on frame 0) of epoch s+1 runs on its own stream and context
-    # while epoch s deconvolves: the recovery kernels occupy few SMs and are latency
-    # bound, the deconvolution passes fill the GPU. Epochs are independent (no shared
-    # buffers: slots/outputs are per epoch, workspaces per context).
+    # Recovery (decode_frame on frame 0) of the next epochs runs on recovery streams (one
+    # context each: separate workspaces) while epoch s deconvolves: the recovery kernels are
+    # latency bound on few SMs, the deconvolution passes fill the GPU. Epochs are
+    # independent (slots/outputs are per epoch). An epoch's buffers are reused only after
+    # its previous deconvolution finished (deb_ev).
     from paper_1203_4874_b200 import _native
-    ctx_rec = _native.Context(local)
-    # The recovery chain is latency bound: its stream has the higher priority and the
-    # deconvolution's persistent grids leave it SM_RESERVE SMs (measured on B200: 16 SMs
-    # + priority -> 12.8k frames/s, vs 10.1k with neither).
-    s_rec = torch.cuda.Stream(dev, priority=-1)
+    # The recovery chains have the higher priority and the deconvolution's persistent
+    # grids leave them SM_RESERVE SMs' worth of slots.
+    ctx_rec = [_native.Context(local) for _ in range(REC_STREAMS)]
+    s_rec = [torch.cuda.Stream(dev, priority=-1) for _ in range(REC_STREAMS)]
     api.set_sm_reserve(SM_RESERVE, device=local)
     s_deb = torch.cuda.current_stream(dev)
     dec_ev = [torch.cuda.Event() for _ in range(E)]
+    deb_ev = [torch.cuda.Event() for _ in range(E)]
+    if E < REC_STREAMS + 2:
+        raise ValueError(f"--pool must be >= {REC_STREAMS + 2} for the pipelined step")
 
     def issue_decode(s):
         # dec_ev[e] after the whole recovery frame (validation included): measured on B200,
         # releasing the deconvolution at slot-ready (decode_frames_async(slot_ready=...))
         # overlaps the FP64 validation with it and costs ~13% of throughput
-        e = s % E
-        api.decode_frames_async(pub[e, 0:1], prv[e], cfg, out[e, 0:1], slots[e], ctx=ctx_rec, stream=s_rec)
-        dec_ev[e].record(s_rec)
+        e, r = s % E, s % REC_STREAMS
+        s_rec[r].wait_event(deb_ev[e])  # the epoch's previous deconvolution read its slot
+        api.decode_frames_async(pub[e, 0:1], prv[e], cfg, out[e, 0:1], slots[e], ctx=ctx_rec[r], stream=s_rec[r])
+        dec_ev[e].record(s_rec[r])
 
     def issue_deblur(s):
         e = s % E
         s_deb.wait_event(dec_ev[e])
         api.spectral_deblur_slot(pub[e, 1:], slots[e].data_ptr(), out[e, 1:], stream=s_deb)
+        deb_ev[e].record(s_deb)
 
     def run_steps(n, start=0):
-        """n pipelined steps: all n recoveries and n deconvolution batches are enqueued."""
-        if E < 3:
-            raise ValueError("--pool must be >= 3 for the pipelined step")
-        issue_decode(start)
+        """n pipelined steps: recoveries run REC_STREAMS epochs ahead of the deconvolution."""
+        for s in range(start, start + min(REC_STREAMS, n)):
+            issue_decode(s)
         for s in range(start, start + n):
-            if s + 1 < start + n:
-                issue_decode(s + 1)
+            if s + REC_STREAMS < start + n:
+                issue_decode(s + REC_STREAMS)
             issue_deblur(s)
-        done = torch.cuda.Event()
-        done.record(s_rec)
-        s_deb.wait_event(done)
+        for st in s_rec:
+            done = torch.cuda.Event()
+            done.record(st)
+            s_deb.wait_event(done)
 
     def step(s):
         run_steps(1, s)
@@ -314,17 +320,18 @@ def run_b200(args, world, rank, local):
         s += 1
         if s % 8 == 0:
             torch.cuda.synchronize(dev)
-    launches0 = api.launch_count(local) + int(_native.lib().cbp_launch_count(ctx_rec.ptr))
+    launches0 = api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec)
     barrier(world)
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    s_rec.wait_event(ev0)
+    for st in s_rec:
+        st.wait_event(ev0)
     run_steps(args.steps)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     barrier(world)
-    launches = api.launch_count(local) + int(_native.lib().cbp_launch_count(ctx_rec.ptr)) - launches0
+    launches = api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec) - launches0
     ms_rank = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
     ms = max_over_ranks(ms_rank, world)
@@ -336,7 +343,8 @@ def run_b200(args, world, rank, local):
     torch.cuda.synchronize(dev)
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pe0.record(stream)
-    s_rec.wait_event(pe0)
+    for st in s_rec:
+        st.wait_event(pe0)
     run_steps(args.profile_steps)
     pe1.record(stream)
     torch.cuda.synchronize(dev)
@@ -408,8 +416,9 @@ def run_b200(args, world, rank, local):
                                        "(1 decode_frame + 29 spectral_deblur per step)",
                            "rows": ROWS, "cols": COLS, "channels": CH, "kernel_width": T,
                            "frames_per_step": EPOCH, "pool_epochs": E,
-                           "schedule": "recovery of epoch s+1 overlapped with deconvolution of epoch s "
-                                       f"(2 streams; recovery stream high priority; deconvolution leaves {SM_RESERVE} SMs)",
+                           "schedule": f"recoveries of epochs s+1..s+{REC_STREAMS} overlapped with deconvolution of epoch s "
+                                       f"({REC_STREAMS} high-priority recovery streams + 1 deconvolution stream; "
+                                       f"deconvolution leaves {SM_RESERVE} SMs)",
                            "l2": "inputs larger than L2 (each step reads 0.76 GB of distinct frames)",
                            "decode_cfg": "search 9..25, tau 1e-6, default epsilon, validate=true",
                            "parallelism": f"{world} independent GPU(s), no data-path collective"},
