@@ -126,7 +126,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.ld = ld;
   a.t_max = t_max;
   a.lmax = std::max(rows, cols);
-  a.nrb = (rows + 63) / 64;  // row blocks of rows_per_block(t) <= 64 + t - 1 rows
+  fold_plan(batch, rows, cols, t_max, a.ncb, a.fold_rh, a.part_stride);
   a.search_min = smin;
   a.search_max = smax;
   a.nsizes = smax >= smin ? (smax - smin) / 2 + 1 : 0;
@@ -147,7 +147,8 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
     off += (bytes + 255) & ~size_t(255);
     return o;
   };
-  const size_t o_part = take(B * 2 * a.nrb * T * cols * sizeof(double));
+  const size_t o_part = take(B * 2 * a.part_stride * sizeof(double));
+  const size_t o_part2 = take(B * 2 * a.ncb * T * rows * sizeof(double));
   const size_t o_slices = take(B * 4 * T * L * sizeof(double2));
   const size_t o_values = take(B * 2 * T * T * sizeof(double2));
   const size_t o_gaps = take(B * 2 * T * sizeof(double));
@@ -161,6 +162,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   char* base = static_cast<char*>(workspace(ctx, WS_MISC, off));
   if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   a.part = reinterpret_cast<double*>(base + o_part);
+  a.part2 = reinterpret_cast<double*>(base + o_part2);
   a.slices = reinterpret_cast<double2*>(base + o_slices);
   a.values = reinterpret_cast<double2*>(base + o_values);
   a.gaps = reinterpret_cast<double*>(base + o_gaps);

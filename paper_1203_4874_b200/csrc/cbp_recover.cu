@@ -3,6 +3,8 @@
 // Every stage keeps the reference's FP64 arithmetic (decoder.cpp, poly.cpp, fft.cpp);
 // inputs are the FP32 frames as stored in HBM.
 #include "cbp_linalg.cuh"
+#include <algorithm>
+#include <cstdio>
 #include <type_traits>
 
 #include "cbp_recover.cuh"
@@ -48,39 +50,127 @@ cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaS
 __device__ __forceinline__ int fold_width(const RecoverArgs& a, int b, int t_fixed) {
   return t_fixed > 0 ? t_fixed : a.slots[b].width;
 }
-__device__ __forceinline__ int rows_per_block(int t) { return t * ((64 + t - 1) / t); }
-
 // ---------------------------------------------------- polynomial evaluation
-// Z1 fold (fft.cpp:206-208): fold[r][n] = sum_{m = r mod t} luma[m][n]. Partial sums
-// per block of rows_per_block(t) rows; grid (ceil(cols/256), nrb, batch*2).
-__global__ void __launch_bounds__(256) k_fold_z1_part(RecoverArgs a, int t_fixed) {
+// Both folds (fft.cpp:206-212) from ONE read of each frame. A CTA owns a strip of FT_W
+// columns and a block of fold_rows(t) = t * FT_J * G rows, walked residue-major: step
+// (r, g) loads the FT_J rows r0 + r + t (FT_J g + j), so
+//  - Z1: thread = column; the rows of one step share the residue r, so the partial
+//    fold[r][n] over the block is one register (ascending rows), written per residue;
+//  - Z2: the step's luma tile goes to shared memory and warp j folds row j over the strip
+//    by column residue (lanes = residue x contiguous column part, parts combined in order).
+// The next step's samples are fetched before the current one is folded. Partials are
+// reduced in a fixed order by k_fold_z1_dft / k_fold_z2_dft (deterministic sums).
+// Also flags negative luma (decoder.cpp:52) and non-finite samples (image.cpp:33).
+// The block height adapts to the problem (a.fold_rh, set by plan_recover for ~1200 CTAs):
+// small frames get short blocks (latency), large batches long ones (fewer partials).
+constexpr int FT_W = 256, FT_J = 8;
+__host__ __device__ __forceinline__ int fold_groups(int t, int rh) {
+  const int g = (rh + FT_J * t - 1) / (FT_J * t);
+  return g < 1 ? 1 : (g > 32 ? 32 : g);
+}
+__host__ __device__ __forceinline__ int fold_rows(int t, int rh) { return t * FT_J * fold_groups(t, rh); }
+
+template <int C>
+__global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
+  __shared__ double tile[2][FT_J][FT_W];
   const int b = blockIdx.z >> 1, q = blockIdx.z & 1;
-  const cbp_kernel_slot* slot = a.slots + b;
+  cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0) return;
   const int t = fold_width(a, b, t_fixed);
   if (t <= 0) return;
-  const int RB = rows_per_block(t);
-  const int rb = blockIdx.y;
-  const int r0 = rb * RB;
+  const int G = fold_groups(t, a.fold_rh), RH = t * FT_J * G;
+  const int r0 = blockIdx.y * RH;
   if (r0 >= a.rows) return;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= a.cols) return;
+  const int r1 = min(r0 + RH, a.rows);
+  const int c0 = blockIdx.x * FT_W, n = c0 + threadIdx.x;
+  const bool col_ok = n < a.cols;
   const size_t plane = size_t(a.rows) * a.ld;
-  const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane;
-  const int r1 = min(r0 + RB, a.rows);
-  double* out = a.part + (((size_t(b) * 2 + q) * a.nrb + rb) * a.t_max) * a.cols + n;
-  for (int r = 0; r < t; ++r) {
-    double acc = 0.0;
-#pragma unroll 4
-    for (int m = r0 + r; m < r1; m += t) acc += luma_at(base, plane, a.channels, size_t(m) * a.ld + n);
-    out[size_t(r) * a.cols] = acc;
+  const float* base = (q ? a.prv : a.pub) + size_t(b) * C * plane + (col_ok ? n : 0);
+  double* p1 = a.part + (size_t(b) * 2 + q) * a.part_stride + size_t(blockIdx.y) * t * a.cols + n;
+  double* p2 = a.part2 + ((size_t(b) * 2 + q) * a.ncb + blockIdx.x) * size_t(a.t_max) * a.rows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Z2 lanes: residue rz, contiguous column part hz of H (t > 32: lanes loop residues)
+  const int H = t <= 32 ? 32 / t : 1;
+  const int rz = lane % t, hz = lane / t;
+  const int lo = hz < H ? hz * FT_W / H : 0, hi = hz < H ? (hz + 1) * FT_W / H : 0;
+  float cur[FT_J][C], nxt[FT_J][C];
+  auto fetch = [&](int r, int g, float (&x)[FT_J][C]) {
+#pragma unroll
+    for (int j = 0; j < FT_J; ++j) {
+      const int m = r0 + r + t * (FT_J * g + j);
+      const bool ok = col_ok && m < r1;
+#pragma unroll
+      for (int c = 0; c < C; ++c) x[j][c] = ok ? __ldg(base + size_t(m) * a.ld + c * plane) : 0.f;
+    }
+  };
+  bool neg = false, bad = false;
+  double acc = 0.0;
+  int r = 0, g = 0;
+  fetch(0, 0, cur);
+  const int steps = t * G;
+  for (int it = 0; it < steps; ++it) {
+    int rn = r, gn = g + 1;
+    if (gn == G) gn = 0, rn = r + 1;
+    if (rn < t) fetch(rn, gn, nxt);
+    double* tl = &tile[it & 1][0][0];
+#pragma unroll
+    for (int j = 0; j < FT_J; ++j) {
+      double v;
+      if constexpr (C == 1) {
+        v = double(cur[j][0]);
+      } else {  // unfused, as luma_at (bit-identical to the CPU restatement)
+        v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, double(cur[j][0])), __dmul_rn(0.587, double(cur[j][1]))),
+                      __dmul_rn(0.114, double(cur[j][2])));
+      }
+      neg |= v < 0.0;
+      bad |= !isfinite(v);
+      acc += v;
+      tl[j * FT_W + threadIdx.x] = v;
+    }
+    if (gn == 0) {  // residue r done
+      if (col_ok) p1[size_t(r) * a.cols] = acc;
+      acc = 0.0;
+    }
+    __syncthreads();
+    const int m = r0 + r + t * (FT_J * g + warp);
+    if (m < r1) {  // warp-uniform
+      if (t <= 32) {
+        double sz = 0.0;
+        // first column of part hz with absolute residue rz
+        for (int c = lo + ((rz - (c0 + lo) % t) % t + t) % t; c < hi; c += t) sz += tl[warp * FT_W + c];
+        for (int hh = 1; hh < H; ++hh) {
+          const double o = __shfl_sync(0xffffffffu, sz, min(lane + t * hh, 31));
+          if (hz == 0) sz += o;
+        }
+        if (hz == 0) p2[size_t(rz) * a.rows + m] = sz;
+      } else {
+        for (int rr = lane; rr < t; rr += 32) {
+          double sz = 0.0;
+          for (int c = ((rr - c0 % t) % t + t) % t; c < FT_W; c += t) sz += tl[warp * FT_W + c];
+          p2[size_t(rr) * a.rows + m] = sz;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < FT_J; ++j)
+#pragma unroll
+      for (int c = 0; c < C; ++c) cur[j][c] = nxt[j][c];
+    r = rn;
+    g = gn;
+  }
+  neg = __syncthreads_or(neg);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    if (neg) atomicOr(a.flags + b, 1);
+    if (bad) slot_fail(slot, CBP_RANGE_EXCEEDED, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_NONFINITE);
   }
 }
 
-// Sum the row-block partials in a fixed order, then the t x t DFT epilogue:
-// slice_i[n] = sum_r W(i, r) fold[r][n], W(i, r) = exp(-2 pi i ((i r) mod t) / t)
-// (fft.cpp:203-208). grid (ceil(cols/128), batch*2), smem t_max*128 doubles + roots.
-__global__ void __launch_bounds__(128) k_fold_z1_dft(RecoverArgs a, int t_fixed) {
+// Sum the partials in a fixed order (Z1: row blocks of column n; Z2: column strips of row
+// m), then the t x t DFT epilogue: slice_i[x] = sum_r W(i, r) fold[r][x],
+// W(i, r) = exp(-2 pi i ((i r) mod t) / t) (fft.cpp:203-212). One launch for both axes:
+// blocks [0, ceil(cols/128)) do Z1, the rest Z2. grid (.., batch*2), smem t_max*128 doubles + roots.
+__global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
   extern __shared__ double sh[];
   const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
   const cbp_kernel_slot* slot = a.slots + b;
@@ -91,17 +181,28 @@ __global__ void __launch_bounds__(128) k_fold_z1_dft(RecoverArgs a, int t_fixed)
   double* fold = sh + 2 * a.t_max;
   for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
   __syncthreads();
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= a.cols) return;
-  const int RB = rows_per_block(t);
-  const int nrb = (a.rows + RB - 1) / RB;
-  const double* part = a.part + ((size_t(b) * 2 + q) * a.nrb * a.t_max) * a.cols + n;
-  for (int r = 0; r < t; ++r) {
-    double acc = 0.0;
-    for (int rb = 0; rb < nrb; ++rb) acc += part[(size_t(rb) * a.t_max + r) * a.cols];
-    fold[r * blockDim.x + threadIdx.x] = acc;
+  const int nb1 = (a.cols + 127) / 128;
+  const bool z1 = int(blockIdx.x) < nb1;
+  const int x = (z1 ? blockIdx.x : blockIdx.x - nb1) * blockDim.x + threadIdx.x;
+  if (x >= (z1 ? a.cols : a.rows)) return;
+  if (z1) {
+    const int RB = fold_rows(t, a.fold_rh);
+    const int nrb = (a.rows + RB - 1) / RB;
+    const double* part = a.part + (size_t(b) * 2 + q) * a.part_stride + x;
+    for (int r = 0; r < t; ++r) {
+      double acc = 0.0;
+      for (int rb = 0; rb < nrb; ++rb) acc += part[(size_t(rb) * t + r) * a.cols];
+      fold[r * blockDim.x + threadIdx.x] = acc;
+    }
+  } else {
+    const double* part = a.part2 + (size_t(b) * 2 + q) * a.ncb * size_t(a.t_max) * a.rows + x;
+    for (int r = 0; r < t; ++r) {
+      double acc = 0.0;
+      for (int cb = 0; cb < a.ncb; ++cb) acc += part[(size_t(cb) * a.t_max + r) * a.rows];
+      fold[r * blockDim.x + threadIdx.x] = acc;
+    }
   }
-  double2* out = a.slices + slice_offset(a, b, 0, q, 0) + n;
+  double2* out = a.slices + slice_offset(a, b, z1 ? 0 : 1, q, 0) + x;
   for (int i = 0; i < t; ++i) {
     double re = 0.0, im = 0.0;
     int idx = 0;
@@ -116,80 +217,31 @@ __global__ void __launch_bounds__(128) k_fold_z1_dft(RecoverArgs a, int t_fixed)
   }
 }
 
-// Z2 fold (fft.cpp:210-212), one 128-thread CTA per row: thread -> (residue r, part h) sums
-// columns r + t*(h + nh*j) in a register; the nh parts are combined in a fixed order, then
-// the t-point DFT epilogue. Also flags negative luma (decoder.cpp:52) and non-finite
-// samples (image.cpp:33). grid (rows, batch*2).
-__global__ void __launch_bounds__(128) k_fold_z2(RecoverArgs a, int t_fixed) {
-  __shared__ double2 root[CBP_MAX_WIDTH];
-  __shared__ double acc[128 + CBP_MAX_WIDTH];
-  __shared__ double fold[CBP_MAX_WIDTH];
-  const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
-  cbp_kernel_slot* slot = a.slots + b;
-  if (slot->status != 0) return;
-  const int t = fold_width(a, b, t_fixed);
-  if (t <= 0) return;
-  for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
-  const int m = blockIdx.x;
-  const size_t plane = size_t(a.rows) * a.ld;
-  const float* base = (q ? a.prv : a.pub) + size_t(b) * a.channels * plane + size_t(m) * a.ld;
-  const int nh = t <= 128 ? 128 / t : 1;
-  bool neg = false, bad = false;
-  for (int rr = threadIdx.x; rr < t * nh; rr += blockDim.x) {
-    const int r = rr % t, h = rr / t;
-    double racc = 0.0;
-#pragma unroll 4
-    for (int n = r + t * h; n < a.cols; n += t * nh) {
-      const double x = luma_at(base, plane, a.channels, n);
-      neg |= x < 0.0;
-      bad |= !isfinite(x);
-      racc += x;
-    }
-    acc[rr] = racc;
-  }
-  neg = __syncthreads_or(neg);
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
-    if (neg) atomicOr(a.flags + b, 1);
-    if (bad) slot_fail(slot, CBP_RANGE_EXCEEDED, CBP_STAGE_NONE, -1, -1, 0.0, CBP_REASON_NONFINITE);
-  }
-  for (int rr = threadIdx.x; rr < t; rr += blockDim.x) {
-    double s = 0.0;
-    for (int hh = 0; hh < nh; ++hh) s += acc[hh * t + rr];
-    fold[rr] = s;
-  }
-  __syncthreads();
-  double2* out = a.slices + slice_offset(a, b, 1, q, 0) + m;
-  for (int i = threadIdx.x; i < t; i += blockDim.x) {
-    double re = 0.0, im = 0.0;
-    int idx = 0;
-    for (int rr = 0; rr < t; ++rr) {
-      re = fma(root[idx].x, fold[rr], re);
-      im = fma(root[idx].y, fold[rr], im);
-      idx += i;
-      if (idx >= t) idx -= t;
-    }
-    out[size_t(i) * a.lmax] = make_double2(re, im);
-  }
-}
-
 cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
-  const int tm = t_fixed > 0 ? t_fixed : a.t_max;
-  RecoverArgs b = a;
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_fold_z1_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_fold_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cfg = true;
   }
-  dim3 g1((a.cols + 255) / 256, a.nrb, a.batch * 2);
-  k_fold_z1_part<<<g1, 256, 0, s>>>(b, t_fixed);
-  dim3 g2((a.cols + 127) / 128, a.batch * 2);
-  size_t sm2 = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
-  k_fold_z1_dft<<<g2, 128, sm2, s>>>(b, t_fixed);
-  dim3 g3(a.rows, a.batch * 2);
-  k_fold_z2<<<g3, 128, 0, s>>>(b, t_fixed);
-  (void)tm;
+  if (a.channels != 1 && a.channels != 3) return cudaErrorInvalidValue;
+  // row blocks: grid.y covers the shortest blocks (t = 1); taller ones exit at once
+  const int tmin = t_fixed > 0 ? t_fixed : 1;
+  dim3 g1(a.ncb, (a.rows + fold_rows(tmin, a.fold_rh) - 1) / fold_rows(tmin, a.fold_rh), a.batch * 2);
+  if (a.channels == 1) k_fold_tile<1><<<g1, 256, 0, s>>>(a, t_fixed);
+  else k_fold_tile<3><<<g1, 256, 0, s>>>(a, t_fixed);
+  const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
+  dim3 g2((a.cols + 127) / 128 + (a.rows + 127) / 128, a.batch * 2);
+  k_fold_dft<<<g2, 128, smf, s>>>(a, t_fixed);
   return cudaGetLastError();
+}
+
+// Fold workspace geometry (plan_recover): target rows per block for ~1200 CTAs, Z1 partial
+// doubles per (frame, stream) for any t (blocks of >= 8 t rows: <= rows/8 + t rows of partials).
+void fold_plan(int batch, int rows, int cols, int t_max, int& ncb, int& rh, size_t& part_stride) {
+  ncb = (cols + FT_W - 1) / FT_W;
+  const int want = std::max(1, 1200 / std::max(1, ncb * 2 * batch));
+  rh = std::max(1, (rows + want - 1) / want);
+  part_stride = (size_t(rows) / FT_J + t_max + 1) * cols;
 }
 
 // -------------------------------------------------- kernel degree estimation

@@ -15,8 +15,11 @@ struct RecoverArgs {
   int t_max;                            // upper bound of t over the batch
   int lmax;                             // max(rows, cols)
   // fold workspaces
-  double* part;       // [batch][2][nrb][t_max][cols]
-  int nrb;            // row blocks (rows per block >= 128)
+  double* part;       // Z1 partials [batch][2][part_stride]: [row block][t][cols]
+  size_t part_stride;
+  int fold_rh;        // target rows per fold block (fold_plan)
+  double* part2;      // Z2 partials [batch][2][ncb][t_max][rows]
+  int ncb;            // column strips of the fold (256 columns)
   double2* slices;    // [batch][2 axes][2 streams][t_max][lmax]
   // solve outputs
   double2* values;    // [batch][2 axes][t_max][t_max]
@@ -49,6 +52,7 @@ struct HintChunk {
 cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaStream_t s);
 // t_fixed > 0 folds with that t (1 = DC sums); otherwise with slots[b].width.
 cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s);
+void fold_plan(int batch, int rows, int cols, int t_max, int& ncb, int& rh, size_t& part_stride);
 cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s);
 // signed content (decoder.cpp:65-82): replaces the DC slices of frames with a negative
 // luma sample by the maximum-energy axis_spectrum_half slices (cbp_signed.cu)
