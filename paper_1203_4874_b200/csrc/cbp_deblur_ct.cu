@@ -557,46 +557,55 @@ __global__ void k_wiener_s(DeblurArgs a, int frames) {
 }
 
 // H[f][u][v] = conj(K)/(|K|^2 + eps) / (Gr*Gc), K(u,v) = sum_a S[v][a] exp(-2 pi i u a / Gr)
-// in FP64 (decoder.cpp:209-211, fft.cpp:268); grid (ceil(Gr/32), ceil(Hc/8), frames):
-// lanes run along u so each warp writes within one table column.
-__global__ void __launch_bounds__(256) k_wiener_h(DeblurArgs a, int frames) {
-  __shared__ double2 Ss[8 * CBP_MAX_WIDTH];
+// in FP64 (decoder.cpp:209-211, fft.cpp:268). Thread = one u and WH_V consecutive v: the
+// powers of W_Gr^u (recurrence from one sincos; drift ~t ulp, far below the float2 the
+// table is stored in) are shared by the WH_V sums. grid (ceil(Gr/128), ceil(Hc/WH_V), frames).
+constexpr int WH_V = 8;
+__global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
+  __shared__ double2 Ss[WH_V * CBP_MAX_WIDTH];
   const int f = blockIdx.z;
   const cbp_kernel_slot* slot = a.slot + f;
   if (slot->status != 0) return;
   const int t = slot->width;
-  const int v0 = blockIdx.y * 8;
+  const int v0 = blockIdx.y * WH_V;
   const double2* S = a.S + size_t(f) * a.s_frame;
-  for (int i = threadIdx.x; i < 8 * t; i += blockDim.x) {
+  for (int i = threadIdx.x; i < WH_V * t; i += blockDim.x) {
     const int vv = i / t, ai = i - vv * t;
-    Ss[i] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
+    Ss[ai * WH_V + vv] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int vv = threadIdx.x >> 5, v = v0 + vv;
-  const int u = blockIdx.x * 32 + (threadIdx.x & 31);
-  if (v >= a.Hc || u >= a.Gr) return;
-  // powers of W_Gr^u by recurrence (one sincos per thread; drift ~t ulp, far below the
-  // float2 the table is stored in)
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.Gr) return;
   const double2 wu = zroot(u, a.Gr);
-  double2 w = make_double2(1.0, 0.0), acc = make_double2(0.0, 0.0);
+  double2 w = make_double2(1.0, 0.0);
+  double2 acc[WH_V];
+#pragma unroll
+  for (int vv = 0; vv < WH_V; ++vv) acc[vv] = make_double2(0.0, 0.0);
   for (int ai = 0; ai < t; ++ai) {
-    acc = zadd(acc, zmul(Ss[vv * t + ai], w));
+#pragma unroll
+    for (int vv = 0; vv < WH_V; ++vv) acc[vv] = zadd(acc[vv], zmul(Ss[ai * WH_V + vv], w));
     w = zmul(w, wu);
   }
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
-  const double den = (acc.x * acc.x + acc.y * acc.y + slot->epsilon);
   // transposed table HT[v][slot(u)]: slot(u) = pos(u) of the column plan (a.hpos), so pass B
   // multiplies element-wise in its DIF output order
   const int su = a.hpos ? int(a.hpos[u]) : u;
-  a.H[size_t(f) * a.h_frame + size_t(v) * a.hp + su] =
-      make_float2(float(acc.x * sc / den), float(-acc.y * sc / den));
+  float2* H = a.H + size_t(f) * a.h_frame + su;
+#pragma unroll
+  for (int vv = 0; vv < WH_V; ++vv) {
+    const int v = v0 + vv;
+    if (v < a.Hc) {
+      const double g = sc / (acc[vv].x * acc[vv].x + acc[vv].y * acc[vv].y + slot->epsilon);
+      H[size_t(v) * a.hp] = make_float2(float(acc[vv].x * g), float(-acc[vv].y * g));
+    }
+  }
 }
 
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s) {
   dim3 g1((a.Hc * CBP_MAX_WIDTH + 255) / 256, frames);
   k_wiener_s<<<g1, 256, 0, s>>>(a, frames);
-  dim3 g2((a.Gr + 31) / 32, (a.Hc + 7) / 8, frames);
-  k_wiener_h<<<g2, 256, 0, s>>>(a, frames);
+  dim3 g2((a.Gr + 127) / 128, (a.Hc + WH_V - 1) / WH_V, frames);
+  k_wiener_h<<<g2, 128, 0, s>>>(a, frames);
   return cudaGetLastError();
 }
 
