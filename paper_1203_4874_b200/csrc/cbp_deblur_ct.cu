@@ -241,7 +241,24 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a,
     const int next = tile + gridDim.x;
     if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
     cp_async_commit();
-    if (status == 0) {  // uniform over the CTA
+    if (status == 0 && !P::HD && !a.dbg) {  // fused filter stage (see k_cols_filter_bulk)
+      const int t = slot->width;
+      FFT::dif_head(cur, a.twst_col, R{});
+      cp_async_wait<1>();
+      __syncthreads();  // filter strip (copied by all threads) visible
+      FFT::filter_stage(cur, Hs, R{});
+      FFT::dit_tail(cur, a.twst_col, R{});
+      const int M = a.Mb - t + 1;
+      float2* XT = a.X + size_t(p) * a.x_plane;
+#pragma unroll
+      for (int s = 0; s < W; ++s) {
+        if (v0 + s >= a.Hc) break;
+        float2* col = XT + size_t(v0 + s) * a.xp;
+        const float4* src = reinterpret_cast<const float4*>(cur + s * GP);
+        for (int c = threadIdx.x; c < M / 2; c += NT) reinterpret_cast<float4*>(col)[c] = src[c];
+        if ((M & 1) && threadIdx.x == 0) col[M - 1] = cur[s * GP + M - 1];
+      }
+    } else if (status == 0) {  // uniform over the CTA
       const int t = slot->width;
       if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
       cp_async_wait<1>();
@@ -357,7 +374,22 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
         issue(next, nb, &bar[cb ^ 1]);
       }
     }
-    if (status == 0) {  // uniform over the CTA
+    if (status == 0 && !a.dbg) {  // uniform over the CTA
+      // fused: DIF head, (last DIF stage, filter, first DIT stage) in registers, DIT tail
+      const int t = slot->width;
+      FFT::dif_head(cur, a.twst_col, R{});
+      mbar_wait(&bar[2], phh);  // every thread observes the filter strip's arrival
+      phh ^= 1u;
+      FFT::filter_stage(cur, Hs, R{});
+      FFT::dit_tail(cur, a.twst_col, R{});
+      const int M = a.Mb - t + 1;  // even: Mb even, t odd
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        float2* XT = a.X + size_t(p) * a.x_plane;
+        for (int s = 0; s < nc; ++s) bulk_s2g(XT + size_t(v0 + s) * a.xp, cur + s * GP, unsigned(M) * 8u);
+        bulk_commit();
+      }
+    } else if (status == 0) {  // profiling variants (a.dbg): separate filter pass
       const int t = slot->width;
       if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
       mbar_wait(&bar[2], phh);

@@ -215,6 +215,42 @@ struct FftIP {
     stage<false, INV, R, PP>(buf, tw);
   }
 
+  // Filtered round trip x -> DIT_inv(H .* DIF_fwd(x)) split so that the last DIF stage, the
+  // element-wise product with H and the first DIT stage run as ONE register-resident step:
+  // both stages have radix R_1 and PP = 1 (no twiddles) and touch the same R_1 contiguous
+  // slots, so the spectrum of a butterfly never goes back to shared memory between them.
+  // H has the tile's layout (slot pos of sequence q at hbuf[q*SP + pos*ES]).
+  //   dif_head: DIF stages R_m..R_2;  filter_stage: DFT_R1, * H, IDFT_R1;  dit_tail: R_2..R_m.
+  template <int R1, int... Rest>
+  __device__ __forceinline__ static void dif_head(float2* buf, const float2* tw, Radices<R1, Rest...>) {
+    dif_impl<false, R1>(buf, tw + (R1 - 1) * (N / R1), Radices<Rest...>{});
+  }
+  template <int R1, int... Rest>
+  __device__ __forceinline__ static void dit_tail(float2* buf, const float2* tw, Radices<R1, Rest...>) {
+    dit_impl<true, R1>(buf, tw + (R1 - 1) * (N / R1), Radices<Rest...>{});
+  }
+  template <int R1, int... Rest>
+  __device__ __forceinline__ static void filter_stage(float2* buf, const float2* hbuf, Radices<R1, Rest...>) {
+    constexpr int R = R1, NB = N / R, NG = NSEQ * NB;
+#pragma unroll 1
+    for (int g = threadIdx.x; g < NG; g += NT) {
+      const int q = SEQ_FAST ? g % NSEQ : g / NB;
+      const int b = SEQ_FAST ? g / NSEQ : g - q * NB;
+      float2* sb = buf + q * SP + b * R * ES;
+      const float2* hb = hbuf + q * SP + b * R * ES;
+      float2 v[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = sb[i * ES];
+      dft<R, false>(v);
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], hb[i * ES]);
+      dft<R, true>(v);
+#pragma unroll
+      for (int i = 0; i < R; ++i) sb[i * ES] = v[i];
+    }
+    __syncthreads();
+  }
+
   // digit-reversed input -> natural output. Contains __syncthreads (whole CTA).
   template <bool INV, int... Rs>
   __device__ __forceinline__ static void dit(float2* buf, const float2* tw, Radices<Rs...> r) {

@@ -98,8 +98,8 @@ def epoch_fps(ch, rows, cols, t, epoch, seed, label, pool=3):
             "hbm_roofline_frac": fps * byts / HBM, "bytes_per_frame": byts}
 
 
-def c4(trust):
-    rows, cols, t, B = 2160, 3840, 15, 4
+def c4(trust, B=4):
+    rows, cols, t = 2160, 3840, 15
     pub, prv = make_pairs(B, 1, rows, cols, t, 7, shared_kernel=False)
     out = torch.empty_like(pub)
     slots = torch.zeros((B, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
@@ -111,7 +111,7 @@ def c4(trust):
     Mb, Nb = rows + t - 1, cols + t - 1
     fps = B / (ms / 1e3)
     return {"config": f"c4: 3840x2160 gray, t=15, per-frame recovery ({'trusted hint' if trust else 'estimated width'})",
-            "frames_per_s": fps, "ms_per_batch_of_4": ms, "hbm_roofline_frac": fps * (2 * Mb * Nb + rows * cols) * 4 / HBM}
+            "frames_per_s": fps, "batch": B, "ms_per_batch": ms, "hbm_roofline_frac": fps * (2 * Mb * Nb + rows * cols) * 4 / HBM}
 
 
 def c5():
