@@ -78,14 +78,18 @@ const float2* stage_twiddles(cbp_ctx* ctx, int n, bool column) {
 
 // slot(u) of the compile-time column plan's DIF output order (null: no plan, natural
 // order); the Wiener table is stored in that order so pass B filters element-wise
-const short* column_slots(cbp_ctx* ctx, int n) {
+// bmajor: slot b*R1 + i (butterfly b of the first DIT radix R1) is stored at i*(n/R1) + b
+const short* column_slots(cbp_ctx* ctx, int n, bool bmajor) {
   std::vector<int> rad;
   if (!ct_radices(n, true, rad)) return nullptr;
-  const int key = -(n + (1 << 24));  // distinct from the twiddle keys
+  const int key = -(n + (1 << 24) + (bmajor ? (1 << 25) : 0));  // distinct from the twiddle keys
   auto it = ctx->tw.find(key);
   if (it != ctx->tw.end()) return reinterpret_cast<const short*>(it->second);
   std::vector<short> h(static_cast<size_t>(n));
-  for (int u = 0; u < n; ++u) h[u] = short(ct_pos(rad, u));
+  for (int u = 0; u < n; ++u) {
+    const int sl = ct_pos(rad, u);
+    h[u] = short(bmajor ? (sl % rad[0]) * (n / rad[0]) + sl / rad[0] : sl);
+  }
   float2* d = nullptr;
   if (cudaMalloc(&d, h.size() * sizeof(short) + sizeof(float2)) != cudaSuccess) return nullptr;
   cudaMemcpy(d, h.data(), h.size() * sizeof(short), cudaMemcpyHostToDevice);
@@ -149,7 +153,9 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
     return set_error(ctx, CBP_UNSUPPORTED, "transform grid is not 2/3/5/7-smooth");
   a.xp = (a.Mb + 3) & ~3;  // XT column pitch
   a.hp = (a.Gr + 3) & ~3;
-  a.hpos = column_slots(ctx, a.Gr);
+  static const int variant = getenv("CBP_FFT_VARIANT") ? atoi(getenv("CBP_FFT_VARIANT")) : 0;
+  a.hpos = column_slots(ctx, a.Gr, true);  // compile-time column plans: butterfly-major filter
+  a.h_bmajor = a.hpos != nullptr;
   // rows per CTA for passes A/C: keep 2*rpc*L*8 bytes <= 64 KB, at most 8 rows
   int rpc = 8;
   while (rpc > 1 && size_t(2) * rpc * L * sizeof(float2) > 64 * 1024) rpc /= 2;
@@ -163,7 +169,6 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.twst_col = stage_twiddles(ctx, a.Gr, true);
   static const int dbg = getenv("CBP_DEBLUR_DBG") ? atoi(getenv("CBP_DEBLUR_DBG")) : 0;
   a.dbg = dbg;
-  static const int variant = getenv("CBP_FFT_VARIANT") ? atoi(getenv("CBP_FFT_VARIANT")) : 0;
   a.variant = variant;
   if (!a.tw_row || !a.tw_post || !a.tw_col)
     return set_error(ctx, CBP_CUDA_ERROR, "twiddle table allocation failed");

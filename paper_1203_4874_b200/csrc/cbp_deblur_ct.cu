@@ -241,50 +241,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a,
     const int next = tile + gridDim.x;
     if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
     cp_async_commit();
-    if (status == 0 && !P::HD && !a.dbg) {  // fused filter stage (see k_cols_filter_bulk)
+    if (status == 0) {  // uniform over the CTA; fused filter stage (see k_cols_filter_bulk)
       const int t = slot->width;
       FFT::dif_head(cur, a.twst_col, R{});
-      cp_async_wait<1>();
-      __syncthreads();  // filter strip (copied by all threads) visible
-      FFT::filter_stage(cur, Hs, R{});
+      if constexpr (P::HD) {
+        FFT::filter_stage_g(cur, a.H + size_t(f) * a.h_frame + size_t(v0) * a.hp, a.hp, min(W, a.Hc - v0), R{});
+      } else {
+        cp_async_wait<1>();
+        __syncthreads();  // filter strip (copied by all threads) visible
+        FFT::filter_stage(cur, Hs, R{});
+      }
       FFT::dit_tail(cur, a.twst_col, R{});
-      const int M = a.Mb - t + 1;
-      float2* XT = a.X + size_t(p) * a.x_plane;
-#pragma unroll
-      for (int s = 0; s < W; ++s) {
-        if (v0 + s >= a.Hc) break;
-        float2* col = XT + size_t(v0 + s) * a.xp;
-        const float4* src = reinterpret_cast<const float4*>(cur + s * GP);
-        for (int c = threadIdx.x; c < M / 2; c += NT) reinterpret_cast<float4*>(col)[c] = src[c];
-        if ((M & 1) && threadIdx.x == 0) col[M - 1] = cur[s * GP + M - 1];
-      }
-    } else if (status == 0) {  // uniform over the CTA
-      const int t = slot->width;
-      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
-      cp_async_wait<1>();
-      __syncthreads();
-      if (!(a.dbg & 2)) {
-        float4* c4 = reinterpret_cast<float4*>(cur);
-        auto mul = [](float4 x, float4 h) {
-          return make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
-                             x.z * h.w + x.w * h.z);
-        };
-        if constexpr (P::HD) {
-          const float2* Ht = a.H + size_t(f) * a.h_frame;
-          for (int i = threadIdx.x; i < W * (G / 2); i += NT) {
-            const int s = i / (G / 2), c = i - s * (G / 2);
-            if (v0 + s < a.Hc) {
-              const float4 h = __ldg(reinterpret_cast<const float4*>(Ht + size_t(v0 + s) * a.hp) + c);
-              c4[s * (GP / 2) + c] = mul(c4[s * (GP / 2) + c], h);
-            }
-          }
-        } else {
-          const float4* h4 = reinterpret_cast<const float4*>(Hs);
-          for (int i = threadIdx.x; i < TILE / 2; i += NT) c4[i] = mul(c4[i], h4[i]);
-        }
-      }
-      __syncthreads();
-      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_col, R{});
       const int M = a.Mb - t + 1;
       float2* XT = a.X + size_t(p) * a.x_plane;
 #pragma unroll
@@ -312,7 +279,9 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
   constexpr int HB = ((G + 1) / 2) * 2;  // filter run: G rounded up to an even count (16-byte multiple)
   using R = typename P::R;
   using FFT = FftIP<G, W, GP, 1, NT, false>;
-  static_assert(P::PIPE && !P::HD, "bulk pass B keeps two tile buffers and a staged filter strip");
+  static_assert(P::PIPE, "bulk pass B keeps two tile buffers");
+  // HD: the filter is read from L2 in the fused stage (butterfly-major table, hpos from
+  // column_slots(..., bmajor)); otherwise a filter strip is staged in shared memory
   extern __shared__ __align__(16) float2 sm[];
   float2* Hs = sm + 2 * TILE;
   __shared__ __align__(8) unsigned long long bar[3];  // tile buffers 0, 1; filter strip
@@ -359,7 +328,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     ph[cb] ^= 1u;
     __syncthreads();  // tile data and zero padding visible to all threads
     const int nc = min(W, a.Hc - v0);
-    if (status == 0 && threadIdx.x == 0) {  // filter strip in flight during the forward transform
+    if (!P::HD && status == 0 && threadIdx.x == 0) {  // filter strip in flight during the forward transform
       const float2* Ht = a.H + size_t(f) * a.h_frame;
       fence_proxy_async();
       mbar_expect_tx(&bar[2], unsigned(nc) * unsigned(HB) * 8u);
@@ -374,38 +343,18 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
         issue(next, nb, &bar[cb ^ 1]);
       }
     }
-    if (status == 0 && !a.dbg) {  // uniform over the CTA
+    if (status == 0) {  // uniform over the CTA
       // fused: DIF head, (last DIF stage, filter, first DIT stage) in registers, DIT tail
       const int t = slot->width;
       FFT::dif_head(cur, a.twst_col, R{});
-      mbar_wait(&bar[2], phh);  // every thread observes the filter strip's arrival
-      phh ^= 1u;
-      FFT::filter_stage(cur, Hs, R{});
+      if constexpr (P::HD) {
+        FFT::filter_stage_g(cur, a.H + size_t(f) * a.h_frame + size_t(v0) * a.hp, a.hp, nc, R{});
+      } else {
+        mbar_wait(&bar[2], phh);  // every thread observes the filter strip's arrival
+        phh ^= 1u;
+        FFT::filter_stage(cur, Hs, R{});
+      }
       FFT::dit_tail(cur, a.twst_col, R{});
-      const int M = a.Mb - t + 1;  // even: Mb even, t odd
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        float2* XT = a.X + size_t(p) * a.x_plane;
-        for (int s = 0; s < nc; ++s) bulk_s2g(XT + size_t(v0 + s) * a.xp, cur + s * GP, unsigned(M) * 8u);
-        bulk_commit();
-      }
-    } else if (status == 0) {  // profiling variants (a.dbg): separate filter pass
-      const int t = slot->width;
-      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_col, R{});
-      mbar_wait(&bar[2], phh);
-      phh ^= 1u;
-      __syncthreads();
-      if (!(a.dbg & 2)) {
-        float4* c4 = reinterpret_cast<float4*>(cur);
-        const float4* h4 = reinterpret_cast<const float4*>(Hs);
-        for (int i = threadIdx.x; i < TILE / 2; i += NT) {
-          const float4 x = c4[i], h = h4[i];
-          c4[i] = make_float4(x.x * h.x - x.y * h.y, x.x * h.y + x.y * h.x, x.z * h.z - x.w * h.w,
-                              x.z * h.w + x.w * h.z);
-        }
-      }
-      __syncthreads();
-      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_col, R{});
       const int M = a.Mb - t + 1;  // even: Mb even, t odd
       if (threadIdx.x == 0) {
         fence_proxy_async();
@@ -759,15 +708,16 @@ void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
     pB = resident_per_sm(k_cols_filter_ct<P>, P::NT, sm);
-    if constexpr (P::PIPE && !P::HD) {
+    if constexpr (P::PIPE) {
       cudaFuncSetAttribute(k_cols_filter_bulk<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
       pT = resident_per_sm(k_cols_filter_bulk<P>, P::NT, sm);
     }
   }
   const int total = planes * ((a.Hc + P::W - 1) / P::W);
-  if constexpr (P::PIPE && !P::HD) {
+  if constexpr (P::PIPE) {
     static const bool bulk = !getenv("CBP_NO_BULK");
-    if (bulk && a.Mb % 2 == 0) {  // column runs of Mb complex values are 16-byte multiples
+    // column runs of Mb complex values are 16-byte multiples; HD reads a butterfly-major H
+    if (bulk && a.Mb % 2 == 0 && (!P::HD || a.h_bmajor)) {
       k_cols_filter_bulk<P><<<persistent_grid(pT, sms, a.sm_reserve, total), P::NT, sm, s>>>(a, planes);
       return;
     }
@@ -783,9 +733,8 @@ using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
 using Row1944 = RowPlan<1944, 2, Radices<27, 8, 9>, 256>;  // 4K: Gc = 3888
 using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
 using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
-using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;  // 1080p: Gr = 1120
-using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 1>;
-using Col1120b = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;
+using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;  // 1080p: Gr = 1120, filter from L2
+using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;        // staged filter strip
 using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false, 4, true>;
 using Col2187 = ColPlan<2187, 2, Radices<27, 9, 9>, 256>;  // 4K: Gr = 2187
 using Col490 = ColPlan<490, 8, Radices<35, 14>, 288>;      // 640x480: Gr = 490
@@ -839,7 +788,6 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
     switch (a.Gr) {
       case 1120:
         if (a.variant == 1) launch_cols<Col1120a>(a, planes, s);
-        else if (a.variant == 2) launch_cols<Col1120b>(a, planes, s);
         else if (a.variant == 3) launch_cols<Col1120c>(a, planes, s);
         else launch_cols<Col1120>(a, planes, s);
         return true;

@@ -219,7 +219,8 @@ struct FftIP {
   // element-wise product with H and the first DIT stage run as ONE register-resident step:
   // both stages have radix R_1 and PP = 1 (no twiddles) and touch the same R_1 contiguous
   // slots, so the spectrum of a butterfly never goes back to shared memory between them.
-  // H has the tile's layout (slot pos of sequence q at hbuf[q*SP + pos*ES]).
+  // H is butterfly-major: element i of butterfly b of sequence q at hbuf[q*SP + i*NB + b]
+  // (conflict-free: a warp reads consecutive words).
   //   dif_head: DIF stages R_m..R_2;  filter_stage: DFT_R1, * H, IDFT_R1;  dit_tail: R_2..R_m.
   template <int R1, int... Rest>
   __device__ __forceinline__ static void dif_head(float2* buf, const float2* tw, Radices<R1, Rest...>) {
@@ -237,13 +238,39 @@ struct FftIP {
       const int q = SEQ_FAST ? g % NSEQ : g / NB;
       const int b = SEQ_FAST ? g / NSEQ : g - q * NB;
       float2* sb = buf + q * SP + b * R * ES;
-      const float2* hb = hbuf + q * SP + b * R * ES;
+      const float2* hb = hbuf + q * SP + b;
       float2 v[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) v[i] = sb[i * ES];
       dft<R, false>(v);
 #pragma unroll
-      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], hb[i * ES]);
+      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], hb[i * NB]);
+      dft<R, true>(v);
+#pragma unroll
+      for (int i = 0; i < R; ++i) sb[i * ES] = v[i];
+    }
+    __syncthreads();
+  }
+
+  // filter_stage with H read from global memory (L2) in butterfly-major order: element i of
+  // butterfly b of sequence q at hg[q*hsp + i*NB + b], so a warp's loads are contiguous.
+  // Sequences q >= nq (absent columns) reuse sequence nq-1's filter (never stored).
+  template <int R1, int... Rest>
+  __device__ __forceinline__ static void filter_stage_g(float2* buf, const float2* __restrict__ hg, size_t hsp,
+                                                        int nq, Radices<R1, Rest...>) {
+    constexpr int R = R1, NB = N / R, NG = NSEQ * NB;
+#pragma unroll 1
+    for (int g = threadIdx.x; g < NG; g += NT) {
+      const int q = SEQ_FAST ? g % NSEQ : g / NB;
+      const int b = SEQ_FAST ? g / NSEQ : g - q * NB;
+      float2* sb = buf + q * SP + b * R * ES;
+      const float2* hb = hg + size_t(min(q, nq - 1)) * hsp + b;
+      float2 v[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = sb[i * ES];
+      dft<R, false>(v);
+#pragma unroll
+      for (int i = 0; i < R; ++i) v[i] = cmul(v[i], __ldg(hb + i * NB));
       dft<R, true>(v);
 #pragma unroll
       for (int i = 0; i < R; ++i) sb[i * ES] = v[i];
