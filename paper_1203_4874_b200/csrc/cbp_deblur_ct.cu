@@ -134,21 +134,18 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     if constexpr (BULK) {
       const int cb = it & 1;
       if (next < total && threadIdx.x == 0) issue_bulk(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
+      // every thread observes the rows' arrival; the first DIF stage reads floats >= Nb
+      // (row tails, stale rows past the frame) as zeros, so no zeroing and no barrier
       mbar_wait(&bar[cb], ph[cb]);
       ph[cb] ^= 1u;
-      const int r0t = (tile - (tile / groups) * groups) * RPC;
-      float* cf = reinterpret_cast<float*>(cur);
-      for (int s = 0; s < RPC; ++s) {  // zero the tails (and the rows past the frame)
-        const int lo = r0t + s < a.Mb ? a.Nb : 0;
-        for (int x = lo + threadIdx.x; x < 2 * L; x += NT) cf[s * 2 * L + x] = 0.f;
-      }
+      if (!(a.dbg & 1)) FFT::template dif_masked<false>(cur, a.twst_row, a.Nb, R{});
     } else {
       if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
       cp_async_commit();
       cp_async_wait<1>();
+      __syncthreads();
+      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     }
-    __syncthreads();
-    if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     float2* XT = a.X + size_t(p) * a.x_plane + r0;
     const int nrows = min(RPC, a.Mb - r0);
@@ -450,14 +447,14 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
     if constexpr (TMA) {
       const int cb = it & 1;
       if (next < total && threadIdx.x == 0) issue_tma(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
-      mbar_wait(&bar[cb], ph[cb]);
+      mbar_wait(&bar[cb], ph[cb]);  // every thread observes the tile's arrival: no barrier
       ph[cb] ^= 1u;
     } else {
       if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
       cp_async_commit();
       cp_async_wait<1>();
+      __syncthreads();
     }
-    __syncthreads();
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     const int M = rows_of(p);
     const int nrows = min(RPC, M - r0);

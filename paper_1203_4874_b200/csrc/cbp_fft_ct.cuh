@@ -145,9 +145,13 @@ struct FftIP {
   // DIT = false: DIF stage (DFT, then twiddle); true: DIT stage (twiddle, then DFT).
   // twst: this stage's twiddles in butterfly order, twst[(i-1)*NB + b] = W_{PS}^{i*(b % PP)},
   // so a warp's twiddle loads are contiguous.
-  template <bool DIT, bool INV, int R, int PP>
-  __device__ __forceinline__ static void stage(float2* buf, const float2* __restrict__ twst) {
+  // MASK (first DIF stage only): input element n of a sequence holds floats 2n, 2n+1 of a
+  // real row of nf valid floats; floats >= nf are read as zero, so the tile's row tails
+  // (and any rows past the frame, whose outputs are discarded) need no zeroing.
+  template <bool DIT, bool INV, int R, int PP, bool MASK = false>
+  __device__ __forceinline__ static void stage(float2* buf, const float2* __restrict__ twst, int nf = 0) {
     constexpr int NB = N / R;
+    static_assert(!MASK || (!DIT && PP > 1), "masked loads: first DIF stage of a multi-stage plan");
     // Butterfly g of the CTA: sequence q, butterfly b. SEQ_FAST: consecutive threads take
     // consecutive sequences of one butterfly; otherwise butterflies are numbered flat over
     // (sequence, butterfly), so idle lanes gather in whole idle warps at the end.
@@ -175,7 +179,14 @@ struct FftIP {
         const int base = (b - k) * R + k;  // block * PS + k
         float2 v[R];
 #pragma unroll
-        for (int i = 0; i < R; ++i) v[i] = sb[(base + i * PP) * ES];
+        for (int i = 0; i < R; ++i) {
+          v[i] = sb[(base + i * PP) * ES];
+          if constexpr (MASK) {
+            const int n2 = 2 * (base + i * PP);
+            if (n2 >= nf) v[i] = make_float2(0.f, 0.f);
+            else if (n2 + 1 == nf) v[i].y = 0.f;
+          }
+        }
         if (DIT && PP > 1) {
 #pragma unroll
           for (int i = 1; i < R; ++i) {
@@ -276,6 +287,23 @@ struct FftIP {
       for (int i = 0; i < R; ++i) sb[i * ES] = v[i];
     }
     __syncthreads();
+  }
+
+  template <bool INV, int PP, int R, int... Rest>
+  __device__ __forceinline__ static void dif_impl_m(float2* buf, const float2* tw, int nf, Radices<R, Rest...>) {
+    if constexpr (sizeof...(Rest) == 0) {
+      stage<false, INV, R, PP, true>(buf, tw, nf);
+    } else {
+      dif_impl_m<INV, PP * R>(buf, tw + (R - 1) * (N / R), nf, Radices<Rest...>{});
+      stage<false, INV, R, PP>(buf, tw);
+    }
+  }
+  // dif() of real rows with nf valid floats per row (element n = floats 2n, 2n+1); the
+  // contents of the tile beyond them are ignored
+  template <bool INV, int... Rs>
+  __device__ __forceinline__ static void dif_masked(float2* buf, const float2* tw, int nf, Radices<Rs...>) {
+    static_assert(RadixProduct<Rs...>::value == N, "radix plan does not multiply to N");
+    dif_impl_m<INV, 1>(buf, tw, nf, Radices<Rs...>{});
   }
 
   // digit-reversed input -> natural output. Contains __syncthreads (whole CTA).
