@@ -30,8 +30,12 @@ struct RadixCount<Radices<Rs...>> {
 // otherwise one tile per CTA and latency is hidden by many resident CTAs.
 // MINB: resident CTAs per SM the register allocation must allow (__launch_bounds__).
 // HD (columns): read the filter straight from L2 in the multiply instead of staging it.
-template <int L_, int RPC_, class Rs, int NT_, bool PIPE_ = true, int MINB_ = 1>
+// RTW (rows): the split twiddles tw_post and the used stage twiddles are copied to shared
+// memory per CTA and the digit reversal pos(k) is computed (no pos table).
+template <int L_, int RPC_, class Rs, int NT_, bool PIPE_ = true, int MINB_ = 1, bool RTW_ = false>
 struct RowPlan {
+  static constexpr bool RTW = RTW_;
+  static constexpr int TWN = RTW_ ? L_ / 2 + 1 + TwUsed<L_, Rs>::count : 0;  // shared float2 entries
   static constexpr int L = L_;
   static constexpr int RPC = RPC_;
   static constexpr int NT = NT_;
@@ -49,6 +53,17 @@ struct ColPlan {
   static constexpr bool HD = HD_;
   using R = Rs;
 };
+
+// RTW: copy tw_post[0..L/2] and the used stage twiddles into tws; returns the stage table
+// base to hand to FftIP (offset so that the plan's own indices land in the copy).
+template <class P>
+__device__ __forceinline__ const float2* stage_row_twiddles(const DeblurArgs& a, float2* tws) {
+  constexpr int L = P::L, NP = L / 2 + 1;
+  using U = TwUsed<L, typename P::R>;
+  for (int i = threadIdx.x; i < NP; i += P::NT) tws[i] = __ldg(&a.tw_post[i]);
+  for (int i = threadIdx.x; i < U::count; i += P::NT) tws[NP + i] = __ldg(&a.twst_row[U::offset + i]);
+  return tws + NP - U::offset;
+}
 
 __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a, int p) {
   return a.slot + (a.slot_per_frame ? p / a.channels : 0);
@@ -70,11 +85,20 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
   constexpr int NT = P::NT;
   constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, L, 1, NT, false>;
+  using FFT = FftIP<L, RPC, L, 1, NT, false, P::RTW>;
   static_assert(!BULK || (P::PIPE && L % 2 == 0), "bulk rows need two buffers and 16-byte row starts");
   extern __shared__ __align__(16) float2 sm[];
   short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);
-  for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
+  float2* tws = sm + (P::PIPE ? 2 : 1) * TILE;  // RTW: [tw_post][stage twiddles]
+  const float2* twst = a.twst_row;
+  const float2* twp = a.tw_post;
+  if constexpr (P::RTW) {
+    twst = stage_row_twiddles<P>(a, tws);
+    twp = tws;
+  } else {
+    for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
+  }
+  auto posk = [&](int k) { return P::RTW ? Pos<R>::get(k) : int(pos[k]); };
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
   const bool v16 = a.in_vec4 && (L % 2 == 0);
@@ -87,8 +111,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
       mbar_init(&bar[1], 1);
       mbar_init_fence();
     }
-    __syncthreads();
   }
+  __syncthreads();  // pos table / staged twiddles, barriers
   auto issue_bulk = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     const float* src = a.in + size_t(p) * a.in_plane + size_t(r0) * a.in_ld;
@@ -138,13 +162,13 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
       // (row tails, stale rows past the frame) as zeros, so no zeroing and no barrier
       mbar_wait(&bar[cb], ph[cb]);
       ph[cb] ^= 1u;
-      if (!(a.dbg & 1)) FFT::template dif_masked<false>(cur, a.twst_row, a.Nb, R{});
+      if (!(a.dbg & 1)) FFT::template dif_masked<false>(cur, twst, a.Nb, R{});
     } else {
       if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
-      if (!(a.dbg & 1)) FFT::template dif<false>(cur, a.twst_row, R{});
+      if (!(a.dbg & 1)) FFT::template dif<false>(cur, twst, R{});
     }
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
     float2* XT = a.X + size_t(p) * a.x_plane + r0;
@@ -155,8 +179,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     for (int idx = threadIdx.x; idx < NPAIR * HALF; idx += NT) {
       const int k = idx / HALF, j = idx - k * HALF;
       if (2 * j >= nrows) continue;
-      const int pk = pos[k], pc = pos[k == 0 ? 0 : L - k];
-      const float2 w = __ldg(&a.tw_post[k]);
+      const int pk = posk(k), pc = posk(k == 0 ? 0 : L - k);
+      const float2 w = P::RTW ? twp[k] : __ldg(&twp[k]);
       float2 xk[2], xc[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -268,7 +292,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a,
 // Pass B with bulk copies (TMA engine): one thread moves each column strip in (a single
 // copy per column, completion on an mbarrier), the filter strip likewise, and the filtered
 // columns back out (bulk stores, drained before the buffer is refilled). Needs an even
-// Mb (16-byte multiple column runs); the rows Mb..G-1 of the tile are zeroed by threads.
+// Mb (16-byte multiple column runs); the first DIF stage reads rows Mb..G-1 as zeros.
 template <class P>
 __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
@@ -291,15 +315,6 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     mbar_init_fence();
   }
   __syncthreads();
-  // zero the padding rows (and absent columns) of buffer `b` for tile `tile`
-  auto pad = [&](int tile, float2* dst) {
-    const int p = tile / strips, v0 = (tile - p * strips) * W;
-    (void)p;
-    for (int s = 0; s < W; ++s) {
-      const int lo = v0 + s < a.Hc ? a.Mb : 0;
-      for (int u = lo + threadIdx.x; u < G; u += NT) dst[s * GP + u] = make_float2(0.f, 0.f);
-    }
-  };
   auto issue = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
     const int p = tile / strips, v0 = (tile - p * strips) * W;
     const float2* XT = a.X + size_t(p) * a.x_plane;
@@ -310,10 +325,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
   };
   unsigned ph[2] = {0u, 0u}, phh = 0u;
   int tile = blockIdx.x;
-  if (tile < total) {
-    pad(tile, sm);
-    if (threadIdx.x == 0) issue(tile, sm, &bar[0]);
-  }
+  if (tile < total && threadIdx.x == 0) issue(tile, sm, &bar[0]);
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
     const int cb = it & 1;
     float2* cur = sm + cb * TILE;
@@ -321,9 +333,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     const int f = a.slot_per_frame ? p / a.channels : 0;
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
-    mbar_wait(&bar[cb], ph[cb]);
+    mbar_wait(&bar[cb], ph[cb]);  // every thread observes the strip's arrival
     ph[cb] ^= 1u;
-    __syncthreads();  // tile data and zero padding visible to all threads
     const int nc = min(W, a.Hc - v0);
     if (!P::HD && status == 0 && threadIdx.x == 0) {  // filter strip in flight during the forward transform
       const float2* Ht = a.H + size_t(f) * a.h_frame;
@@ -334,7 +345,6 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     const int next = tile + gridDim.x;
     if (next < total) {  // prefetch into the other buffer (its last bulk stores drained first)
       float2* nb = sm + (cb ^ 1) * TILE;
-      pad(next, nb);
       if (threadIdx.x == 0) {
         bulk_wait_read();
         issue(next, nb, &bar[cb ^ 1]);
@@ -343,7 +353,9 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     if (status == 0) {  // uniform over the CTA
       // fused: DIF head, (last DIF stage, filter, first DIT stage) in registers, DIT tail
       const int t = slot->width;
-      FFT::dif_head(cur, a.twst_col, R{});
+      // rows Mb..G-1 read as zeros by the first stage; absent columns (v >= Hc) hold stale
+      // data whose results are never stored
+      FFT::dif_head_masked(cur, a.twst_col, 2 * a.Mb, R{});
       if constexpr (P::HD) {
         FFT::filter_stage_g(cur, a.H + size_t(f) * a.h_frame + size_t(v0) * a.hp, a.hp, nc, R{});
       } else {
@@ -377,12 +389,23 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
   constexpr int L = P::L, RPC = P::RPC, H = L + 1, TILE = ((H * RPC + 15) & ~15);  // 128-byte buffers
   static_assert(RPC % 2 == 0, "16-byte copies carry two rows");
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, 1, RPC, NT, true>;
+  using FFT = FftIP<L, RPC, 1, RPC, NT, true, P::RTW>;
   extern __shared__ __align__(128) float2 sm_c[];  // TMA tile destinations: 128-byte aligned
   float2* const sm = sm_c;
-  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);  // DIT input slot of z[n]
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + (P::PIPE ? 2 : 1) * TILE + (L + 3) / 4);
-  for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
+  // after the tiles: RTW ? [tw_post][stage twiddles] : pos table (DIT input slot of z[n]); then barriers
+  constexpr int AUX = P::RTW ? P::TWN : (L + 3) / 4;
+  short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);
+  float2* tws = sm + (P::PIPE ? 2 : 1) * TILE;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sm + (P::PIPE ? 2 : 1) * TILE + AUX);
+  const float2* twst = a.twst_row;
+  const float2* twp = a.tw_post;
+  if constexpr (P::RTW) {
+    twst = stage_row_twiddles<P>(a, tws);
+    twp = tws;
+  } else {
+    for (int i = threadIdx.x; i < L; i += NT) pos[i] = short(Pos<R>::get(i));
+  }
+  auto posk = [&](int k) { return P::RTW ? Pos<R>::get(k) : int(pos[k]); };
   __syncthreads();
   const int groups = (a.Mb + RPC - 1) / RPC;
   const int total = planes * groups;
@@ -399,7 +422,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
       const int k = idx / HALF, j = idx - k * HALF;
       const int rows_left = M - r0 - 2 * j;
       const int bytes = rows_left >= 2 ? 16 : (rows_left == 1 ? 8 : 0);
-      const int slot = k < L ? pos[k] : L;
+      const int slot = k < L ? posk(k) : L;
       cp_async16(dst + slot * RPC + 2 * j, bytes ? XT + size_t(k) * a.xp + 2 * j : a.X, bytes);
     }
   };
@@ -465,10 +488,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
 #pragma unroll 1
       for (int idx = threadIdx.x; idx < NP * HALF; idx += NT) {
         const int k = idx / HALF, j = idx - k * HALF;
-        float4* pa = reinterpret_cast<float4*>(cur + pos[k] * RPC + 2 * j);
-        float4* pb = reinterpret_cast<float4*>(cur + (k == 0 ? L : pos[L - k]) * RPC + 2 * j);
+        float4* pa = reinterpret_cast<float4*>(cur + posk(k) * RPC + 2 * j);
+        float4* pb = reinterpret_cast<float4*>(cur + (k == 0 ? L : posk(L - k)) * RPC + 2 * j);
         const float4 A4 = *pa, B4 = *pb;
-        const float2 w = cconj(__ldg(&a.tw_post[k]));
+        const float2 w = cconj(P::RTW ? twp[k] : __ldg(&twp[k]));
         const float2 wm = make_float2(-w.x, w.y);  // conj(tw_post[L-k]) = -tw_post[k]
         float2 r1[2], r2[2];
 #pragma unroll
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
         if (k != 0 && 2 * k != L) *pb = make_float4(r2[0].x, r2[0].y, r2[1].x, r2[1].y);
       }
       __syncthreads();
-      if (!(a.dbg & 1)) FFT::template dit<true>(cur, a.twst_row, R{});  // slot -> natural order
+      if (!(a.dbg & 1)) FFT::template dit<true>(cur, twst, R{});  // slot -> natural order
       const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
       float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
       if (a.out_vec2 && N % 2 == 0) {
@@ -650,9 +673,10 @@ bool rows_inverse_tmap(const DeblurArgs& a, int planes, CUtensorMap* map) {
 template <class P>
 void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
   constexpr int NB = P::PIPE ? 2 : 1;
-  const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) + P::L * sizeof(short);
+  const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) +
+                     (P::RTW ? size_t(P::TWN) * sizeof(float2) : P::L * sizeof(short));
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 15) & ~15) * sizeof(float2) +
-                     size_t((P::L + 3) / 4) * sizeof(float2) + 2 * sizeof(unsigned long long);
+                     size_t(P::RTW ? P::TWN : (P::L + 3) / 4) * sizeof(float2) + 2 * sizeof(unsigned long long);
   static int pA = 0, pC = 0, pAb = 0, pCt = 0, sms = 0;
   constexpr bool kBulk = P::PIPE && P::L % 2 == 0;
   if (!sms) {
@@ -724,7 +748,10 @@ void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
 
 // Radix plans in DIT order; the first (contiguous-butterfly) radix is odd so its strided
 // shared-memory accesses are bank-conflict free. Large radices run in registers.
-using Row972 = RowPlan<972, 4, Radices<27, 36>, 160, true, 3>;  // 1080p: Gc = 1944
+#ifndef CBP_RTW972
+#define CBP_RTW972 1
+#endif
+using Row972 = RowPlan<972, 4, Radices<27, 36>, 160, true, 3, CBP_RTW972>;  // 1080p: Gc = 1944
 using Row972a = RowPlan<972, 4, Radices<27, 36>, 160, true, 1>;
 using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
 using Row1944 = RowPlan<1944, 2, Radices<27, 8, 9>, 256>;  // 4K: Gc = 3888
@@ -734,7 +761,7 @@ using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;  // 1080p
 using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;        // staged filter strip
 using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false, 4, true>;
 using Col2187 = ColPlan<2187, 2, Radices<27, 9, 9>, 256>;  // 4K: Gr = 2187
-using Col490 = ColPlan<490, 8, Radices<35, 14>, 288>;      // 640x480: Gr = 490
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 288, true, 2>;      // 640x480: Gr = 490
 using Col270 = ColPlan<270, 8, Radices<27, 10>, 224>;      // 256x256: Gr = 270
 
 // Radix plans of the specialisations above (host mirror; DIT stage order).

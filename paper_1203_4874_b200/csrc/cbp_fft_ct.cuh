@@ -138,8 +138,34 @@ using InvPos = Pos<typename Reverse<Radices<>, Rs>::type>;
 
 // NSEQ sequences of length N; element position p of sequence q at buf[q*SP + p*ES].
 // SEQ_FAST: consecutive threads walk sequences first (column strips).
-template <int N, int NSEQ, int SP, int ES, int NT, bool SEQ_FAST>
+// Twiddle table layout of a plan (stage_twiddles() on the host, DIT stage order): stage s
+// holds (R_s - 1) * N / R_s entries; stage 1 (PP = 1) has no twiddles, so the used part of
+// the table starts at TwUsed::offset and has TwUsed::count entries.
+template <int N, class Rs>
+struct TwTotal;
+template <int N>
+struct TwTotal<N, Radices<>> {
+  static constexpr int value = 0;
+};
+template <int N, int R, int... Rest>
+struct TwTotal<N, Radices<R, Rest...>> {
+  static constexpr int value = (R - 1) * (N / R) + TwTotal<N, Radices<Rest...>>::value;
+};
+template <int N, class Rs>
+struct TwUsed;
+template <int N, int R1, int... Rest>
+struct TwUsed<N, Radices<R1, Rest...>> {
+  static constexpr int offset = (R1 - 1) * (N / R1);
+  static constexpr int count = TwTotal<N, Radices<R1, Rest...>>::value - offset;
+};
+
+// TWS: the stage twiddle table lives in shared memory (plain loads instead of __ldg).
+template <int N, int NSEQ, int SP, int ES, int NT, bool SEQ_FAST, bool TWS = false>
 struct FftIP {
+  __device__ __forceinline__ static float2 ldtw(const float2* p) {
+    if constexpr (TWS) return *p;
+    else return __ldg(p);
+  }
   static_assert(!SEQ_FAST || NT % NSEQ == 0, "threads must split evenly over sequences");
 
   // DIT = false: DIF stage (DFT, then twiddle); true: DIT stage (twiddle, then DFT).
@@ -190,7 +216,7 @@ struct FftIP {
         if (DIT && PP > 1) {
 #pragma unroll
           for (int i = 1; i < R; ++i) {
-            float2 w = __ldg(&twst[(i - 1) * NB + b]);
+            float2 w = ldtw(&twst[(i - 1) * NB + b]);
             if (INV) w.y = -w.y;
             v[i] = cmul(v[i], w);
           }
@@ -199,7 +225,7 @@ struct FftIP {
         if (!DIT && PP > 1) {
 #pragma unroll
           for (int i = 1; i < R; ++i) {
-            float2 w = __ldg(&twst[(i - 1) * NB + b]);
+            float2 w = ldtw(&twst[(i - 1) * NB + b]);
             if (INV) w.y = -w.y;
             v[i] = cmul(v[i], w);
           }
@@ -236,6 +262,12 @@ struct FftIP {
   template <int R1, int... Rest>
   __device__ __forceinline__ static void dif_head(float2* buf, const float2* tw, Radices<R1, Rest...>) {
     dif_impl<false, R1>(buf, tw + (R1 - 1) * (N / R1), Radices<Rest...>{});
+  }
+  // dif_head whose first stage reads elements n >= nf/2 (rows past the column) as zeros
+  template <int R1, int... Rest>
+  __device__ __forceinline__ static void dif_head_masked(float2* buf, const float2* tw, int nf, Radices<R1, Rest...>) {
+    static_assert(sizeof...(Rest) > 0, "masked head needs a second radix");
+    dif_impl_m<false, R1>(buf, tw + (R1 - 1) * (N / R1), nf, Radices<Rest...>{});
   }
   template <int R1, int... Rest>
   __device__ __forceinline__ static void dit_tail(float2* buf, const float2* tw, Radices<R1, Rest...>) {
