@@ -1158,7 +1158,13 @@ cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const 
 // 8 rows (64 threads) for kernels wider than 40 taps, whose halo would not fit otherwise.
 constexpr int VT_C = 64;
 // outputs per thread (a column strip) and output rows per CTA (4 row groups of 64 threads)
-__host__ __device__ inline int conv_out(int) { return 8; }
+#ifndef CBP_CONV_OUT
+#define CBP_CONV_OUT 8
+#endif
+// Rows per thread for t <= 32 (CBP_CONV_OUT): 16 rows halve the shared-memory wavefronts per
+// DFMA but measured no faster on B200 (1080p RGB 142 us either way: the tile load phase is
+// long-scoreboard bound at 2-3 CTAs/SM), so 8 rows (3 CTAs/SM, fewer spills) is the default.
+__host__ __device__ inline int conv_out(int t) { return t <= 32 ? CBP_CONV_OUT : 8; }
 __host__ __device__ inline int conv_rows(int t) { return t > 40 ? 8 : 4 * conv_out(t); }
 __host__ __device__ inline int conv_pad(int t) { return (t + 3) & ~3; }
 int validate_tiles(int rows, int cols, int t) {
@@ -1241,22 +1247,22 @@ __device__ __forceinline__ void conv_colT(const double* tile, int tw, const doub
 template <int OUT>
 __device__ __forceinline__ void conv_dispatch(const double* tile, int tw, const double* kt, int t, int tp, int li0,
                                               int lj, double* acc) {
-  {
-    switch (tp) {
-      case 4: return conv_colT<8, 4>(tile, tw, kt, t, li0, lj, acc);
-      case 8: return conv_colT<8, 8>(tile, tw, kt, t, li0, lj, acc);
-      case 12: return conv_colT<8, 12>(tile, tw, kt, t, li0, lj, acc);
-      case 16: return conv_colT<8, 16>(tile, tw, kt, t, li0, lj, acc);
-      case 20: return conv_colT<8, 20>(tile, tw, kt, t, li0, lj, acc);
-      case 24: return conv_colT<8, 24>(tile, tw, kt, t, li0, lj, acc);
-      case 28: return conv_colT<8, 28>(tile, tw, kt, t, li0, lj, acc);
-      case 32: return conv_colT<8, 32>(tile, tw, kt, t, li0, lj, acc);
-      default: return conv_col8(tile, tw, kt, t, tp, li0, lj, acc);  // t > 32
-    }
+  if constexpr (OUT == 8) {
+    if (tp > 32) return conv_col8(tile, tw, kt, t, tp, li0, lj, acc);  // t > 32
+  }
+  switch (tp) {
+    case 4: return conv_colT<OUT, 4>(tile, tw, kt, t, li0, lj, acc);
+    case 8: return conv_colT<OUT, 8>(tile, tw, kt, t, li0, lj, acc);
+    case 12: return conv_colT<OUT, 12>(tile, tw, kt, t, li0, lj, acc);
+    case 16: return conv_colT<OUT, 16>(tile, tw, kt, t, li0, lj, acc);
+    case 20: return conv_colT<OUT, 20>(tile, tw, kt, t, li0, lj, acc);
+    case 24: return conv_colT<OUT, 24>(tile, tw, kt, t, li0, lj, acc);
+    case 28: return conv_colT<OUT, 28>(tile, tw, kt, t, li0, lj, acc);
+    default: return conv_colT<OUT, 32>(tile, tw, kt, t, li0, lj, acc);
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
+__global__ void __launch_bounds__(256, CBP_CONV_OUT == 16 ? 2 : 3) k_conv_resid(ConvResidArgs a) {
   extern __shared__ double shd[];
   const int plane = blockIdx.y;
   const int frame = plane / a.channels;
@@ -1347,7 +1353,10 @@ __global__ void __launch_bounds__(256, 3) k_conv_resid(ConvResidArgs a) {
       }
     }
   };
-  accumulate(std::integral_constant<int, 8>{});
+  if (CBP_CONV_OUT == 16 && t <= 32)
+    accumulate(std::integral_constant<int, CBP_CONV_OUT>{});
+  else
+    accumulate(std::integral_constant<int, 8>{});
   num = warp_sum(num);
   den = warp_sum(den);
   __shared__ double rn[8], rd[8];
