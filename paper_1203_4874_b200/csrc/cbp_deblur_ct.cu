@@ -754,7 +754,13 @@ void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
 using Row972 = RowPlan<972, 4, Radices<27, 36>, 160, true, 3, CBP_RTW972>;  // 1080p: Gc = 1944
 using Row972a = RowPlan<972, 4, Radices<27, 36>, 160, true, 1>;
 using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
-using Row1944 = RowPlan<1944, 2, Radices<27, 8, 9>, 256>;  // 4K: Gc = 3888
+#ifndef CBP_ROW1944_RPC
+#define CBP_ROW1944_RPC 4
+#endif
+// 4K: Gc = 3888. Four rows per tile (one CTA of 512 threads per SM): a tile then writes whole
+// 32-byte XT sectors (4 rows of one frequency); with two rows per tile every pass-A store was
+// a half sector (pass A 41.4 -> 26.8 us per 4K plane)
+using Row1944 = RowPlan<1944, CBP_ROW1944_RPC, Radices<27, 8, 9>, CBP_ROW1944_RPC == 4 ? 512 : 256>;
 using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
 using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
 using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;  // 1080p: Gr = 1120, filter from L2
