@@ -29,22 +29,6 @@ struct RadixProduct<R, Rs...> {
   static constexpr int value = R * RadixProduct<Rs...>::value;
 };
 
-// ---------------------------------------------------------------- cp.async
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-// 16-byte copy that bypasses L1 (.cg); src_bytes < 16 zero-fills the tail
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 // ------------------------------------------------- bulk copies (TMA, no tensor map)
 // One elected thread moves a whole contiguous run (size a multiple of 16 bytes, 16-byte
 // aligned ends) between global and shared memory; loads complete on an mbarrier.

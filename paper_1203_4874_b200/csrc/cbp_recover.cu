@@ -56,9 +56,10 @@ __device__ __forceinline__ int fold_width(const RecoverArgs& a, int b, int t_fix
 // (r, g) loads the FT_J rows r0 + r + t (FT_J g + j), so
 //  - Z1: thread = column; the rows of one step share the residue r, so the partial
 //    fold[r][n] over the block is one register (ascending rows), written per residue;
-//  - Z2: the step's luma tile goes to shared memory and warp j folds row j over the strip
-//    by column residue (lanes = residue x contiguous column part, parts combined in order).
-// The next step's samples are fetched before the current one is folded. Partials are
+//  - Z2: the step's luma tile goes to shared memory; for t <= 32 thread (j, r) folds row j
+//    over the strip's columns of residue r (two interleaved accumulators; t > 32: warp j
+//    loops the residues of row j).
+// Partials are
 // reduced in a fixed order by k_fold_z1_dft / k_fold_z2_dft (deterministic sums).
 // Also flags negative luma (decoder.cpp:52) and non-finite samples (image.cpp:33).
 // The block height adapts to the problem (a.fold_rh, set by plan_recover for ~1200 CTAs):
@@ -70,9 +71,25 @@ __host__ __device__ __forceinline__ int fold_groups(int t, int rh) {
 }
 __host__ __device__ __forceinline__ int fold_rows(int t, int rh) { return t * FT_J * fold_groups(t, rh); }
 
+// Raw samples arrive through a ring of FOLD_NS(C) shared-memory stages filled by cp.async
+// (16-byte copies when rows are 16-byte aligned), FOLD_NS - 1 steps ahead: one step is only
+// FT_J rows x FT_W columns, so a single-step register prefetch left ~25 KB in flight per SM
+// and the fold ran at ~1.2 TB/s, latency-bound.
+template <int C>
+struct FoldNS {
+  static constexpr int value = C == 1 ? 8 : 3;  // C = 3: 72 KB of stages + 32 KB luma tiles
+};
+template <int C>
+constexpr size_t fold_smem() {
+  return size_t(FoldNS<C>::value) * C * FT_J * FT_W * sizeof(float) + (C == 1 ? 0 : 2 * FT_J * FT_W * sizeof(double));
+}
+
 template <int C>
 __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
-  __shared__ double tile[2][FT_J][FT_W];
+  constexpr int NS = FoldNS<C>::value;
+  extern __shared__ __align__(16) float fsm[];
+  float* raw = fsm;                                                        // [NS][C][FT_J][FT_W]
+  double* tile = reinterpret_cast<double*>(fsm + NS * C * FT_J * FT_W);  // C = 3: [2][FT_J][FT_W] luma
   const int b = blockIdx.z >> 1, q = blockIdx.z & 1;
   cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0) return;
@@ -85,79 +102,115 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
   const int c0 = blockIdx.x * FT_W, n = c0 + threadIdx.x;
   const bool col_ok = n < a.cols;
   const size_t plane = size_t(a.rows) * a.ld;
-  const float* base = (q ? a.prv : a.pub) + size_t(b) * C * plane + (col_ok ? n : 0);
+  const float* fbase = (q ? a.prv : a.pub) + size_t(b) * C * plane;
   double* p1 = a.part + (size_t(b) * 2 + q) * a.part_stride + size_t(blockIdx.y) * t * a.cols + n;
   double* p2 = a.part2 + ((size_t(b) * 2 + q) * a.ncb + blockIdx.x) * size_t(a.t_max) * a.rows;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // Z2 lanes: residue rz, contiguous column part hz of H (t > 32: lanes loop residues)
-  const int H = t <= 32 ? 32 / t : 1;
-  const int rz = lane % t, hz = lane / t;
-  const int lo = hz < H ? hz * FT_W / H : 0, hi = hz < H ? (hz + 1) * FT_W / H : 0;
-  float cur[FT_J][C], nxt[FT_J][C];
-  auto fetch = [&](int r, int g, float (&x)[FT_J][C]) {
+  const int warp = threadIdx.x >> 5;
+  // Z2 (t <= 32): pair (jz, rz) sums row jz of the step over the strip's columns of residue
+  // rz (first one cz). t <= 16: two adjacent lanes per pair (hz = 0: occurrences 0, 2, ..,
+  // hz = 1: 1, 3, ..) combined by one shuffle, so 8t <= 128 pairs keep all 256 threads busy;
+  // t > 16: one thread per pair, two interleaved accumulators.
+  const bool split = t <= 16;
+  const int pz = split ? threadIdx.x >> 1 : threadIdx.x, hz = split ? threadIdx.x & 1 : 0;
+  const int jz = pz / t, rz = pz - jz * t;
+  const int cz = ((rz - c0 % t) % t + t) % t;
+  const bool v16 = (a.ld % 4 == 0) && (reinterpret_cast<uintptr_t>(fbase) % 16 == 0);
+  const int steps = t * G;
+  // step it = (r, g): rows r0 + r + t (FT_J g + j), j < FT_J
+  auto issue = [&](int it) {
+    if (it < steps) {
+      const int r = it / G, g = it - r * G;
+      float* st = raw + (it % NS) * (C * FT_J * FT_W);
+      if (v16) {  // 64 threads per row: 4 rows per pass
 #pragma unroll
-    for (int j = 0; j < FT_J; ++j) {
-      const int m = r0 + r + t * (FT_J * g + j);
-      const bool ok = col_ok && m < r1;
+        for (int u = 0; u < C * FT_J / 4; ++u) {
+          const int row = u * 4 + (threadIdx.x >> 6), cc = row / FT_J, j = row - cc * FT_J;
+          const int col = (threadIdx.x & 63) * 4;
+          const int m = r0 + r + t * (FT_J * g + j);
+          const int bytes = m < r1 ? min(max((a.cols - c0 - col) * 4, 0), 16) : 0;
+          const float* src = bytes ? fbase + cc * plane + size_t(m) * a.ld + c0 + col : a.pub;
+          cp_async16(st + (cc * FT_J + j) * FT_W + col, src, bytes);
+        }
+      } else {
 #pragma unroll
-      for (int c = 0; c < C; ++c) x[j][c] = ok ? __ldg(base + size_t(m) * a.ld + c * plane) : 0.f;
+        for (int row = 0; row < C * FT_J; ++row) {
+          const int cc = row / FT_J, j = row - cc * FT_J;
+          const int m = r0 + r + t * (FT_J * g + j);
+          const bool ok = col_ok && m < r1;
+          const float* src = ok ? fbase + cc * plane + size_t(m) * a.ld + n : a.pub;
+          cp_async4(st + (cc * FT_J + j) * FT_W + threadIdx.x, src, ok ? 4 : 0);
+        }
+      }
     }
+    cp_async_commit();  // possibly empty: keeps the group count uniform
   };
+  for (int i = 0; i < NS - 1; ++i) issue(i);
   bool neg = false, bad = false;
   double acc = 0.0;
-  int r = 0, g = 0;
-  fetch(0, 0, cur);
-  const int steps = t * G;
   for (int it = 0; it < steps; ++it) {
-    int rn = r, gn = g + 1;
-    if (gn == G) gn = 0, rn = r + 1;
-    if (rn < t) fetch(rn, gn, nxt);
-    double* tl = &tile[it & 1][0][0];
+    const int r = it / G, g = it - r * G;
+    cp_async_wait<NS - 2>();
+    __syncthreads();  // step it's samples visible; every thread is done with step it - 1
+    issue(it + NS - 1);  // into the stage step it - 1 used
+    const float* st = raw + (it % NS) * (C * FT_J * FT_W);
+    double* tl = tile + (it & 1) * (FT_J * FT_W);
 #pragma unroll
     for (int j = 0; j < FT_J; ++j) {
       double v;
       if constexpr (C == 1) {
-        v = double(cur[j][0]);
+        v = double(st[j * FT_W + threadIdx.x]);
       } else {  // unfused, as luma_at (bit-identical to the CPU restatement)
-        v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, double(cur[j][0])), __dmul_rn(0.587, double(cur[j][1]))),
-                      __dmul_rn(0.114, double(cur[j][2])));
+        v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, double(st[j * FT_W + threadIdx.x])),
+                                __dmul_rn(0.587, double(st[(FT_J + j) * FT_W + threadIdx.x]))),
+                      __dmul_rn(0.114, double(st[(2 * FT_J + j) * FT_W + threadIdx.x])));
+        tl[j * FT_W + threadIdx.x] = v;
       }
       neg |= v < 0.0;
       bad |= !isfinite(v);
       acc += v;
-      tl[j * FT_W + threadIdx.x] = v;
     }
-    if (gn == 0) {  // residue r done
+    if (g == G - 1) {  // residue r done
       if (col_ok) p1[size_t(r) * a.cols] = acc;
       acc = 0.0;
     }
-    __syncthreads();
-    const int m = r0 + r + t * (FT_J * g + warp);
-    if (m < r1) {  // warp-uniform
-      if (t <= 32) {
-        double sz = 0.0;
-        // first column of part hz with absolute residue rz
-        for (int c = lo + ((rz - (c0 + lo) % t) % t + t) % t; c < hi; c += t) sz += tl[warp * FT_W + c];
-        for (int hh = 1; hh < H; ++hh) {
-          const double o = __shfl_sync(0xffffffffu, sz, min(lane + t * hh, 31));
-          if (hz == 0) sz += o;
+    if constexpr (C != 1) __syncthreads();  // luma tile visible
+    auto val = [&](int j, int c) -> double {
+      if constexpr (C == 1) return double(st[j * FT_W + c]);
+      else return tl[j * FT_W + c];
+    };
+    if (split) {  // uniform: t is per frame
+      const int m = r0 + r + t * (FT_J * g + jz);
+      double sz = 0.0;
+      if (jz < FT_J) {
+#pragma unroll 4
+        for (int c = cz + hz * t; c < FT_W; c += 2 * t) sz += val(jz, c);
+      }
+      const double o = __shfl_xor_sync(0xffffffffu, sz, 1);
+      if (jz < FT_J && m < r1 && hz == 0) p2[size_t(rz) * a.rows + m] = sz + o;
+    } else if (t <= 32) {
+      const int m = r0 + r + t * (FT_J * g + jz);
+      if (jz < FT_J && m < r1) {
+        double s0 = 0.0, s1 = 0.0;
+        int c = cz;
+        for (; c + t < FT_W; c += 2 * t) {
+          s0 += val(jz, c);
+          s1 += val(jz, c + t);
         }
-        if (hz == 0) p2[size_t(rz) * a.rows + m] = sz;
-      } else {
-        for (int rr = lane; rr < t; rr += 32) {
+        if (c < FT_W) s0 += val(jz, c);
+        p2[size_t(rz) * a.rows + m] = s0 + s1;
+      }
+    } else {
+      const int m = r0 + r + t * (FT_J * g + warp);
+      if (m < r1) {  // warp-uniform
+        for (int rr = (threadIdx.x & 31); rr < t; rr += 32) {
           double sz = 0.0;
-          for (int c = ((rr - c0 % t) % t + t) % t; c < FT_W; c += t) sz += tl[warp * FT_W + c];
+          for (int c = ((rr - c0 % t) % t + t) % t; c < FT_W; c += t) sz += val(warp, c);
           p2[size_t(rr) * a.rows + m] = sz;
         }
       }
     }
-#pragma unroll
-    for (int j = 0; j < FT_J; ++j)
-#pragma unroll
-      for (int c = 0; c < C; ++c) cur[j][c] = nxt[j][c];
-    r = rn;
-    g = gn;
   }
+  cp_async_wait<0>();
   neg = __syncthreads_or(neg);
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
@@ -227,8 +280,14 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
   // row blocks: grid.y covers the shortest blocks (t = 1); taller ones exit at once
   const int tmin = t_fixed > 0 ? t_fixed : 1;
   dim3 g1(a.ncb, (a.rows + fold_rows(tmin, a.fold_rh) - 1) / fold_rows(tmin, a.fold_rh), a.batch * 2);
-  if (a.channels == 1) k_fold_tile<1><<<g1, 256, 0, s>>>(a, t_fixed);
-  else k_fold_tile<3><<<g1, 256, 0, s>>>(a, t_fixed);
+  static bool cfg_tile = false;
+  if (!cfg_tile) {
+    cudaFuncSetAttribute(k_fold_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<1>()));
+    cudaFuncSetAttribute(k_fold_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<3>()));
+    cfg_tile = true;
+  }
+  if (a.channels == 1) k_fold_tile<1><<<g1, 256, fold_smem<1>(), s>>>(a, t_fixed);
+  else k_fold_tile<3><<<g1, 256, fold_smem<3>(), s>>>(a, t_fixed);
   const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
   dim3 g2((a.cols + 127) / 128 + (a.rows + 127) / 128, a.batch * 2);
   k_fold_dft<<<g2, 128, smf, s>>>(a, t_fixed);
