@@ -296,6 +296,35 @@ def run_b200(args, world, rank, local):
     def step(s):
         run_steps(1, s)
 
+    def count_launches():
+        return api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec)
+
+    def run_steady(n, start=0):
+        """n steps of the running pipeline: the recoveries of epochs start..start+REC_STREAMS-1
+        are issued and finished BEFORE the timed region (pipeline pre-roll, untimed); inside it
+        every step issues one recovery (REC_STREAMS epochs ahead) and one deconvolution batch,
+        so the region holds exactly n recoveries + n x 29 deblurs, in steady state (no fill
+        stall while the first recovery runs alone). Returns (ev0, ev1) around the region."""
+        for s in range(start, start + REC_STREAMS):
+            issue_decode(s)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        l0 = count_launches()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for st in s_rec:
+            st.wait_event(e0)
+        for s in range(start, start + n):
+            issue_decode(s + REC_STREAMS)
+            issue_deblur(s)
+        for st in s_rec:
+            done = torch.cuda.Event()
+            done.record(st)
+            s_deb.wait_event(done)
+        e1.record(stream)
+        return e0, e1, count_launches() - l0
+
     # ---- correctness guard on the pool (every epoch recovers its own kernel)
     for s in range(E):
         step(s)
@@ -320,18 +349,10 @@ def run_b200(args, world, rank, local):
         s += 1
         if s % 8 == 0:
             torch.cuda.synchronize(dev)
-    launches0 = api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec)
-    barrier(world)
     torch.cuda.synchronize(dev)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for st in s_rec:
-        st.wait_event(ev0)
-    run_steps(args.steps)
-    ev1.record(stream)
+    ev0, ev1, launches = run_steady(args.steps)
     torch.cuda.synchronize(dev)
     barrier(world)
-    launches = api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec) - launches0
     ms_rank = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
     ms = max_over_ranks(ms_rank, world)
@@ -424,7 +445,9 @@ def run_b200(args, world, rank, local):
                            "frames_per_step": EPOCH, "pool_epochs": E,
                            "schedule": f"recoveries of epochs s+1..s+{REC_STREAMS} overlapped with deconvolution of epoch s "
                                        f"({REC_STREAMS} high-priority recovery streams + 1 deconvolution stream; "
-                                       f"deconvolution leaves {SM_RESERVE} SMs)",
+                                       f"deconvolution leaves {SM_RESERVE} SMs); steady state: the recoveries of "
+                                       f"the first {REC_STREAMS} epochs run before the timed region, each timed step "
+                                       f"issues 1 recovery ({REC_STREAMS} epochs ahead) + 29 deblurs",
                            "l2": "inputs larger than L2 (each step reads 0.76 GB of distinct frames)",
                            "decode_cfg": "search 9..25, tau 1e-6, default epsilon, validate=true",
                            "parallelism": f"{world} independent GPU(s), no data-path collective"},

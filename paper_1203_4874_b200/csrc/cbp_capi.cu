@@ -154,6 +154,8 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.xp = (a.Mb + 3) & ~3;  // XT column pitch
   a.hp = (a.Gr + 3) & ~3;
   static const int variant = getenv("CBP_FFT_VARIANT") ? atoi(getenv("CBP_FFT_VARIANT")) : 0;
+  static const bool dyn = !getenv("CBP_STATIC_TILES");
+  a.tile_ctr = dyn ? ctx->tile_ctr : nullptr;
   a.hpos = column_slots(ctx, a.Gr, true);  // compile-time column plans: butterfly-major filter
   a.h_bmajor = a.hpos != nullptr;
   // rows per CTA for passes A/C: keep 2*rpc*L*8 bytes <= 64 KB, at most 8 rows
@@ -237,6 +239,7 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
       ctx->prof_planes += np;
       cudaEventRecord(ev[0], stream);
     }
+    if (a.tile_ctr) cudaMemsetAsync(a.tile_ctr, 0, 3 * sizeof(unsigned), stream);
     for (int pass = 0; pass < 3; ++pass) {
       int st = cuda_check(ctx, launch_deblur_pass(a, np, pass, stream), "deconvolution launch");
       if (st) return st;
@@ -284,6 +287,7 @@ int cbp_create(int device, cbp_ctx** out) {
     return CBP_CUDA_ERROR;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  if (cudaMalloc(&ctx->tile_ctr, 4 * sizeof(unsigned)) != cudaSuccess) ctx->tile_ctr = nullptr;  // static tiles then
   *out = ctx;
   return 0;
 }
@@ -296,6 +300,7 @@ void cbp_destroy(cbp_ctx* ctx) {
   for (void* p : ctx->ws)
     if (p) cudaFree(p);
   if (ctx->host_slot) cudaFreeHost(ctx->host_slot);
+  if (ctx->tile_ctr) cudaFree(ctx->tile_ctr);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   delete ctx;

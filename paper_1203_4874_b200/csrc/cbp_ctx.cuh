@@ -27,6 +27,7 @@ struct cbp_ctx {
   int prof_used = 0;
   long long prof_planes = 0;
   long long launches = 0;  // kernels enqueued by this context
+  unsigned* tile_ctr = nullptr;  // dynamic-tile counters of the deconvolution passes (device)
 };
 
 namespace cbp_host {

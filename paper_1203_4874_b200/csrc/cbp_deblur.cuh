@@ -44,6 +44,7 @@ struct DeblurArgs {
   size_t h_frame;         // H stride per slot
   int hp;                 // H column pitch (>= Gr, multiple of 4)
   const short* hpos;      // slot(u) of the column plan's DIF output, or null (natural order)
+  unsigned* tile_ctr;     // 3 dynamic-tile counters (passes A, B, C), zeroed per launch group, or null
   int h_bmajor;           // hpos is butterfly-major (i*NB + b for slot b*R1 + i): bulk pass B reads H from L2
 };
 

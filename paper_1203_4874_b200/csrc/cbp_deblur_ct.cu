@@ -152,9 +152,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     if (tile < total) issue(tile, sm);
     cp_async_commit();
   }
-  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+  // dynamic tiles: after its first (static) tile a CTA takes the next one from a counter,
+  // so CTAs that start late (SMs still held by another stream's kernels) take fewer tiles
+  unsigned* const ctr = BULK && a.tile_ctr ? a.tile_ctr + 0 : nullptr;
+  __shared__ int s_next[2];
+  for (int it = 0; tile < total; ++it) {
     float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
-    const int next = tile + gridDim.x;
+    int next = tile + gridDim.x;
+    if (ctr && threadIdx.x == 0) {  // only thread 0 uses `next` before the loop-end barrier
+      next = int(gridDim.x + atomicAdd(ctr, 1u));
+      s_next[it & 1] = next;
+    }
     if constexpr (BULK) {
       const int cb = it & 1;
       if (next < total && threadIdx.x == 0) issue_bulk(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
@@ -203,6 +211,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
       }
     }
     __syncthreads();
+    tile = ctr ? s_next[it & 1] : tile + gridDim.x;
   }
   if constexpr (!BULK) cp_async_wait<0>();
 }
@@ -326,7 +335,11 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
   unsigned ph[2] = {0u, 0u}, phh = 0u;
   int tile = blockIdx.x;
   if (tile < total && threadIdx.x == 0) issue(tile, sm, &bar[0]);
-  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+  // dynamic tiles: after its first (static) tile a CTA takes the next one from a counter,
+  // so CTAs that start late (SMs still held by another stream's kernels) take fewer tiles
+  unsigned* const ctr = a.tile_ctr ? a.tile_ctr + 1 : nullptr;
+  __shared__ int s_next[2];
+  for (int it = 0; tile < total; ++it) {
     const int cb = it & 1;
     float2* cur = sm + cb * TILE;
     const int p = tile / strips, v0 = (tile - p * strips) * W;
@@ -342,7 +355,11 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
       mbar_expect_tx(&bar[2], unsigned(nc) * unsigned(HB) * 8u);
       for (int s = 0; s < nc; ++s) bulk_g2s(Hs + s * GP, Ht + size_t(v0 + s) * a.hp, unsigned(HB) * 8u, &bar[2]);
     }
-    const int next = tile + gridDim.x;
+    int next = tile + gridDim.x;
+    if (ctr && threadIdx.x == 0) {  // only thread 0 uses `next` before the loop-end barrier
+      next = int(gridDim.x + atomicAdd(ctr, 1u));
+      s_next[it & 1] = next;
+    }
     if (next < total) {  // prefetch into the other buffer (its last bulk stores drained first)
       float2* nb = sm + (cb ^ 1) * TILE;
       if (threadIdx.x == 0) {
@@ -373,6 +390,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
       }
     }
     __syncthreads();
+    tile = ctr ? s_next[it & 1] : tile + gridDim.x;
   }
   if (threadIdx.x == 0) bulk_wait_all();
 }
@@ -464,9 +482,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
     if (tile < total) issue(tile, sm);
     cp_async_commit();
   }
-  for (int it = 0; tile < total; tile += gridDim.x, ++it) {
+  // dynamic tiles: after its first (static) tile a CTA takes the next one from a counter,
+  // so CTAs that start late (SMs still held by another stream's kernels) take fewer tiles
+  unsigned* const ctr = TMA && a.tile_ctr ? a.tile_ctr + 2 : nullptr;
+  int* const s_next = reinterpret_cast<int*>(bar + 2);  // dynamic smem: static smem would break the 128-byte TMA alignment
+  for (int it = 0; tile < total; ++it) {
     float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
-    const int next = tile + gridDim.x;
+    int next = tile + gridDim.x;
+    if (ctr && threadIdx.x == 0) {  // only thread 0 uses `next` before the loop-end barrier
+      next = int(gridDim.x + atomicAdd(ctr, 1u));
+      s_next[it & 1] = next;
+    }
     if constexpr (TMA) {
       const int cb = it & 1;
       if (next < total && threadIdx.x == 0) issue_tma(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
@@ -532,6 +558,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
       }
     }
     __syncthreads();
+    tile = ctr ? s_next[it & 1] : tile + gridDim.x;
   }
   if constexpr (!TMA) cp_async_wait<0>();
 }
@@ -676,7 +703,7 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
   const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) +
                      (P::RTW ? size_t(P::TWN) * sizeof(float2) : P::L * sizeof(short));
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 15) & ~15) * sizeof(float2) +
-                     size_t(P::RTW ? P::TWN : (P::L + 3) / 4) * sizeof(float2) + 2 * sizeof(unsigned long long);
+                     size_t(P::RTW ? P::TWN : (P::L + 3) / 4) * sizeof(float2) + 3 * sizeof(unsigned long long);
   static int pA = 0, pC = 0, pAb = 0, pCt = 0, sms = 0;
   constexpr bool kBulk = P::PIPE && P::L % 2 == 0;
   if (!sms) {

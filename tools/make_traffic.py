@@ -1,0 +1,35 @@
+"""profiles/deblur_traffic.json from an `ncu --set full` report of tools/prof_deblur.py
+(12 planes per launch): per-pass duration, DRAM bytes and instructions, and DRAM bytes per
+plane (bench.py reads `dram_bytes_per_plane` for roofline.traffic). Profiling aid.
+usage: make_traffic.py report.ncu-rep source-note"""
+import csv, io, json, subprocess, sys
+
+rep, note = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+PLANES = 12
+scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+out, tot = {}, 0.0
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    u = dict(zip(hdr, units))
+    name = d["Kernel Name"]
+    key = ("k_rows_forward_ct" if "rows_forward" in name else "k_cols_filter_bulk" if "cols_filter" in name
+           else "k_rows_inverse_ct")
+    rd = float(d["dram__bytes_read.sum"]) * scale[u["dram__bytes_read.sum"]]
+    wr = float(d["dram__bytes_write.sum"]) * scale[u["dram__bytes_write.sum"]]
+    us = float(d["gpu__time_duration.sum"]) * tscale[u["gpu__time_duration.sum"]]
+    out[key] = {"us": round(us, 2), "dram_read_MB": round(rd, 2), "dram_write_MB": round(wr, 2),
+                "inst_executed": int(float(d["smsp__inst_executed.sum"])),
+                "registers": int(float(d["launch__registers_per_thread"])),
+                "issue_active_pct": round(float(d["sm__inst_issued.avg.pct_of_peak_sustained_active"]), 1)}
+    tot += (rd + wr) * 1e6
+res = {"source": note, "per_launch_12_planes": out, "dram_bytes_per_plane": int(tot / PLANES),
+       "algorithmic_bytes_per_plane": 16709200,
+       "note": "One launch per pass covers the whole batch, so the transposed half spectrum (8.5 MB per plane) "
+               "round-trips through HBM: A writes it, B reads and rewrites it (the filter table is read from L2, "
+               "shared by the 3 planes of a frame), C reads it."}
+json.dump(res, open("profiles/deblur_traffic.json", "w"), indent=2)
+print(json.dumps(res, indent=1))
