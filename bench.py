@@ -214,7 +214,7 @@ def run_reference(args, world, rank):
 
 
 # --------------------------------------------------------------- B200 arm
-SM_RESERVE = int(os.environ.get("CBP_BENCH_SM_RESERVE", "16"))
+SM_RESERVE = int(os.environ.get("CBP_BENCH_SM_RESERVE", "12"))
 REC_STREAMS = int(os.environ.get("CBP_BENCH_REC_STREAMS", "2"))  # recoveries in flight
 
 
