@@ -10,7 +10,7 @@ recovered kernel, which stays on the device (cbp_kernel_slot).
 
 Inputs: synthetic U[0,1) latents generated on the device, blurred on the device by
 cbp_encode_frames with pairs from cbp_generate_coprime_pair (reference-exact host
-draw). A pool of --pool epochs (90 frames, 2.3 GB of public frames) is cycled, so every
+draw). A pool of --pool epochs (default 5: 150 frames, 3.8 GB of public frames) is cycled, so every
 step reads inputs far larger than the 126 MB L2.
 
 Arms:
@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--pool", type=int, default=4, help="distinct epochs cycled by the steps (>= 3)")
+    p.add_argument("--pool", type=int, default=5, help="distinct epochs cycled by the steps (>= recovery streams + 2)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -215,7 +215,7 @@ def run_reference(args, world, rank):
 
 # --------------------------------------------------------------- B200 arm
 SM_RESERVE = int(os.environ.get("CBP_BENCH_SM_RESERVE", "12"))
-REC_STREAMS = int(os.environ.get("CBP_BENCH_REC_STREAMS", "2"))  # recoveries in flight
+REC_STREAMS = int(os.environ.get("CBP_BENCH_REC_STREAMS", "3"))  # recoveries in flight
 
 
 def run_b200(args, world, rank, local):
