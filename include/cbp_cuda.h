@@ -186,6 +186,21 @@ int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* 
                                int channels, int rows, int cols, int ld, const int* width_hints,
                                const cbp_decode_cfg* cfg, float* latent_dev, int ld_out,
                                cbp_kernel_slot* slots_dev, void* stream, void* slot_ready_event);
+/* decode_frame split at its stage boundaries (decoder.cpp:280-378), for pipelines that batch
+ * the recovery frame's deconvolution with the frames that reuse its kernel:
+ *  - cbp_recover_kernels_async: width estimation, unit-circle sampling, cofactor solves and
+ *    kernel composition (decoder.cpp:290-352) into slots_dev; no deconvolution, no residual;
+ *  - cbp_validate_frames_async: the validation residual (decoder.cpp:367-376) of latents
+ *    already deconvolved with the slots' kernels (e.g. by cbp_spectral_deblur_slot) into
+ *    slots_dev[b].residual.
+ * recover -> spectral_deblur_slot -> validate gives bit-identical slots and latents to
+ * cbp_decode_frames_async. */
+int cbp_recover_kernels_async(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch,
+                              int channels, int rows, int cols, int ld, const int* width_hints,
+                              const cbp_decode_cfg* cfg, cbp_kernel_slot* slots_dev, void* stream);
+int cbp_validate_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* latent_dev, int batch,
+                              int channels, int rows, int cols, int ld, int ld_out,
+                              cbp_kernel_slot* slots_dev, void* stream);
 int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,
                              int rows, int cols, int ld, const cbp_kernel_slot* slot_dev,
                              float* latent_dev, int ld_out, void* stream);

@@ -537,6 +537,32 @@ def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, ou
                                               C.c_void_p(slots.data_ptr()), st))
 
 
+def recover_kernels_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, slots: torch.Tensor, hints=None,
+                          ctx: N.Context | None = None, stream=None):
+    """cbp_recover_kernels_async: decode_frame's recovery stages only (decoder.cpp:290-352),
+    kernels, widths and epsilons into ``slots``; deconvolve with spectral_deblur_slot and
+    finish with validate_frames_async for the same results as decode_frames_async."""
+    B, ch, rows, cols = pub.shape
+    ctx = ctx or context(pub.device.index)
+    hint_arr = (C.c_int * B)(*[int(h) for h in hints]) if hints is not None else None
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
+    ctx.check(N.lib().cbp_recover_kernels_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(prv.data_ptr()), B,
+                                                ch, rows, cols, pub.stride(-2), hint_arr, C.byref(cfg),
+                                                C.c_void_p(slots.data_ptr()), st))
+
+
+def validate_frames_async(pub: torch.Tensor, latent: torch.Tensor, slots: torch.Tensor, ctx: N.Context | None = None,
+                          stream=None):
+    """cbp_validate_frames_async: validation residual (decoder.cpp:367-376) of deconvolved
+    latents into ``slots[b].residual``."""
+    B, ch, rows, cols = pub.shape
+    ctx = ctx or context(pub.device.index)
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
+    ctx.check(N.lib().cbp_validate_frames_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(latent.data_ptr()), B,
+                                                ch, rows, cols, pub.stride(-2), latent.stride(-2),
+                                                C.c_void_p(slots.data_ptr()), st))
+
+
 def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor, ctx: N.Context | None = None,
                          stream=None):
     """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device."""

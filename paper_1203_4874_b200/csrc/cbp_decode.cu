@@ -196,9 +196,11 @@ T* pinned(cbp_ctx* ctx, size_t count) {
 }
 
 // Enqueues the whole decode for a batch (no synchronization).
+// stages: which parts of decode_frame (decoder.cpp:280-378) to enqueue
+constexpr int kStageRecover = 1, kStageDeblur = 2, kStageValidate = 4, kStageAll = 7;
 int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, int channels, int rows, int cols,
                    int ld, const int* hints, const cbp_decode_cfg* cfg, float* latent, int ld_out,
-                   cbp_kernel_slot* slots, cudaStream_t s, bool record_events) {
+                   cbp_kernel_slot* slots, cudaStream_t s, bool record_events, int stages = kStageAll) {
   int st;
   if ((st = check_geometry(ctx, batch, channels, rows, cols, ld))) return st;
   if (ld_out < cols) return set_error(ctx, CBP_INVALID_ARGUMENT, "output row pitch smaller than the row");
@@ -258,6 +260,7 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
   // kernels, widths and epsilons are final here; the frame's own deconvolution and the
   // validation residual follow on this stream, consumers of the slots need not wait for them
   if (ctx->slot_event) cudaEventRecord(static_cast<cudaEvent_t>(ctx->slot_event), s);
+  if (!(stages & kStageDeblur)) return 0;  // cbp_recover_kernels_async
   DeblurArgs d;
   if ((st = deblur_setup(ctx, rows, cols, d))) return st;
   d.in = pub;
@@ -269,7 +272,7 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
   d.channels = channels;
   if ((st = deblur_run(ctx, d, batch * channels, size_t(rows) * ld, size_t(rows) * ld_out, s))) return st;
   if (record_events) cudaEventRecord(ctx->ev[4], s);
-  if (cfg->validate) {
+  if (cfg->validate && (stages & kStageValidate)) {
     a.pub = pub;
     if ((st = cuda_check(ctx, launch_validate(a, latent, ld_out, P.vpart, P.vtiles, s), "validation launch")))
       return st;
@@ -304,6 +307,40 @@ int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv
   if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
   return enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg, latent_dev,
                         ld_out, slots_dev, static_cast<cudaStream_t>(stream), false);
+}
+
+int cbp_recover_kernels_async(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels,
+                              int rows, int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg,
+                              cbp_kernel_slot* slots_dev, void* stream) {
+  if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
+  return enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg, nullptr, ld,
+                        slots_dev, static_cast<cudaStream_t>(stream), false, kStageRecover);
+}
+
+int cbp_validate_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* latent_dev, int batch, int channels,
+                              int rows, int cols, int ld, int ld_out, cbp_kernel_slot* slots_dev, void* stream) {
+  if (!ctx || !slots_dev || !latent_dev) return CBP_INVALID_ARGUMENT;
+  int st;
+  if ((st = check_geometry(ctx, batch, channels, rows, cols, ld))) return st;
+  if (ld_out < cols) return set_error(ctx, CBP_INVALID_ARGUMENT, "output row pitch smaller than the row");
+  if (batch == 0) return 0;
+  RecoverArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.pub = pub_dev;
+  a.batch = batch;
+  a.channels = channels;
+  a.rows = rows;
+  a.cols = cols;
+  a.ld = ld;
+  a.t_max = kDeviceMaxWidth;  // slot widths are <= 31 (solver limit)
+  a.slots = slots_dev;
+  const int vtiles = validate_tiles(rows, cols, kDeviceMaxWidth);
+  double* vpart = ws<double>(ctx, WS_RED, size_t(2) * batch * channels * vtiles + 8);
+  if (!vpart) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  st = cuda_check(ctx, launch_validate(a, latent_dev, ld_out, vpart, vtiles, static_cast<cudaStream_t>(stream)),
+                  "validation launch");
+  ctx->launches += 2;
+  return st;
 }
 
 int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels,

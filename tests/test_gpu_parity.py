@@ -253,6 +253,33 @@ def test_slot_ready_event_pipeline(oracle, api):
     assert torch.equal(out[..., :90, :122], ref[..., :90, :122])
 
 
+@pytest.mark.parametrize("geom", [(96, 128, 3, 7), (1080, 1920, 3, 11)])
+def test_split_decode_equals_decode(oracle, api, geom):
+    """cbp_recover_kernels_async -> cbp_spectral_deblur_slot over ALL frames (the recovery
+    frame batched with the ones reusing its kernel, as bench.py does) -> cbp_validate_frames_async
+    gives bit-identical kernels, residuals and latents to decode_frames_async + deblur."""
+    rows, cols, ch, t = geom
+    pair = oracle.generate_coprime_pair(t, 16)
+    lat = api.synth_frames(3 * ch, rows, cols, seed=5).view(3, ch, rows, cols)
+    P, Q = api.encode_frame(lat, pair.k1, pair.k2)
+    cfg = api.make_cfg(3 if t < 9 else 9, 25 if t >= 9 else 9)
+    out = torch.zeros_like(P)
+    slots = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    api.recover_kernels_async(P[0:1], Q[0:1], cfg, slots[0])
+    api.spectral_deblur_slot(P, slots[0].data_ptr(), out)
+    api.validate_frames_async(P[0:1], out[0:1], slots[0])
+    ref = torch.zeros_like(P)
+    slots2 = torch.zeros((1, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    api.decode_frames_async(P[0:1], Q[0:1], cfg, ref[0:1], slots2[0])
+    api.spectral_deblur_slot(P[1:], slots2[0].data_ptr(), ref[1:])
+    torch.cuda.synchronize()
+    a, b = api.read_slots(slots, 1)[0], api.read_slots(slots2, 1)[0]
+    assert a.status == b.status == 0 and a.width == b.width == t
+    assert a.residual == b.residual and 0.0 < a.residual <= 1e-4
+    assert list(a.weights[: t * t]) == list(b.weights[: t * t])
+    assert torch.equal(out[..., : rows, : cols], ref[..., : rows, : cols])
+
+
 def test_host_pipeline_equals_device_path(oracle, api):
     pair = oracle.generate_coprime_pair(5, 31)
     frames = [oracle.encode_frame(oracle.random_frame(60, 70, 1, 40 + i), pair.k1, pair.k2) for i in range(5)]
