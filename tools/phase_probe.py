@@ -10,7 +10,7 @@ lat = api.synth_frames(CH, R, Cc, seed=1).view(1, CH, R, Cc)
 pub, prv = api.encode_frame(lat, pair.k1, pair.k2)
 out = torch.empty_like(pub)
 slots = torch.zeros(api.SLOT_BYTES, dtype=torch.uint8, device="cuda")
-cfg = api.make_cfg(9, 25, 1e-6, validate=True)
+cfg = api.make_cfg(3 if T < 9 else 9, 25, 1e-6, validate=True)
 for it in range(3):
     api.decode_frames_async(pub, prv, cfg, out, slots)
 torch.cuda.synchronize()
