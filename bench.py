@@ -393,26 +393,31 @@ def run_b200(args, world, rank, local):
     # ---- end-to-end through the host-buffer C ABI call (pinned host memory)
     e2e = None
     if not args.no_e2e:
-        hpub = pub[0].contiguous().cpu().pin_memory()
+        # one host-buffer run of e2e_steps epochs (distinct pool epochs), like the reference CLI
+        # decoding a video run (tools/cbp.cpp:130-207): the pipeline streams across the epoch
+        # boundaries (recovery frames at 0, 30, 60, ...) instead of refilling per epoch
+        nE = args.e2e_steps
+        hpub = torch.cat([pub[e % E].contiguous().cpu() for e in range(nE)]).pin_memory()
         hprv = torch.zeros_like(hpub).pin_memory()
-        hprv[0].copy_(prv[0, 0].cpu())
+        rec = np.zeros(EPOCH * nE, np.int32)
+        for e in range(nE):
+            hprv[EPOCH * e].copy_(prv[e % E, 0].cpu())
+            rec[EPOCH * e] = 1
         hout = torch.empty_like(hpub).pin_memory()
-        rec = np.zeros(EPOCH, np.int32)
-        rec[0] = 1
-        api.decode_run_host(hpub, hprv, rec, cfg, out=hout, device=local)  # warm-up
+        api.decode_run_host(hpub[:EPOCH], hprv[:EPOCH], rec[:EPOCH], cfg, out=hout[:EPOCH], device=local)  # warm-up
         barrier(world)
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            _, sl = api.decode_run_host(hpub, hprv, rec, cfg, out=hout, device=local)
+        _, sl = api.decode_run_host(hpub, hprv, rec, cfg, out=hout, device=local)
         t1 = time.perf_counter()
         barrier(world)
         e2e_s = max_over_ranks(t1 - t0, world)
         frame_bytes = CH * Mb * Nb * 4
-        e2e = {"value": EPOCH * args.e2e_steps * world / e2e_s, "unit": "frames/s",
+        e2e = {"value": EPOCH * nE * world / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * frame_bytes,
-               "steps": args.e2e_steps, "host_memory": "pinned",
-               "api": "cbp_decode_run_host (C ABI, host buffers, H2D/compute/D2H overlapped)"}
-        if sl[0].status != 0 or sl[0].width != T:
+               "steps": nE, "host_memory": "pinned",
+               "api": f"cbp_decode_run_host (C ABI, host buffers, H2D/compute/D2H overlapped): one run of "
+                      f"{nE} epochs = {EPOCH * nE} frames, a recovery frame every {EPOCH}"}
+        if any(x.status != 0 or x.width != T for x in sl):
             raise RuntimeError("e2e recovery failed")
         del hpub, hprv, hout
 

@@ -10,7 +10,9 @@
 #include "cbp_ctx.cuh"
 
 namespace {
-constexpr int kRing = 3;
+// ring depth: H2D runs up to kRing frames ahead, so the ~1 ms recovery of a frame hides
+// under the transfers of the following ones (the path is PCIe-bound)
+constexpr int kRing = 6;
 
 struct Pipe {
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
