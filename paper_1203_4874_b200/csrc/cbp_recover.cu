@@ -178,7 +178,16 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
       if constexpr (C == 1) return double(st[j * FT_W + c]);
       else return tl[j * FT_W + c];
     };
-    if (split) {  // uniform: t is per frame
+    if (t == 1) {  // DC fold (row sums): warp w reduces row w over the strip, fixed-order tree
+      const int lane = threadIdx.x & 31;
+      const int m = r0 + r + (FT_J * g + warp);
+      double sz = 0.0;
+#pragma unroll
+      for (int k = 0; k < FT_W / 32; ++k) sz += val(warp, lane + 32 * k);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, off);
+      if (lane == 0 && m < r1) p2[m] = sz;
+    } else if (split) {  // uniform: t is per frame
       const int m = r0 + r + t * (FT_J * g + jz);
       double sz = 0.0;
       if (jz < FT_J) {
