@@ -1438,6 +1438,180 @@ __global__ void __launch_bounds__(256, CBP_CONV_OUT == 16 ? 2 : 3) k_conv_resid(
   }
 }
 
+// Validation residual, mode 0 (decode), two output columns per thread: tile column c feeds
+// output column 2l (kernel column b2 = b - 1) and 2l + 1 (b2 = b) for c = 2l + t - b, so a
+// thread loads t + 1 windows for 2t kernel columns (k_conv_resid: one window per kernel
+// column). Even and odd tile columns live in separate arrays (te, to): lane l reads index
+// l + const in one of them, a conflict-free warp access. CTA = 32 rows x 64 columns, 128
+// threads: the same tiles and partial layout as k_conv_resid, and per output the same FMA
+// order (bit-identical convolution values).
+template <int OUT, int TP>
+__device__ __forceinline__ void conv_col2T(const double* te, const double* to, int twh, const double* kt, int t,
+                                           int li0, int l, double* acc0, double* acc1) {
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) acc0[q] = acc1[q] = 0.0;
+  for (int b = 0; b <= t; ++b) {
+    const int c = 2 * l + t - b;  // parity of c = parity of t - b: warp-uniform
+    const double* col = ((c & 1) ? to : te) + (li0 + TP - 1) * twh + (c >> 1);
+    double v[OUT + TP - 1];
+#pragma unroll
+    for (int k = 0; k < OUT + TP - 1; ++k) v[k] = col[(OUT - 1 - k) * twh];
+    if (b < t) {
+      const double* kc = kt + b * TP;
+#pragma unroll
+      for (int j = 0; j < TP; ++j) {
+        const double w = kc[j];
+#pragma unroll
+        for (int q = 0; q < OUT; ++q) acc1[q] = fma(w, v[OUT - 1 - q + j], acc1[q]);
+      }
+    }
+    if (b > 0) {
+      const double* kc = kt + (b - 1) * TP;
+#pragma unroll
+      for (int j = 0; j < TP; ++j) {
+        const double w = kc[j];
+#pragma unroll
+        for (int q = 0; q < OUT; ++q) acc0[q] = fma(w, v[OUT - 1 - q + j], acc0[q]);
+      }
+    }
+  }
+}
+// one column at a time (wide kernels: the two-column window would not fit in registers)
+template <int OUT, int TP>
+__device__ __forceinline__ void conv_col1T(const double* te, const double* to, int twh, const double* kt, int t,
+                                           int li0, int lj, double* acc) {
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) acc[q] = 0.0;
+  for (int b2 = 0; b2 < t; ++b2) {
+    const int c = lj + t - 1 - b2;
+    const double* col = ((c & 1) ? to : te) + (li0 + TP - 1) * twh + (c >> 1);
+    double v[OUT + TP - 1];
+#pragma unroll
+    for (int k = 0; k < OUT + TP - 1; ++k) v[k] = col[(OUT - 1 - k) * twh];
+    const double* kc = kt + b2 * TP;
+#pragma unroll
+    for (int j = 0; j < TP; ++j) {
+      const double w = kc[j];
+#pragma unroll
+      for (int q = 0; q < OUT; ++q) acc[q] = fma(w, v[OUT - 1 - q + j], acc[q]);
+    }
+  }
+}
+__device__ __forceinline__ void conv2_dispatch(const double* te, const double* to, int twh, const double* kt, int t,
+                                               int tp, int li0, int l, double* a0, double* a1) {
+  switch (tp) {
+    case 4: return conv_col2T<8, 4>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 8: return conv_col2T<8, 8>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 12: return conv_col2T<8, 12>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 16: return conv_col2T<8, 16>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 20:
+      conv_col1T<8, 20>(te, to, twh, kt, t, li0, 2 * l, a0);
+      return conv_col1T<8, 20>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
+    case 24:
+      conv_col1T<8, 24>(te, to, twh, kt, t, li0, 2 * l, a0);
+      return conv_col1T<8, 24>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
+    case 28:
+      conv_col1T<8, 28>(te, to, twh, kt, t, li0, 2 * l, a0);
+      return conv_col1T<8, 28>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
+    default:
+      conv_col1T<8, 32>(te, to, twh, kt, t, li0, 2 * l, a0);
+      return conv_col1T<8, 32>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
+  }
+}
+
+constexpr int CONV2_THREADS = 128;
+__global__ void __launch_bounds__(CONV2_THREADS, 4) k_conv_resid2(ConvResidArgs a) {
+  extern __shared__ double shd2[];
+  constexpr int OUT = 8, VT_R = 4 * OUT;  // 4 row groups of 32 threads
+  const int plane = blockIdx.y;
+  const int frame = plane / a.channels;
+  const cbp_kernel_slot* slot = a.slots + frame;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  const double* K = slot->weights;
+  const int tp = conv_pad(t);
+  const int xr = a.xr - t + 1, xc = a.xc - t + 1;  // the latent extent
+  const int ro = a.xr, co = a.xc;
+  const int tiles_c = (co + VT_C - 1) / VT_C;
+  const int tr = blockIdx.x / tiles_c, tc = blockIdx.x - tr * tiles_c;
+  const int i0 = tr * VT_R, j0 = tc * VT_C;
+  if (i0 >= ro) return;
+  double* kt = shd2;  // t x tp (transposed)
+  const int tw = VT_C + t - 1, th = VT_R + tp - 1, twh = (tw + 1) / 2;
+  double* te = kt + t * tp;   // even tile columns, th x twh
+  double* to = te + th * twh;  // odd tile columns
+  for (int i = threadIdx.x; i < t * tp; i += blockDim.x) {
+    const int bb = i / tp, aa = i - bb * tp;
+    kt[i] = aa < t ? K[aa * t + bb] : 0.0;
+  }
+  const float* X = a.X + size_t(plane) * a.x_plane;
+  const float* Y = a.Y + size_t(plane) * a.y_plane;
+  constexpr int LB = 8;
+  for (int base = threadIdx.x; base < th * tw; base += LB * blockDim.x) {
+    float xv[LB];
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int idx = base + u * blockDim.x;
+      const int li = idx / tw, lj = idx - li * tw;
+      const int gi = i0 - tp + 1 + li, gj = j0 - t + 1 + lj;
+      const bool in = idx < th * tw && gi >= 0 && gi < xr && gj >= 0 && gj < xc;
+      xv[u] = in ? __ldg(X + size_t(gi) * a.xld + gj) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < th * tw) {
+        const int li = idx / tw, lj = idx - li * tw;
+        ((lj & 1) ? to : te)[li * twh + (lj >> 1)] = double(xv[u]);
+      }
+    }
+  }
+  __syncthreads();
+  double num = 0.0, den = 0.0;
+  const int l = threadIdx.x & 31, li0 = (threadIdx.x >> 5) * OUT;
+  const int gj0 = j0 + 2 * l;
+  if (gj0 < co && i0 + li0 < ro) {
+    double c0[OUT], c1[OUT];
+    conv2_dispatch(te, to, twh, kt, t, tp, li0, l, c0, c1);
+    float y0[OUT], y1[OUT];  // the compared samples (after the convolution: registers)
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) {
+      const int gi = i0 + li0 + q;
+      y0[q] = gi < ro ? __ldg(Y + size_t(gi) * a.yld + gj0) : 0.f;
+      y1[q] = gi < ro && gj0 + 1 < co ? __ldg(Y + size_t(gi) * a.yld + gj0 + 1) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < OUT; ++q) {
+      const int gi = i0 + li0 + q;
+      if (gi >= ro) break;
+      const double ya = double(y0[q]);
+      den += ya * ya;
+      num += (c0[q] - ya) * (c0[q] - ya);
+      if (gj0 + 1 < co) {
+        const double yb = double(y1[q]);
+        den += yb * yb;
+        num += (c1[q] - yb) * (c1[q] - yb);
+      }
+    }
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  __shared__ double rn[CONV2_THREADS / 32], rd[CONV2_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) rn[warp] = num, rd[warp] = den;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sn = 0, sd = 0;
+    for (int w = 0; w < CONV2_THREADS / 32; ++w) sn += rn[w], sd += rd[w];
+    a.part[size_t(plane) * a.ntiles + blockIdx.x] = make_double2(sn, sd);
+  }
+}
+
+__host__ inline size_t conv2_smem(int t) {
+  const int tp = conv_pad(t), tw = VT_C + t - 1;
+  return (size_t(t) * tp + 2 * size_t(4 * 8 + tp - 1) * ((tw + 1) / 2)) * sizeof(double);
+}
+
 __host__ inline size_t conv_smem(int t, int mode) {
   const int tp = conv_pad(t);
   // both weight blocks are always carved (the kernel lays the tile out after them)
@@ -1500,11 +1674,18 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.ro = ra.rows;
   a.co = ra.cols;
   dim3 g(ntiles_max, ra.batch * ra.channels);
+  static const bool two = !getenv("CBP_CONV_ONECOL") && conv_rows(1) == 32;
   size_t sm = 0;  // the device-side width is <= min(t_max, 31) (solver limit); tile heights vary with t
-  for (int t = 1; t <= std::min(ra.t_max, 31); ++t) sm = std::max(sm, conv_smem(t, 0));
-  if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
-    return cudaErrorInvalidValue;
-  k_conv_resid<<<g, 256, sm, s>>>(a);
+  for (int t = 1; t <= std::min(ra.t_max, 31); ++t) sm = std::max(sm, two ? conv2_smem(t) : conv_smem(t, 0));
+  if (two) {
+    if (cudaFuncSetAttribute(k_conv_resid2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    k_conv_resid2<<<g, CONV2_THREADS, sm, s>>>(a);
+  } else {
+    if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
+      return cudaErrorInvalidValue;
+    k_conv_resid<<<g, 256, sm, s>>>(a);
+  }
   k_resid_reduce<<<ra.batch, 256, 0, s>>>(a.part, ntiles_max, ra.channels, ra.slots, nullptr, ra.batch);
   return cudaGetLastError();
 }
