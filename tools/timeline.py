@@ -11,8 +11,9 @@ import torch
 
 from paper_1203_4874_b200 import api, _native
 
-ROWS, COLS, CH, T, EPOCH, E = 1080, 1920, 3, 11, 30, 4
-reserve = int(os.environ.get("TL_RESERVE", "16"))
+ROWS, COLS, CH, T, EPOCH = 1080, 1920, 3, 11, 30
+E = int(os.environ.get("TL_POOL", "5"))
+reserve = int(os.environ.get("TL_RESERVE", "12"))
 steps = int(os.environ.get("TL_STEPS", "12"))
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(dev)
@@ -30,7 +31,7 @@ for e in range(E):
 out = torch.empty((E, EPOCH, CH, Mb, NbP), dtype=torch.float32, device=dev)[..., :Nb]
 slots = torch.zeros((E, api.SLOT_BYTES), dtype=torch.uint8, device=dev)
 cfg = api.make_cfg(9, 25, 1e-6, validate=True)
-NREC = int(os.environ.get("TL_REC", "2"))
+NREC = int(os.environ.get("TL_REC", "3"))
 ctxs = [_native.Context(0) for _ in range(NREC)]
 recs = [torch.cuda.Stream(dev, priority=-1) for _ in range(NREC)]
 ctx_rec, s_rec = ctxs[0], recs[0]
