@@ -186,6 +186,13 @@ int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* 
                                int channels, int rows, int cols, int ld, const int* width_hints,
                                const cbp_decode_cfg* cfg, float* latent_dev, int ld_out,
                                cbp_kernel_slot* slots_dev, void* stream, void* slot_ready_event);
+/* Many kernels in one call: frame f of the batch is deconvolved with slots_dev[f /
+ * frames_per_slot] (e.g. S camera streams x n frames, stream-major, frames_per_slot = n:
+ * one launch group and one Wiener-table launch for all streams instead of S calls). A
+ * failed slot leaves its frames' outputs untouched. */
+int cbp_spectral_deblur_slots(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,
+                              int rows, int cols, int ld, const cbp_kernel_slot* slots_dev,
+                              int frames_per_slot, float* latent_dev, int ld_out, void* stream);
 /* decode_frame split at its stage boundaries (decoder.cpp:280-378), for pipelines that batch
  * the recovery frame's deconvolution with the frames that reuse its kernel:
  *  - cbp_recover_kernels_async: width estimation, unit-circle sampling, cofactor solves and

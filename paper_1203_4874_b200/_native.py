@@ -86,6 +86,7 @@ _SIGS = {
     "cbp_spectral_deblur": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _D, _P, _I, _P]),
     "cbp_spectral_deblur_slot": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P]),
     "cbp_recover_kernels_async": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "cbp_spectral_deblur_slots": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P]),
     "cbp_validate_frames_async": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P]),
     "cbp_estimate_kernel_width": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _D, _P, _P, _P]),
     "cbp_sample_slices": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P]),

@@ -563,6 +563,18 @@ def validate_frames_async(pub: torch.Tensor, latent: torch.Tensor, slots: torch.
                                                 C.c_void_p(slots.data_ptr()), st))
 
 
+def spectral_deblur_slots(blurred: torch.Tensor, slots: torch.Tensor, frames_per_slot: int, out: torch.Tensor,
+                          ctx: N.Context | None = None, stream=None):
+    """cbp_spectral_deblur_slots: frame f of ``blurred`` (batch, ch, rows, cols) is deconvolved
+    with slot ``f // frames_per_slot`` of ``slots`` (uint8 device tensor of kernel slots)."""
+    B, ch, rows, cols = blurred.shape
+    ctx = ctx or context(blurred.device.index)
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(blurred.device)
+    ctx.check(N.lib().cbp_spectral_deblur_slots(ctx.ptr, C.c_void_p(blurred.data_ptr()), B, ch, rows, cols,
+                                                blurred.stride(-2), C.c_void_p(slots.data_ptr()),
+                                                int(frames_per_slot), C.c_void_p(out.data_ptr()), out.stride(-2), st))
+
+
 def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor, ctx: N.Context | None = None,
                          stream=None):
     """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device."""

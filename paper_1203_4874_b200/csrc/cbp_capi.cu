@@ -140,6 +140,7 @@ int friendly_size(int n) {  // fft.cpp:272-280
 
 int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   std::memset(&a, 0, sizeof(a));
+  a.frames_per_slot = 1;
   a.Mb = Mb;
   a.Nb = Nb;
   a.Gr = friendly_size(Mb);
@@ -194,6 +195,9 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   int frames_per_group = int(std::max<size_t>(1, budget / (plane_bytes * ch)));
   const int frames = planes / ch;
   frames_per_group = std::min(frames_per_group, std::max(frames, 1));
+  const int fps = a.slot_per_frame ? std::max(a.frames_per_slot, 1) : 1;
+  a.frames_per_slot = fps;
+  if (fps > 1 && frames_per_group >= fps) frames_per_group -= frames_per_group % fps;  // groups start on a slot
   const int group_planes = frames_per_group * ch;
   float2* X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * group_planes));
   if (!X) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
@@ -202,7 +206,7 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   a.in_plane = in_plane_stride;
   a.out_plane = out_plane_stride;
   // Wiener filter table(s) H[u][v] for the kernel slot(s) of this batch
-  const int nslots = a.slot_per_frame ? std::max(frames, 1) : 1;
+  const int nslots = a.slot_per_frame ? std::max((frames + fps - 1) / fps, 1) : 1;
   a.s_frame = size_t(a.Hc) * CBP_MAX_WIDTH;
   a.h_frame = size_t(a.Hc) * a.hp;
   a.S = static_cast<double2*>(workspace(ctx, WS_RED + 1, sizeof(double2) * a.s_frame * nslots));
@@ -219,9 +223,13 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
     const int np = std::min(group_planes, planes - p0);
     a.in = in0 + size_t(p0) * in_plane_stride;
     a.out = out0 + size_t(p0) * out_plane_stride;
-    a.slot = slot0 + (a.slot_per_frame ? p0 / ch : 0);
-    a.S = S0 + (a.slot_per_frame ? size_t(p0 / ch) * a.s_frame : 0);
-    a.H = H0 + (a.slot_per_frame ? size_t(p0 / ch) * a.h_frame : 0);
+    // a group starts on a slot boundary when it can (frames_per_group a multiple of fps);
+    // otherwise (fps > frames per group) slot indices stay global: base slot 0
+    const int s0 = a.slot_per_frame && frames_per_group % fps == 0 ? (p0 / ch) / fps : 0;
+    a.slot = slot0 + s0;
+    a.S = S0 + size_t(s0) * (a.slot_per_frame ? a.s_frame : 0);
+    a.H = H0 + size_t(s0) * (a.slot_per_frame ? a.h_frame : 0);
+    a.frame0 = a.slot_per_frame && frames_per_group % fps != 0 ? p0 / ch : 0;
     a.in_vec2 = (reinterpret_cast<uintptr_t>(a.in) % 8 == 0) && a.in_ld % 2 == 0 && in_plane_stride % 2 == 0;
     a.out_vec2 = (reinterpret_cast<uintptr_t>(a.out) % 8 == 0) && a.out_ld % 2 == 0 && out_plane_stride % 2 == 0;
     a.in_vec4 = (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) && a.in_ld % 4 == 0 && in_plane_stride % 4 == 0;
@@ -401,6 +409,28 @@ int cbp_spectral_deblur(cbp_ctx* ctx, const float* blurred_dev, int batch, int c
   a.slot_per_frame = 0;
   a.channels = channels;
   return deblur_run(ctx, a, batch * channels, size_t(rows) * ld, size_t(rows) * ld_out, s);
+}
+
+int cbp_spectral_deblur_slots(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels, int rows, int cols,
+                              int ld, const cbp_kernel_slot* slots_dev, int frames_per_slot, float* latent_dev,
+                              int ld_out, void* stream) {
+  if (!ctx || !slots_dev) return CBP_INVALID_ARGUMENT;
+  if (frames_per_slot < 1) return set_error(ctx, CBP_INVALID_ARGUMENT, "frames_per_slot must be >= 1");
+  int st = check_geometry(ctx, batch, channels, rows, cols, ld);
+  if (st) return st;
+  if (batch == 0) return 0;
+  DeblurArgs a;
+  if ((st = deblur_setup(ctx, rows, cols, a))) return st;
+  a.in = blurred_dev;
+  a.in_ld = ld;
+  a.out = latent_dev;
+  a.out_ld = ld_out;
+  a.slot = slots_dev;
+  a.slot_per_frame = 1;
+  a.frames_per_slot = frames_per_slot;
+  a.channels = channels;
+  return deblur_run(ctx, a, batch * channels, size_t(rows) * ld, size_t(rows) * ld_out,
+                    static_cast<cudaStream_t>(stream));
 }
 
 int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,

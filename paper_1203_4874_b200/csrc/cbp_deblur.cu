@@ -75,7 +75,7 @@ template <int W>
 __global__ void __launch_bounds__(256) k_cols_filter(DeblurArgs a) {
   extern __shared__ float2 smem[];
   const int p = blockIdx.y;
-  const cbp_kernel_slot* slot = a.slot + (a.slot_per_frame ? p / a.channels : 0);
+  const cbp_kernel_slot* slot = a.slot + deblur_slot_index(a, p);
   if (slot->status != 0) return;
   const int t = slot->width;
   const int M = a.Mb - t + 1;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) k_cols_filter(DeblurArgs a) {
 __global__ void __launch_bounds__(256) k_rows_inverse(DeblurArgs a) {
   extern __shared__ float2 smem[];
   const int p = blockIdx.y;
-  const cbp_kernel_slot* slot = a.slot + (a.slot_per_frame ? p / a.channels : 0);
+  const cbp_kernel_slot* slot = a.slot + deblur_slot_index(a, p);
   if (slot->status != 0) return;
   const int t = slot->width;
   const int M = a.Mb - t + 1, N = a.Nb - t + 1;

@@ -46,7 +46,14 @@ struct DeblurArgs {
   const short* hpos;      // slot(u) of the column plan's DIF output, or null (natural order)
   unsigned* tile_ctr;     // 3 dynamic-tile counters (passes A, B, C), zeroed per launch group, or null
   int h_bmajor;           // hpos is butterfly-major (i*NB + b for slot b*R1 + i): bulk pass B reads H from L2
+  int frames_per_slot;    // slot_per_frame: frame f uses slot f / frames_per_slot (>= 1)
+  int frame0;             // launch group's first frame when its slot indices are global
 };
+
+// kernel slot (and Wiener table) index of plane p
+__host__ __device__ inline int deblur_slot_index(const DeblurArgs& a, int p) {
+  return a.slot_per_frame ? (a.frame0 + p / a.channels) / (a.frames_per_slot > 0 ? a.frames_per_slot : 1) : 0;
+}
 
 int deblur_col_width(int Gr, int t_max);
 // pass 0: rows forward (A), 1: columns + filter (B), 2: rows inverse + crop (C)

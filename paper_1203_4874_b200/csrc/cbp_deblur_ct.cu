@@ -66,7 +66,7 @@ __device__ __forceinline__ const float2* stage_row_twiddles(const DeblurArgs& a,
 }
 
 __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a, int p) {
-  return a.slot + (a.slot_per_frame ? p / a.channels : 0);
+  return a.slot + deblur_slot_index(a, p);
 }
 
 // The half spectrum lives transposed in HBM/L2: XT[v][u] (v < Hc columns, u < Mb rows,
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_ct(DeblurArgs a,
   for (int it = 0; tile < total; tile += gridDim.x, ++it) {
     float2* cur = sm + (P::PIPE ? (it & 1) * TILE : 0);
     const int p = tile / strips, v0 = (tile - p * strips) * W;
-    const int f = a.slot_per_frame ? p / a.channels : 0;
+    const int f = deblur_slot_index(a, p);
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
     cp_async_wait<0>();
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     const int cb = it & 1;
     float2* cur = sm + cb * TILE;
     const int p = tile / strips, v0 = (tile - p * strips) * W;
-    const int f = a.slot_per_frame ? p / a.channels : 0;
+    const int f = deblur_slot_index(a, p);
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
     mbar_wait(&bar[cb], ph[cb]);  // every thread observes the strip's arrival

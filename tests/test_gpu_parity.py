@@ -574,3 +574,43 @@ def test_deblur_repeatable(oracle, api, rows, cols, ch, t, frames):
     torch.cuda.synchronize()
     assert torch.equal(single[..., :M, :N], outs[0][-1:, :, :M, :N])
     assert torch.isfinite(outs[0][..., :M, :N]).all()
+
+
+@pytest.mark.parametrize("rows,cols", [(96, 128), (1080, 1920)])
+def test_deblur_slots_equals_per_slot_calls(oracle, api, rows, cols):
+    """cbp_spectral_deblur_slots (frame f uses slot f // frames_per_slot: the multi-camera
+    path) equals one cbp_spectral_deblur_slot call per slot, bit for bit."""
+    t, S, n = 7, 3, 4
+    pubs, prvs = [], []
+    for s in range(S):
+        pair = oracle.generate_coprime_pair(t, 40 + s)
+        lat = api.synth_frames(1 + n, rows, cols, seed=50 + s).view(1 + n, 1, rows, cols)
+        p, q = api.encode_frame(lat, pair.k1, pair.k2)
+        pubs.append(p)
+        prvs.append(q)
+    slots = torch.zeros((S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    rec_p = torch.cat([p[0:1] for p in pubs])
+    rec_q = torch.cat([q[0:1] for q in prvs])
+    api.decode_frames_async(rec_p, rec_q, api.make_cfg(3, 9), torch.zeros_like(rec_p), slots)
+    frames = torch.cat([p[1:] for p in pubs])  # stream-major: S x n frames
+    out = torch.zeros_like(frames)
+    api.spectral_deblur_slots(frames, slots, n, out)
+    ref = torch.zeros_like(frames)
+    for s in range(S):
+        api.spectral_deblur_slot(frames[s * n:(s + 1) * n], slots[s].data_ptr(), ref[s * n:(s + 1) * n])
+    torch.cuda.synchronize()
+    assert all(sl.status == 0 and sl.width == t for sl in api.read_slots(slots, S))
+    M, N = rows, cols
+    assert torch.equal(out[..., :M, :N], ref[..., :M, :N])
+
+
+def test_deblur_slots_small_groups():
+    """The same equality when a launch group holds fewer frames than one slot covers
+    (CBP_GROUP_BUDGET_MB=1: one 1080p frame per group, global slot indices via frame0)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, CBP_GROUP_BUDGET_MB="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", __file__,
+                        "-k", "test_deblur_slots_equals_per_slot_calls"], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

@@ -120,30 +120,77 @@ def c4(trust, B=4):
 
 def c5():
     """64 streams x 1080p gray, epochs of 30 frames: per epoch, one batched recovery of the
-    64 streams' first frames, then 29 x 64 slot deblurs (each stream its own kernel)."""
+    64 streams' first frames, then the 64 x 29 following frames in ONE multi-slot deblur call
+    (cbp_spectral_deblur_slots: frame f uses the kernel of stream f // 29)."""
     S, rows, cols, t, epoch = 64, 1080, 1920, 11, 30
     Mb, Nb = rows + t - 1, cols + t - 1
     rec_pub, rec_prv = make_pairs(S, 1, rows, cols, t, 11, shared_kernel=False)
     frames, _ = make_pairs(8, 1, rows, cols, t, 12)  # deblur inputs (content does not change the work)
+    n = S * (epoch - 1)
+    big = pitched(n, 1, Mb, Nb)  # 1856 distinct frame buffers (15.6 GB), filled from the 8 frames
+    for k in range(0, n, 8):
+        big[k:k + 8].copy_(frames[: min(8, n - k)])
+    out = pitched(n, 1, Mb, Nb)
     out_rec = torch.empty_like(rec_pub)
-    out = pitched(8, 1, Mb, Nb)
     slots = torch.zeros((S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
     cfg = api.make_cfg(9, 25)
 
     def ep():
         api.decode_frames_async(rec_pub, rec_prv, cfg, out_rec, slots)
-        for s in range(S):  # 29 frames of stream s with its kernel, 8 frames per call
-            for f0 in range(0, epoch - 1, 8):
-                n = min(8, epoch - 1 - f0)
-                api.spectral_deblur_slot(frames[:n], slots[s].data_ptr(), out[:n])
+        api.spectral_deblur_slots(big, slots, epoch - 1, out)
 
     ms = timed(ep, 2, warm=1)
     sl = api.read_slots(slots, S)
     ok = sum(1 for s in sl if s.status == 0 and s.width == t)
     fps = S * epoch / (ms / 1e3)
-    return {"config": "c5: 64 streams x 1080p gray, t=11, re-estimated every 30 frames (1 GPU)",
-            "frames_per_s": fps, "ms_per_epoch_64_streams": ms, "streams_recovered": ok,
-            "hbm_roofline_frac": fps * (Mb * Nb + rows * cols) * 4 / HBM}
+    serial = {"config": "c5: 64 streams x 1080p gray, t=11, re-estimated every 30 frames (1 GPU)",
+              "frames_per_s": fps, "ms_per_epoch_64_streams": ms, "streams_recovered": ok,
+              "hbm_roofline_frac": fps * (Mb * Nb + rows * cols) * 4 / HBM}
+
+    # pipelined: the 64 recoveries of epoch e+1 (high-priority stream, own context, other slot
+    # set) run while epoch e deconvolves; steady state, recoveries of epoch 0 before the region
+    from paper_1203_4874_b200 import _native
+    ctx_rec = _native.Context(torch.cuda.current_device())
+    s_rec = torch.cuda.Stream(priority=-1)
+    s_deb = torch.cuda.current_stream()
+    slot2 = torch.zeros((2, S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
+    rec_ev = [torch.cuda.Event() for _ in range(2)]
+    deb_ev = [torch.cuda.Event() for _ in range(2)]
+
+    def rec(e):
+        s_rec.wait_event(deb_ev[e % 2])
+        api.decode_frames_async(rec_pub, rec_prv, cfg, out_rec, slot2[e % 2], ctx=ctx_rec, stream=s_rec)
+        rec_ev[e % 2].record(s_rec)
+
+    def deb(e):
+        s_deb.wait_event(rec_ev[e % 2])
+        api.spectral_deblur_slots(big, slot2[e % 2], epoch - 1, out, stream=s_deb)
+        deb_ev[e % 2].record(s_deb)
+
+    K = 4
+    for w in range(2):  # warm-up
+        rec(w)
+        deb(w)
+    rec(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_deb)
+    s_rec.wait_event(e0)
+    for e in range(K):
+        rec(e + 1)
+        deb(e)
+    done = torch.cuda.Event()
+    done.record(s_rec)
+    s_deb.wait_event(done)
+    e1.record(s_deb)
+    torch.cuda.synchronize()
+    ms_p = e0.elapsed_time(e1) / K
+    fps_p = S * epoch / (ms_p / 1e3)
+    del big, out
+    pipe = {"config": "c5 (pipelined: recoveries of epoch e+1 beside the deconvolution of epoch e)",
+            "frames_per_s": fps_p, "ms_per_epoch_64_streams": ms_p,
+            "hbm_roofline_frac": fps_p * (Mb * Nb + rows * cols) * 4 / HBM}
+    return serial, pipe
 
 
 if __name__ == "__main__":
@@ -151,6 +198,6 @@ if __name__ == "__main__":
     res = [c1(),
            epoch_fps(1, 480, 640, 9, 300, 3, "c2: 640x480 gray, t=9, kernel recovered once, 300 frames", pool=2),
            epoch_fps(3, 1080, 1920, 11, 30, 5, "c3 (serial, one stream): 1080p RGB, t=11, 1 decode + 29 deblur"),
-           c4(True), c4(False), c4(True, 16), c4(False, 16), c5()]
+           c4(True), c4(False), c4(True, 16), c4(False, 16), *c5()]
     for r in res:
         print(json.dumps(r), flush=True)
