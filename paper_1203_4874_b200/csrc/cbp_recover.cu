@@ -2,6 +2,7 @@
 // scale resolution / kernel assembly, validation residual and CBP generation.
 // Every stage keeps the reference's FP64 arithmetic (decoder.cpp, poly.cpp, fft.cpp);
 // inputs are the FP32 frames as stored in HBM.
+#include <climits>
 #include "cbp_linalg.cuh"
 #include <algorithm>
 #include <cstdio>
@@ -686,13 +687,17 @@ __device__ SolveSmem carve_solve(void* base, int t) {
   return sm;
 }
 
-// grid (t_max, 2 axes, batch): slice i of axis `axis` of frame b (decoder.cpp:94-123).
-__global__ void __launch_bounds__(256) k_solve(RecoverArgs a) {
+// grid (t bound, 2 axes, batch): slice i of axis `axis` of frame b (decoder.cpp:94-123), for
+// the frames whose device-side width lies in (t_lo, t_hi]: the launcher buckets widths so a
+// batch of narrow kernels is not launched with the shared memory of the widest allowed one.
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo, int t_hi) {
   extern __shared__ double2 shs[];
   const int i = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
   cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0) return;
   const int t = slot->width;
+  if (t <= t_lo || t > t_hi) return;
   if (t > kSolveMaxWidth) {  // the 2t x 2t Gram and eigenvectors must fit in shared memory
     if (i == 0 && axis == 0 && threadIdx.x == 0)
       slot_fail(slot, CBP_UNSUPPORTED, CBP_STAGE_KERNEL_ESTIMATION_1D, -1, -1, 0.0, CBP_REASON_WIDTH_LIMIT);
@@ -729,15 +734,33 @@ __global__ void __launch_bounds__(256) k_solve(RecoverArgs a) {
     }
 }
 
+// Two width buckets, t <= 16 and t > 16 (an empty bucket's CTAs exit at once). Batches with
+// more problems than one wave of 256-thread CTAs (2 per SM, register bound) use 128-thread
+// CTAs (4 per SM): the eigensolver chain is one warp either way.
 cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
   static bool cfg = false;
   if (!cfg) {
-    cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_solve<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_solve<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cfg = true;
   }
+  static const int nt_env = [] {
+    const char* e = getenv("CBP_SOLVE_THREADS");
+    return e ? atoi(e) : 0;
+  }();
+  constexpr int kSplit = 16;
   const int tc = min(a.t_max, kSolveMaxWidth);
-  dim3 g(tc, 2, a.batch);
-  k_solve<<<g, 256, solve_smem_bytes(tc), s>>>(a);
+  for (int bucket = 0; bucket < 2; ++bucket) {
+    const int lo = bucket ? kSplit : 0, hi = bucket ? INT_MAX : (tc > kSplit ? kSplit : INT_MAX);
+    const int tb = bucket ? tc : min(tc, kSplit);
+    if (bucket && tc <= kSplit) break;
+    dim3 g(tb, 2, a.batch);
+    const int nt = nt_env ? nt_env : (size_t(2) * tb * a.batch > 2 * 148 ? 128 : 256);
+    if (nt == 128)
+      k_solve<128><<<g, 128, solve_smem_bytes(tb), s>>>(a, lo, hi);
+    else
+      k_solve<256><<<g, 256, solve_smem_bytes(tb), s>>>(a, lo, hi);
+  }
   return cudaGetLastError();
 }
 
