@@ -146,7 +146,11 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
     cp_async_commit();  // possibly empty: keeps the group count uniform
   };
   for (int i = 0; i < NS - 1; ++i) issue(i);
+  // negative samples: a running float minimum (C = 1) or a luma compare (C = 3); non-finite
+  // samples: checked once per residue on the Z1 partial (a double sum of finite floats
+  // cannot overflow, so it is non-finite exactly when one of its samples is)
   bool neg = false, bad = false;
+  float mnf = 0.0f;
   double acc = 0.0;
   for (int it = 0; it < steps; ++it) {
     const int r = it / G, g = it - r * G;
@@ -159,18 +163,20 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
     for (int j = 0; j < FT_J; ++j) {
       double v;
       if constexpr (C == 1) {
-        v = double(st[j * FT_W + threadIdx.x]);
+        const float x = st[j * FT_W + threadIdx.x];
+        mnf = fminf(mnf, x);
+        v = double(x);
       } else {  // unfused, as luma_at (bit-identical to the CPU restatement)
         v = __dadd_rn(__dadd_rn(__dmul_rn(0.299, double(st[j * FT_W + threadIdx.x])),
                                 __dmul_rn(0.587, double(st[(FT_J + j) * FT_W + threadIdx.x]))),
                       __dmul_rn(0.114, double(st[(2 * FT_J + j) * FT_W + threadIdx.x])));
         tl[j * FT_W + threadIdx.x] = v;
+        neg |= v < 0.0;
       }
-      neg |= v < 0.0;
-      bad |= !isfinite(v);
       acc += v;
     }
     if (g == G - 1) {  // residue r done
+      bad |= !isfinite(acc);
       if (col_ok) p1[size_t(r) * a.cols] = acc;
       acc = 0.0;
     }
@@ -221,6 +227,7 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
     }
   }
   cp_async_wait<0>();
+  if constexpr (C == 1) neg = mnf < 0.0f;
   neg = __syncthreads_or(neg);
   bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {

@@ -435,10 +435,15 @@ def test_input_errors(api):
     with pytest.raises(api.CbpError) as e:  # decoder.cpp:47
         api.decode_frame(x[:20, :20], x[:20, :20], cfg=api.make_cfg(9, 25))
     assert e.value.code == "FrameTooSmall"
-    y = x.copy(); y[3, 4] = np.nan
-    with pytest.raises(api.CbpError) as e:  # image.cpp:33
-        api.decode_frame(y, y, cfg=api.make_cfg(3, 9))
-    assert e.value.code == "RangeExceeded"
+    for bad in (np.nan, np.inf, -np.inf):  # image.cpp:33, gray and RGB, either stream
+        y = x.copy(); y[3, 4] = bad
+        with pytest.raises(api.CbpError) as e:
+            api.decode_frame(y, y, cfg=api.make_cfg(3, 9))
+        assert e.value.code == "RangeExceeded"
+        y3 = np.stack([x, x, x]); y3[2, 39, 0] = bad
+        with pytest.raises(api.CbpError) as e:
+            api.decode_frame(np.stack([x, x, x]), y3, cfg=api.make_cfg(3, 9))
+        assert e.value.code == "RangeExceeded"
     with pytest.raises(api.CbpError) as e:  # decoder.cpp:26-28
         api.decode_frame(x, x, hint=4, cfg=api.make_cfg(3, 9))
     assert e.value.code == "InvalidArgument"
