@@ -118,9 +118,12 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
   const bool v16 = (a.ld % 4 == 0) && (reinterpret_cast<uintptr_t>(fbase) % 16 == 0);
   const int steps = t * G;
   // step it = (r, g): rows r0 + r + t (FT_J g + j), j < FT_J
+  // step indices advance as counters (r, g) instead of it / G: no integer division per step
+  int ir = 0, ig = 0;  // (r, g) of the next step to issue
   auto issue = [&](int it) {
+    const int r = ir, g = ig;
+    if (++ig == G) ig = 0, ++ir;
     if (it < steps) {
-      const int r = it / G, g = it - r * G;
       float* st = raw + (it % NS) * (C * FT_J * FT_W);
       if (v16) {  // 64 threads per row: 4 rows per pass
 #pragma unroll
@@ -152,8 +155,7 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
   bool neg = false, bad = false;
   float mnf = 0.0f;
   double acc = 0.0;
-  for (int it = 0; it < steps; ++it) {
-    const int r = it / G, g = it - r * G;
+  for (int it = 0, r = 0, g = 0; it < steps; ++it, g = g + 1 == G ? 0 : g + 1, r += g == 0) {
     cp_async_wait<NS - 2>();
     __syncthreads();  // step it's samples visible; every thread is done with step it - 1
     issue(it + NS - 1);  // into the stage step it - 1 used
