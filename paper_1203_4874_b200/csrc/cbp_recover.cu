@@ -119,21 +119,26 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
   const int steps = t * G;
   // step it = (r, g): rows r0 + r + t (FT_J g + j), j < FT_J
   // step indices advance as counters (r, g) instead of it / G: no integer division per step
-  int ir = 0, ig = 0;  // (r, g) of the next step to issue
+  int ir = 0, ig = 0;      // (r, g) of the next step to issue
+  int mbase = r0;          // its first row, r0 + r + t FT_J g
+  // v16: thread copies 16 bytes at column c0 + 4 (tid & 63) of rows j = 4u + (tid >> 6)
+  const int col16 = (threadIdx.x & 63) * 4, row16 = threadIdx.x >> 6;
+  const int bytes16 = min(max((a.cols - c0 - col16) * 4, 0), 16);
+  const float* src16 = fbase + c0 + col16;
   auto issue = [&](int it) {
-    const int r = ir, g = ig;
-    if (++ig == G) ig = 0, ++ir;
+    const int r = ir, g = ig, mb = mbase;
+    if (++ig == G) ig = 0, ++ir, mbase = r0 + ir;
+    else mbase += t * FT_J;
     if (it < steps) {
       float* st = raw + (it % NS) * (C * FT_J * FT_W);
       if (v16) {  // 64 threads per row: 4 rows per pass
 #pragma unroll
         for (int u = 0; u < C * FT_J / 4; ++u) {
-          const int row = u * 4 + (threadIdx.x >> 6), cc = row / FT_J, j = row - cc * FT_J;
-          const int col = (threadIdx.x & 63) * 4;
-          const int m = r0 + r + t * (FT_J * g + j);
-          const int bytes = m < r1 ? min(max((a.cols - c0 - col) * 4, 0), 16) : 0;
-          const float* src = bytes ? fbase + cc * plane + size_t(m) * a.ld + c0 + col : a.pub;
-          cp_async16(st + (cc * FT_J + j) * FT_W + col, src, bytes);
+          const int row = u * 4 + row16, cc = row / FT_J, j = row - cc * FT_J;
+          const int m = mb + t * j;
+          const int bytes = m < r1 ? bytes16 : 0;
+          const float* src = bytes ? src16 + cc * plane + size_t(m) * a.ld : a.pub;
+          cp_async16(st + (cc * FT_J + j) * FT_W + col16, src, bytes);
         }
       } else {
 #pragma unroll
