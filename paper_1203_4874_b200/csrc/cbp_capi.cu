@@ -85,10 +85,12 @@ const short* column_slots(cbp_ctx* ctx, int n, bool bmajor) {
   const int key = -(n + (1 << 24) + (bmajor ? (1 << 25) : 0));  // distinct from the twiddle keys
   auto it = ctx->tw.find(key);
   if (it != ctx->tw.end()) return reinterpret_cast<const short*>(it->second);
-  std::vector<short> h(static_cast<size_t>(n));
+  // [slot of u (n)][u of slot (n)]: the inverse lets the Wiener-table kernel write slots in order
+  std::vector<short> h(2 * static_cast<size_t>(n));
   for (int u = 0; u < n; ++u) {
     const int sl = ct_pos(rad, u);
     h[u] = short(bmajor ? (sl % rad[0]) * (n / rad[0]) + sl / rad[0] : sl);
+    h[n + h[u]] = short(u);
   }
   float2* d = nullptr;
   if (cudaMalloc(&d, h.size() * sizeof(short) + sizeof(float2)) != cudaSuccess) return nullptr;

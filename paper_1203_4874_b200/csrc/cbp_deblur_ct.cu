@@ -602,8 +602,11 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
     Ss[ai * WH_V + vv] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= a.Gr) return;
+  // thread = table slot su (consecutive threads, consecutive addresses); u = the row whose
+  // filter value the column plan expects there (inverse of a.hpos, stored after it)
+  const int su = blockIdx.x * blockDim.x + threadIdx.x;
+  if (su >= a.Gr) return;
+  const int u = a.hpos ? int(a.hpos[a.Gr + su]) : su;
   const double2 wu = zroot(u, a.Gr);
   double2 w = make_double2(1.0, 0.0);
   double2 acc[WH_V];
@@ -617,7 +620,6 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
   // transposed table HT[v][slot(u)]: slot(u) = pos(u) of the column plan (a.hpos), so pass B
   // multiplies element-wise in its DIF output order
-  const int su = a.hpos ? int(a.hpos[u]) : u;
   float2* H = a.H + size_t(f) * a.h_frame + su;
 #pragma unroll
   for (int vv = 0; vv < WH_V; ++vv) {
