@@ -70,7 +70,7 @@ def c1():
             "decode_latency_ms_device": ms, "decode_latency_ms_host_buffers": host}
 
 
-def epoch_fps(ch, rows, cols, t, epoch, seed, label, pool=3):
+def epoch_fps(ch, rows, cols, t, epoch, seed, label, pool=3, pipelined=False):
     """1 decode + (epoch-1) slot deblurs per epoch, epochs cycled from a pool (the bench.py step)."""
     Mb, Nb = rows + t - 1, cols + t - 1
     pubs, prvs = [], []
@@ -94,8 +94,54 @@ def epoch_fps(ch, rows, cols, t, epoch, seed, label, pool=3):
     assert all(s.status == 0 and s.width == t for s in sl), [(s.status, s.width) for s in sl]
     fps = epoch / (ms / 1e3)
     byts = ch * (Mb * Nb + rows * cols) * 4
-    return {"config": label, "frames_per_s": fps, "ms_per_epoch": ms,
-            "hbm_roofline_frac": fps * byts / HBM, "bytes_per_frame": byts}
+    serial = {"config": label, "frames_per_s": fps, "ms_per_epoch": ms,
+              "hbm_roofline_frac": fps * byts / HBM, "bytes_per_frame": byts}
+    if not pipelined:
+        return serial
+    # a stream of such videos: the recovery (decode_frame of frame 0) of epoch e+1 runs on a
+    # high-priority stream with its own context while epoch e deconvolves (bench.py's
+    # schedule with one recovery stream); steady state, epoch 0's recovery before the region
+    NR = int(os.environ.get("PIPE_RECOVERY_STREAMS", "3"))  # recovery streams (one context each): a recovery beside the deconvolution takes ~2x its solo time
+    ctx_recs = [_native.Context(torch.cuda.current_device()) for _ in range(NR)]
+    s_recs = [torch.cuda.Stream(priority=-1) for _ in range(NR)]
+    s_deb = torch.cuda.current_stream()
+    rec_ev = [torch.cuda.Event() for _ in range(pool)]
+    deb_ev = [torch.cuda.Event() for _ in range(pool)]
+    for ev in deb_ev:
+        ev.record(s_deb)
+
+    def rec(e):
+        k, s_rec = e % pool, s_recs[e % NR]
+        s_rec.wait_event(deb_ev[k])  # epoch k's buffers free again
+        api.decode_frames_async(pubs[k][0:1], prvs[k][0:1], cfg, outs[k][0:1], slots[k], ctx=ctx_recs[e % NR],
+                                stream=s_rec)
+        rec_ev[k].record(s_rec)
+
+    def deb(e):
+        k = e % pool
+        s_deb.wait_event(rec_ev[k])
+        api.spectral_deblur_slot(pubs[k][1:], slots[k].data_ptr(), outs[k][1:], stream=s_deb)
+        deb_ev[k].record(s_deb)
+
+    K = 8
+    for w in range(3):  # warm-up, then the first NR recoveries ahead of the region
+        rec(w)
+        deb(w)
+    for w in range(3, 3 + NR):
+        rec(w)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_deb)
+    for e in range(3, 3 + K):
+        rec(e + NR)
+        deb(e)
+    e1.record(s_deb)
+    torch.cuda.synchronize()
+    ms_p = e0.elapsed_time(e1) / K
+    fps_p = epoch / (ms_p / 1e3)
+    pipe = {"config": label.split(":")[0] + " (pipelined: a stream of such videos, recoveries of the next epochs on 3 streams beside the deconvolution of epoch e)",
+            "frames_per_s": fps_p, "ms_per_epoch": ms_p, "hbm_roofline_frac": fps_p * byts / HBM}
+    return serial, pipe
 
 
 def c4(trust, B=4):
@@ -150,8 +196,9 @@ def c5():
     # pipelined: the 64 recoveries of epoch e+1 (high-priority stream, own context, other slot
     # set) run while epoch e deconvolves; steady state, recoveries of epoch 0 before the region
     from paper_1203_4874_b200 import _native
-    ctx_rec = _native.Context(torch.cuda.current_device())
-    s_rec = torch.cuda.Stream(priority=-1)
+    NR = int(os.environ.get("PIPE_RECOVERY_STREAMS", "3"))  # recovery streams (one context each): a recovery beside the deconvolution takes ~2x its solo time
+    ctx_recs = [_native.Context(torch.cuda.current_device()) for _ in range(NR)]
+    s_recs = [torch.cuda.Stream(priority=-1) for _ in range(NR)]
     s_deb = torch.cuda.current_stream()
     slot2 = torch.zeros((2, S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
     rec_ev = [torch.cuda.Event() for _ in range(2)]
@@ -196,7 +243,8 @@ def c5():
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     res = [c1(),
-           epoch_fps(1, 480, 640, 9, 300, 3, "c2: 640x480 gray, t=9, kernel recovered once, 300 frames", pool=2),
+           *epoch_fps(1, 480, 640, 9, 300, 3, "c2: 640x480 gray, t=9, kernel recovered once, 300 frames", pool=6,
+                      pipelined=True),
            epoch_fps(3, 1080, 1920, 11, 30, 5, "c3 (serial, one stream): 1080p RGB, t=11, 1 decode + 29 deblur"),
            c4(True), c4(False), c4(True, 16), c4(False, 16), *c5()]
     for r in res:
