@@ -164,6 +164,50 @@ def c4(trust, B=4):
             "status_codes": sorted({s.status for s in sl}), "hbm_roofline_frac": fps * (2 * Mb * Nb + rows * cols) * 4 / HBM}
 
 
+def c4_streams(trust, B=16, NS=None):
+    """c4 with NS batches in flight on NS streams (one context each): the latency-bound
+    recovery kernels of one batch (cofactor solves, composition: one CTA per problem/frame)
+    overlap the bandwidth-bound kernels of the others."""
+    NS = NS or int(os.environ.get("C4_STREAMS", "3"))
+    rows, cols, t = 2160, 3840, 15
+    sets = [make_pairs(B, 1, rows, cols, t, 7 + 100 * k, shared_kernel=False) for k in range(NS)]
+    outs = [torch.empty_like(p) for p, _ in sets]
+    slots = [torch.zeros((B, api.SLOT_BYTES), dtype=torch.uint8, device="cuda") for _ in range(NS)]
+    ctxs = [_native.Context(torch.cuda.current_device()) for _ in range(NS)]
+    sts = [torch.cuda.Stream() for _ in range(NS)]
+    cfg = api.make_cfg(9, 25, trust_hint=trust)
+    hints = [t] * B if trust else None
+    main = torch.cuda.current_stream()
+
+    def step(reps):
+        ev = torch.cuda.Event()
+        ev.record(main)
+        for k in range(NS):
+            sts[k].wait_event(ev)
+            for _ in range(reps):
+                api.decode_frames_async(sets[k][0], sets[k][1], cfg, outs[k], slots[k], hints=hints, ctx=ctxs[k],
+                                        stream=sts[k])
+            done = torch.cuda.Event()
+            done.record(sts[k])
+            main.wait_event(done)
+
+    step(2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 4
+    e0.record(main)
+    step(reps)
+    e1.record(main)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps  # per round of NS batches
+    ok = sum(sum(s.status == 0 and s.width == t for s in api.read_slots(sl, B)) for sl in slots)
+    Mb, Nb = rows + t - 1, cols + t - 1
+    fps = NS * B / (ms / 1e3)
+    return {"config": f"c4 ({NS} batches of {B} in flight on {NS} streams, {'trusted hint' if trust else 'estimated width'})",
+            "frames_per_s": fps, "ms_per_round": ms, "frames_recovered": ok, "frames": NS * B,
+            "hbm_roofline_frac": fps * (2 * Mb * Nb + rows * cols) * 4 / HBM}
+
+
 def c5():
     """64 streams x 1080p gray, epochs of 30 frames: per epoch, one batched recovery of the
     64 streams' first frames, then the 64 x 29 following frames in ONE multi-slot deblur call
@@ -246,6 +290,6 @@ if __name__ == "__main__":
            *epoch_fps(1, 480, 640, 9, 300, 3, "c2: 640x480 gray, t=9, kernel recovered once, 300 frames", pool=6,
                       pipelined=True),
            epoch_fps(3, 1080, 1920, 11, 30, 5, "c3 (serial, one stream): 1080p RGB, t=11, 1 decode + 29 deblur"),
-           c4(True), c4(False), c4(True, 16), c4(False, 16), *c5()]
+           c4(True), c4(False), c4(True, 16), c4(False, 16), c4_streams(True), c4_streams(False), *c5()]
     for r in res:
         print(json.dumps(r), flush=True)
