@@ -240,9 +240,8 @@ def c5():
     # pipelined: the 64 recoveries of epoch e+1 (high-priority stream, own context, other slot
     # set) run while epoch e deconvolves; steady state, recoveries of epoch 0 before the region
     from paper_1203_4874_b200 import _native
-    NR = int(os.environ.get("PIPE_RECOVERY_STREAMS", "3"))  # recovery streams (one context each): a recovery beside the deconvolution takes ~2x its solo time
-    ctx_recs = [_native.Context(torch.cuda.current_device()) for _ in range(NR)]
-    s_recs = [torch.cuda.Stream(priority=-1) for _ in range(NR)]
+    ctx_rec = _native.Context(torch.cuda.current_device())
+    s_rec = torch.cuda.Stream(priority=-1)
     s_deb = torch.cuda.current_stream()
     slot2 = torch.zeros((2, S, api.SLOT_BYTES), dtype=torch.uint8, device="cuda")
     rec_ev = [torch.cuda.Event() for _ in range(2)]
