@@ -1482,19 +1482,21 @@ __global__ void __launch_bounds__(256, CBP_CONV_OUT == 16 ? 2 : 3) k_conv_resid(
 // l + const in one of them, a conflict-free warp access. CTA = 32 rows x 64 columns, 128
 // threads: the same tiles and partial layout as k_conv_resid, and per output the same FMA
 // order (bit-identical convolution values).
-template <int OUT, int TP>
+// TP taps per kernel column are applied out of a table padded to KS >= TP rows (taps TP..KS-1
+// of the padded table are zero: an odd width t runs with TP = t, skipping them).
+template <int OUT, int TP, int KS = TP>
 __device__ __forceinline__ void conv_col2T(const double* te, const double* to, int twh, const double* kt, int t,
                                            int li0, int l, double* acc0, double* acc1) {
 #pragma unroll
   for (int q = 0; q < OUT; ++q) acc0[q] = acc1[q] = 0.0;
   for (int b = 0; b <= t; ++b) {
     const int c = 2 * l + t - b;  // parity of c = parity of t - b: warp-uniform
-    const double* col = ((c & 1) ? to : te) + (li0 + TP - 1) * twh + (c >> 1);
+    const double* col = ((c & 1) ? to : te) + (li0 + KS - 1) * twh + (c >> 1);
     double v[OUT + TP - 1];
 #pragma unroll
     for (int k = 0; k < OUT + TP - 1; ++k) v[k] = col[(OUT - 1 - k) * twh];
     if (b < t) {
-      const double* kc = kt + b * TP;
+      const double* kc = kt + b * KS;
 #pragma unroll
       for (int j = 0; j < TP; ++j) {
         const double w = kc[j];
@@ -1503,7 +1505,7 @@ __device__ __forceinline__ void conv_col2T(const double* te, const double* to, i
       }
     }
     if (b > 0) {
-      const double* kc = kt + (b - 1) * TP;
+      const double* kc = kt + (b - 1) * KS;
 #pragma unroll
       for (int j = 0; j < TP; ++j) {
         const double w = kc[j];
@@ -1538,9 +1540,17 @@ __device__ __forceinline__ void conv2_dispatch(const double* te, const double* t
                                                int tp, int li0, int l, double* a0, double* a1) {
   switch (tp) {
     case 4: return conv_col2T<8, 4>(te, to, twh, kt, t, li0, l, a0, a1);
-    case 8: return conv_col2T<8, 8>(te, to, twh, kt, t, li0, l, a0, a1);
-    case 12: return conv_col2T<8, 12>(te, to, twh, kt, t, li0, l, a0, a1);
-    case 16: return conv_col2T<8, 16>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 8:
+      if (t == 7) return conv_col2T<8, 7, 8>(te, to, twh, kt, t, li0, l, a0, a1);
+      return conv_col2T<8, 8>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 12:
+      if (t == 11) return conv_col2T<8, 11, 12>(te, to, twh, kt, t, li0, l, a0, a1);
+      if (t == 9) return conv_col2T<8, 9, 12>(te, to, twh, kt, t, li0, l, a0, a1);
+      return conv_col2T<8, 12>(te, to, twh, kt, t, li0, l, a0, a1);
+    case 16:
+      if (t == 15) return conv_col2T<8, 15, 16>(te, to, twh, kt, t, li0, l, a0, a1);
+      if (t == 13) return conv_col2T<8, 13, 16>(te, to, twh, kt, t, li0, l, a0, a1);
+      return conv_col2T<8, 16>(te, to, twh, kt, t, li0, l, a0, a1);
     case 20:
       conv_col1T<8, 20>(te, to, twh, kt, t, li0, 2 * l, a0);
       return conv_col1T<8, 20>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
