@@ -20,6 +20,12 @@
  *    reference's cbp::Error::what() (error.hpp:31-39, decoder.cpp:294-360).
  *  - There is no CPU fallback: without a CUDA device every compute entry point
  *    fails with CBP_CUDA_ERROR.
+ *  - Threading: a context owns its scratch (workspaces, Wiener tables, dynamic-tile
+ *    counters, a pinned staging slot). Use a context from one host thread and one
+ *    stream at a time; work for another stream or thread needs its own context (the
+ *    reference's callers run one decode per host thread, tools/cbp.cpp:141-164). Every
+ *    entry point makes ctx's device current for the call, so contexts of different GPUs
+ *    can be driven from one thread.
  */
 #ifndef CBP_CUDA_H
 #define CBP_CUDA_H
@@ -162,6 +168,11 @@ int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv
                             int channels, int rows, int cols, int ld, const int* width_hints,
                             const cbp_decode_cfg* cfg, float* latent_dev, int ld_out,
                             cbp_kernel_slot* slots_dev, void* stream);
+
+/* Writes the reference's error text for a failed slot (host copy) into buf: the message
+ * decode_frame would throw, "<Errc>: <stage>: <Errc>: <detail>" (decoder.cpp:294-360);
+ * "" for a successful slot. Returns the slot's status. */
+int cbp_slot_message(const cbp_kernel_slot* slot_host, char* buf, int len);
 
 /* Copies `count` slots to host memory (synchronizes the stream). */
 int cbp_read_slots(cbp_ctx* ctx, const cbp_kernel_slot* slots_dev, int count,

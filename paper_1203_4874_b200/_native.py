@@ -83,6 +83,7 @@ _SIGS = {
     "cbp_decode_frames_async": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P]),
     "cbp_decode_frames_async_ev": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P]),
     "cbp_read_slots": (_I, [_P, _P, _I, _P, _P]),
+    "cbp_slot_message": (_I, [_P, C.c_char_p, _I]),
     "cbp_spectral_deblur": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _I, _D, _P, _I, _P]),
     "cbp_spectral_deblur_slot": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P]),
     "cbp_recover_kernels_async": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P]),

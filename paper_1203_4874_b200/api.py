@@ -593,6 +593,14 @@ def read_slots(slots: torch.Tensor, count: int) -> list:
     return [host[i] for i in range(count)]
 
 
+def slot_message(slot) -> str:
+    """The reference's error text for a failed slot (cbp_slot_message): what decode_frame
+    throws for that frame, "<Errc>: <stage>: <Errc>: <detail>"; "" for a good slot."""
+    buf = C.create_string_buffer(512)
+    N.lib().cbp_slot_message(C.byref(slot), buf, 512)
+    return buf.value.decode()
+
+
 def set_sm_reserve(sms: int, ctx: N.Context | None = None, device: int | None = None):
     """cbp_set_sm_reserve: SMs the deconvolution passes of this context leave to other streams."""
     ctx = ctx or context(device)

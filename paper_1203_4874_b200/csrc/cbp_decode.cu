@@ -72,6 +72,21 @@ std::string full_message(const cbp_kernel_slot& s) {
   return inner;
 }
 
+}  // namespace
+
+// The reference's error text for a failed slot (what decode_frame would throw), for
+// pipelines that read slots instead of cbp_decode_info.
+extern "C" int cbp_slot_message(const cbp_kernel_slot* slot, char* buf, int len) {
+  if (!slot) return CBP_INVALID_ARGUMENT;
+  if (buf && len > 0) {
+    const std::string m = slot->status == 0 ? std::string() : full_message(*slot);
+    std::snprintf(buf, size_t(len), "%s", m.c_str());
+  }
+  return slot->status;
+}
+
+namespace {
+
 int check_search(cbp_ctx* ctx, int smin, int smax) {  // decoder.cpp:31-34
   if (!(smin >= 3 && smax <= 63 && smin <= smax && smin % 2 == 1 && smax % 2 == 1))
     return set_error(ctx, CBP_INVALID_ARGUMENT, "width search range must be odd values within [3,63]");
