@@ -1,35 +1,44 @@
 #!/usr/bin/env python
 """CBP decryption benchmark on B200 (BASELINE.json metric: frames/sec @1080p).
 
-Workload (BASELINE.json configs[2], the 1080p config the metric is quoted on):
-1920x1080 RGB latents, coprime 11x11 kernel pairs, kernel re-estimated every 30 frames.
-One *step* = one 30-frame kernel epoch: decode_frame on frame 0 (luma width search
-9..25, tau 1e-6, default epsilon, validation on: the reference decoder defaults,
-decoder.hpp:10-20) followed by spectral_deblur of all 3 planes of frames 1..29 with the
-recovered kernel, which stays on the device (cbp_kernel_slot).
+Workloads (BASELINE.json configs):
+  c3 (default; configs[2], the config the metric is quoted on): 1920x1080 RGB latents,
+     coprime 11x11 kernel pairs, kernel re-estimated every 30 frames. One *step* = one
+     30-frame kernel epoch: decode_frame on frame 0 (luma width search 9..25, tau 1e-6,
+     default epsilon, validation on: the reference decoder defaults, decoder.hpp:10-20)
+     followed by spectral_deblur of all 3 planes of frames 1..29 with the recovered kernel,
+     which stays on the device (cbp_kernel_slot). Schedule: paper_1203_4874_b200/pipeline.py.
+  c5 (--workload c5; configs[4]): 64 independent 1080p gray streams, t = 11, epochs of 30
+     frames; stream s runs on GPU s mod G. One step = one epoch of every stream of the rank:
+     one batched recovery of the streams' recovery frames + ONE multi-slot deconvolution
+     (cbp_spectral_deblur_slots) of their 29 following frames each; the recoveries of epoch
+     e+1 run on a high-priority stream beside the deconvolution of epoch e.
 
 Inputs: synthetic U[0,1) latents generated on the device, blurred on the device by
-cbp_encode_frames with pairs from cbp_generate_coprime_pair (reference-exact host
-draw). A pool of --pool epochs (default 5: 150 frames, 3.8 GB of public frames) is cycled, so every
-step reads inputs far larger than the 126 MB L2.
+cbp_encode_frames with pairs from cbp_generate_coprime_pair (reference-exact host draw).
+Every step reads inputs far larger than the 126 MB L2 (pool of distinct epochs).
 
 Arms:
   default          the B200 path (libcbp_cuda.so via the C ABI), device-resident inputs
                    (`value`), plus the same metric through the host-buffer C ABI call
-                   cbp_decode_run_host with pinned host memory (`e2e`).
+                   cbp_decode_run_host with pinned host memory (`e2e`, c3).
   --impl reference the reference's CPU implementation of the path: the FP64 oracle
-                   restatement (oracle/, the reference itself cannot be built here:
+                   restatement (oracle/; the reference itself cannot be built here:
                    Eigen3/FFTW3 absent) on all host threads, frames in parallel like
                    `cbp decode` (tools/cbp.cpp:141-164).
 
-Multi-GPU (torchrun): each rank decodes its own epochs (frames/streams are independent,
-no collective on the data path); value = all frames / max-over-ranks time.
+Multi-GPU: one process per GPU. `--gpus N` without a torchrun environment re-launches
+itself under torch.distributed.run with N ranks (127.0.0.1). Every rank decodes its own
+epochs / streams (no collective on the data path); value = all frames / max-over-ranks time.
+`--dry-run` exercises the launch path, sharding and max-over-ranks reduction on CPU (gloo),
+with no GPU work (used by tests/test_multirank.py).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,23 +51,47 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "CBP decrypt frames/sec @1080p (1/2/4/8 B200); HBM GB/s % of peak; vs CPU ref"
-ROWS, COLS, CH, T = 1080, 1920, 3, 11
+ROWS, COLS, T = 1080, 1920, 11
 EPOCH = 30
+STREAMS = 64
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
-    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--gpus", type=int, default=None, help="GPUs (ranks); default: WORLD_SIZE or 1")
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--pool", type=int, default=5, help="distinct epochs cycled by the steps (>= recovery streams + 2)")
+    p.add_argument("--workload", default="c3", choices=["c3", "c5"])
+    p.add_argument("--pool", type=int, default=5, help="c3: distinct epochs cycled by the steps (>= recovery streams + 2)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile-steps", type=int, default=3)
     p.add_argument("--cpu-threads", type=int, default=0)
-    return p.parse_args()
+    p.add_argument("--dry-run", action="store_true", help="launch path + sharding on CPU, no GPU work")
+    return p.parse_args(argv)
+
+
+def channels_of(workload: str) -> int:
+    return 3 if workload == "c3" else 1
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` dict both arms print (identical keys and values)."""
+    ch = channels_of(args.workload)
+    if args.workload == "c3":
+        wl = ("c3: 1920x1080 RGB, t=11, kernel re-estimated every 30 frames "
+              "(1 decode_frame + 29 spectral_deblur per step)")
+        fps = EPOCH
+    else:
+        wl = (f"c5: {STREAMS} independent 1080p gray streams, t=11, re-estimated every 30 frames; stream s on "
+              f"GPU s mod G (one step = one epoch of every stream of the rank)")
+        fps = EPOCH * STREAMS
+    return {"workload": wl, "rows": ROWS, "cols": COLS, "channels": ch, "kernel_width": T,
+            "frames_per_step": fps, "decode_cfg": "search 9..25, tau 1e-6, default epsilon, validate=true",
+            "l2": "inputs larger than L2 (distinct frames every step)",
+            "parallelism": f"{world} independent rank(s), no data-path collective"}
 
 
 # ------------------------------------------------------------------ helpers
@@ -66,8 +99,8 @@ def peaks():
     path = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -120,18 +153,34 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup():
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(n: int) -> int:
+    """Re-run this command under torch.distributed.run with n ranks on this node (the
+    driver's own N>1 launch line), rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def dist_setup(dry_run: bool = False):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    gpu = torch.cuda.is_available() and not dry_run
     if world > 1:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if torch.cuda.is_available():
+        if gpu:
             torch.cuda.set_device(local)
-        dist.init_process_group(backend, init_method="env://")
-    elif torch.cuda.is_available():
+        dist.init_process_group("nccl" if gpu else "gloo", init_method="env://")
+    elif gpu:
         torch.cuda.set_device(local)
     return world, rank, local
 
@@ -164,12 +213,19 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def base_line(args, world, value, ms_per_step, config, dtype):
+    return {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "c5" else "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config}
+
+
 # ------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(pub32: np.ndarray, prv32: np.ndarray, kernel: np.ndarray, eps: float, threads: int,
                          n_frames: int):
     """Times the FP64 oracle (the reference restatement) on n_frames of one epoch with
     `threads` workers: frame 0 recovers the kernel (decode_frame), the rest reuse it
-    (spectral_deblur of every plane). Returns frames/second."""
+    (spectral_deblur of every plane). Returns (frames/second, seconds)."""
     from oracle import oracle as O
     rec = np.zeros(n_frames, np.int32)
     rec[0] = 1
@@ -178,17 +234,35 @@ def cpu_reference_sample(pub32: np.ndarray, prv32: np.ndarray, kernel: np.ndarra
     return n_frames / secs, secs
 
 
+def cpu_stage_row(pub: np.ndarray, prv: np.ndarray) -> dict:
+    """Single-worker oracle decode_frame of one recovery frame, per-stage milliseconds in
+    the reference's bench_csv schema (bench.cpp:55-68; run_bench decodes with validate=false)."""
+    from oracle import oracle as O
+    cfg = O.make_cfg(9, 25, 1e-6, validate=False)
+    O.decode_frame(pub, prv, cfg=cfg)  # warm-up (bench.cpp:34)
+    d = O.decode_frame(pub, prv, cfg=cfg)
+    return stage_csv_row(d.width_used, d.stage_ms)
+
+
+STAGE_SCHEMA = ("kernel_width,polynomial_evaluation_ms,kernel_degree_estimation_ms,"
+                "kernel_estimation_1d_ms,kernel_estimation_2d_fft_ms,total_ms")
+
+
+def stage_csv_row(t, ms) -> str:
+    return f"{t}," + ",".join(f"{x:.3f}" for x in list(ms)[:5])
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU path (oracle port) on the box's host cores."""
     if rank != 0:
         return
     from oracle import oracle as O
     threads = args.cpu_threads or os.cpu_count() or 1
-    n = EPOCH  # one step = one whole epoch, the same frame mix as the GPU arm's step
-    # identical synthetic workload shape: 1080p RGB, t = 11, epoch of 30 frames
+    ch = channels_of(args.workload)
+    n = EPOCH  # one step = one whole (stream) epoch: 1 decode_frame + 29 spectral_deblur
     pair = O.generate_coprime_pair(T, O.frame_seed(2, 0))
-    lat = np.stack([O.random_frame(ROWS, COLS, CH, O.frame_seed(1, i)) for i in range(n)])
-    pub = np.empty((n, CH, ROWS + T - 1, COLS + T - 1), np.float32)
+    lat = np.stack([O.random_frame(ROWS, COLS, ch, O.frame_seed(1, i)) for i in range(n)])
+    pub = np.empty((n, ch, ROWS + T - 1, COLS + T - 1), np.float32)
     prv = np.empty_like(pub)
     for i in range(n):
         a, b = O.encode_frame(lat[i], pair.k1, pair.k2)
@@ -197,20 +271,38 @@ def run_reference(args, world, rank):
         cpu_reference_sample(pub, prv, pair.k1, 1e-8, threads, n)
     times = []
     for _ in range(args.steps):
-        fps, secs = cpu_reference_sample(pub, prv, pair.k1, 1e-8, threads, n)
-        times.append(secs)
+        times.append(cpu_reference_sample(pub, prv, pair.k1, 1e-8, threads, n)[1])
     value = n * len(times) / sum(times)
-    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "c3: 1920x1080 RGB, t=11, kernel re-estimated every 30 frames",
-                       "rows": ROWS, "cols": COLS, "channels": CH, "kernel_width": T,
-                       "parallelism": f"{threads} host threads, frames in parallel (tools/cbp.cpp:141-164)"},
-            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "sample": f"{n} frames of one epoch per step (1 decode_frame + {n - 1} spectral_deblur)"},
-            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    cfg = workload_config(args, world)
+    line = base_line(args, world, value, 1000 * sum(times) / len(times) * (cfg["frames_per_step"] / n), cfg, "f64")
+    line.update({"impl": "reference",
+                 "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
+                                  "sample": f"{n} frames of one {'RGB' if ch == 3 else 'gray'} 1080p epoch per "
+                                            f"timed step (1 decode_frame + {n - 1} spectral_deblur), frames in "
+                                            f"parallel on {threads} threads (tools/cbp.cpp:141-164)"},
+                 "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "stages": {"schema": STAGE_SCHEMA,
+                            "cpu_1worker": cpu_stage_row(pub[0].astype(np.float64), prv[0].astype(np.float64))}})
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- dry run (CPU)
+def run_dry(args, world, rank):
+    """The launch path without GPU work: every rank takes its shard (c5 streams s mod G, or
+    its own c3 epochs), times a token CPU workload per step, and rank 0 prints the line with
+    the max-over-ranks time."""
+    mine = streams_for_rank(STREAMS, world, rank) if args.workload == "c5" else [epoch_seed(0, rank)]
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        np.fft.rfft2(np.ones((64, 64)))
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    cfg = workload_config(args, world)
+    frames = cfg["frames_per_step"] * args.steps * (world if args.workload == "c3" else 1)
+    if rank == 0:
+        line = base_line(args, world, frames / dt, 1000 * dt / args.steps, cfg, "none")
+        line.update({"dry_run": True, "shard_rank0": mine})
+        print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------- B200 arm
@@ -218,21 +310,69 @@ SM_RESERVE = int(os.environ.get("CBP_BENCH_SM_RESERVE", "12"))
 REC_STREAMS = int(os.environ.get("CBP_BENCH_REC_STREAMS", "3"))  # recoveries in flight
 
 
-def run_b200(args, world, rank, local):
+def pitched(shape, dev, fill=None):
+    """float32 planes whose rows are padded to 16 bytes (like cudaMallocPitch): vector copies."""
+    import torch
+    cols = shape[-1]
+    full = (*shape[:-1], (cols + 3) // 4 * 4)
+    x = torch.empty(full, dtype=torch.float32, device=dev) if fill is None else \
+        torch.full(full, fill, dtype=torch.float32, device=dev)
+    return x[..., :cols]
+
+
+def deblur_roofline(api, run, planes_hint, ch, local, steps):
+    """Roofline of the dominant kernel group (deconvolution passes A+B+C), from CUDA events
+    recorded around each pass on its own stream (cbp_profile) over `steps` runs of `run`."""
+    import torch
+    api.profile(True, local)
+    torch.cuda.synchronize()
+    run(steps)
+    torch.cuda.synchronize()
+    pass_ms, planes, groups = api.profile_read(local)
+    api.profile(False, local)
+    Mb, Nb = ROWS + T - 1, COLS + T - 1
+    deblur_ms = sum(pass_ms)
+    bytes_per_plane = (Mb * Nb + ROWS * COLS) * 4  # compulsory: blurred plane in, latent plane out
+    achieved = bytes_per_plane * planes / (deblur_ms / 1000.0) / 1e9
+    peak, peak_kind = peaks()
+    # nominal FP32 flops per plane (SURVEY.md 8(d)): 5 G log2 G + 10 Gr (Gc/2+1)
+    Gr, Gc = 1120, 1944
+    G = Gr * Gc
+    flops_plane = 5 * G * np.log2(G) + 10 * Gr * (Gc // 2 + 1)
+    fp32_peak = 148 * 128 * 2 * 1.965e9  # 148 SMs x 128 FP32 lanes x FMA x max SM clock
+    fp32_rate = flops_plane * planes / (deblur_ms / 1000.0)
+    prof = {}
+    tp = os.path.join(HERE, "profiles", "deblur_traffic.json")
+    if os.path.exists(tp):
+        try:
+            prof = json.load(open(tp))
+        except Exception:
+            prof = {}
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": prof.get("dram_bytes_per_plane"), "peak_kind": peak_kind,
+            "kernel": "deconvolution passes A+B+C (k_rows_forward_ct, k_cols_filter_bulk, k_rows_inverse_ct)",
+            "algorithmic_bytes_per_plane": bytes_per_plane, "planes": planes, "launch_groups": groups,
+            "pass_ms_per_plane": [m / max(planes, 1) for m in pass_ms],
+            "fp32_frac": fp32_rate / fp32_peak,
+            "fp32_note": "nominal FFT flops (5 G log2 G + 10 Gr Hc per plane) / live pass time / "
+                         "(148 SMs x 128 lanes x 2 x 1.965 GHz)",
+            "fma_pipe_frac_ncu": prof.get("fma_pipe_active_frac"),
+            "traffic_source": prof.get("source")}
+
+
+def run_c3(args, world, rank, local):
     import torch
     from paper_1203_4874_b200 import api
+    from paper_1203_4874_b200.pipeline import VideoPipeline
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream(dev)
+    CH = 3
     Mb, Nb = ROWS + T - 1, COLS + T - 1
-    M, Nn = ROWS, COLS
     E = max(1, args.pool)
     # ---- inputs: device-generated latents, device encode (untimed)
-    # device frames use a 16-byte row pitch (like cudaMallocPitch): vector copies in pass A
-    NbP = (Nb + 3) // 4 * 4
-    pub = torch.empty((E, EPOCH, CH, Mb, NbP), dtype=torch.float32, device=dev)[..., :Nb]
-    prv = torch.empty((E, 1, CH, Mb, NbP), dtype=torch.float32, device=dev)[..., :Nb]
+    pub = pitched((E, EPOCH, CH, Mb, Nb), dev)
+    prv = pitched((E, 1, CH, Mb, Nb), dev)
     pairs = []
     for e in range(E):
         pair = api.generate_coprime_pair(T, api.frame_seed(2, epoch_seed(e, rank)))
@@ -243,91 +383,15 @@ def run_b200(args, world, rank, local):
         pub[e].copy_(p)
         prv[e, 0].copy_(q[0])
         del lat, p, q
-    out = torch.empty((E, EPOCH, CH, Mb, NbP), dtype=torch.float32, device=dev)[..., :Nb]
+    out = pitched((E, EPOCH, CH, Mb, Nb), dev)
     slots = torch.zeros((E, api.SLOT_BYTES), dtype=torch.uint8, device=dev)
     cfg = api.make_cfg(9, 25, 1e-6, validate=True)
     torch.cuda.synchronize(dev)
-
-    # Recovery (decode_frame on frame 0) of the next epochs runs on recovery streams (one
-    # context each: separate workspaces) while epoch s deconvolves: the recovery kernels are
-    # latency bound on few SMs, the deconvolution passes fill the GPU. Epochs are
-    # independent (slots/outputs are per epoch). An epoch's buffers are reused only after
-    # its previous deconvolution finished (deb_ev).
-    from paper_1203_4874_b200 import _native
-    # The recovery chains have the higher priority and the deconvolution's persistent
-    # grids leave them SM_RESERVE SMs' worth of slots.
-    ctx_rec = [_native.Context(local) for _ in range(REC_STREAMS)]
-    s_rec = [torch.cuda.Stream(dev, priority=-1) for _ in range(REC_STREAMS)]
-    api.set_sm_reserve(SM_RESERVE, device=local)
-    s_deb = torch.cuda.current_stream(dev)
-    dec_ev = [torch.cuda.Event() for _ in range(E)]
-    deb_ev = [torch.cuda.Event() for _ in range(E)]
-    if E < REC_STREAMS + 2:
-        raise ValueError(f"--pool must be >= {REC_STREAMS + 2} for the pipelined step")
-
-    def issue_decode(s):
-        # dec_ev[e] after the whole recovery frame (validation included): measured on B200,
-        # releasing the deconvolution at slot-ready (decode_frames_async(slot_ready=...))
-        # overlaps the FP64 validation with it and costs ~13% of throughput
-        e, r = s % E, s % REC_STREAMS
-        s_rec[r].wait_event(deb_ev[e])  # the epoch's previous deconvolution read its slot
-        api.decode_frames_async(pub[e, 0:1], prv[e], cfg, out[e, 0:1], slots[e], ctx=ctx_rec[r], stream=s_rec[r])
-        dec_ev[e].record(s_rec[r])
-
-    def issue_deblur(s):
-        e = s % E
-        s_deb.wait_event(dec_ev[e])
-        api.spectral_deblur_slot(pub[e, 1:], slots[e].data_ptr(), out[e, 1:], stream=s_deb)
-        deb_ev[e].record(s_deb)
-
-    def run_steps(n, start=0):
-        """n pipelined steps: recoveries run REC_STREAMS epochs ahead of the deconvolution."""
-        for s in range(start, start + min(REC_STREAMS, n)):
-            issue_decode(s)
-        for s in range(start, start + n):
-            if s + REC_STREAMS < start + n:
-                issue_decode(s + REC_STREAMS)
-            issue_deblur(s)
-        for st in s_rec:
-            done = torch.cuda.Event()
-            done.record(st)
-            s_deb.wait_event(done)
-
-    def step(s):
-        run_steps(1, s)
-
-    def count_launches():
-        return api.launch_count(local) + sum(int(_native.lib().cbp_launch_count(c.ptr)) for c in ctx_rec)
-
-    def run_steady(n, start=0):
-        """n steps of the running pipeline: the recoveries of epochs start..start+REC_STREAMS-1
-        are issued and finished BEFORE the timed region (pipeline pre-roll, untimed); inside it
-        every step issues one recovery (REC_STREAMS epochs ahead) and one deconvolution batch,
-        so the region holds exactly n recoveries + n x 29 deblurs, in steady state (no fill
-        stall while the first recovery runs alone). Returns (ev0, ev1) around the region."""
-        for s in range(start, start + REC_STREAMS):
-            issue_decode(s)
-        torch.cuda.synchronize(dev)
-        barrier(world)
-        torch.cuda.synchronize(dev)
-        l0 = count_launches()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for st in s_rec:
-            st.wait_event(e0)
-        for s in range(start, start + n):
-            issue_decode(s + REC_STREAMS)
-            issue_deblur(s)
-        for st in s_rec:
-            done = torch.cuda.Event()
-            done.record(st)
-            s_deb.wait_event(done)
-        e1.record(stream)
-        return e0, e1, count_launches() - l0
+    pipe = VideoPipeline(pub, prv, out, slots, cfg, rec_streams=REC_STREAMS, sm_reserve=SM_RESERVE, device=local)
 
     # ---- correctness guard on the pool (every epoch recovers its own kernel)
     for s in range(E):
-        step(s)
+        pipe.run_steps(1, s)
     torch.cuda.synchronize(dev)
     for e, sl in enumerate(api.read_slots(slots, E)):
         if sl.status != 0 or sl.width != T:
@@ -340,17 +404,27 @@ def run_b200(args, world, rank, local):
     sampler = ClockSampler(local)
     sampler.start()
     for s in range(args.warmup):
-        step(s)
+        pipe.run_steps(1, s)
     # keep the GPU busy >= 0.3 s before the timed region so clocks are sampled under load
     t_end = time.time() + 0.3
     s = 0
     while time.time() < t_end:
-        step(s)
+        pipe.run_steps(1, s)
         s += 1
         if s % 8 == 0:
             torch.cuda.synchronize(dev)
     torch.cuda.synchronize(dev)
-    ev0, ev1, launches = run_steady(args.steps)
+    # steady state: the recoveries of the first REC_STREAMS epochs run before the region
+    pipe.preroll(0)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    l0 = pipe.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(pipe.s_deb)
+    pipe.steady(args.steps, 0, start_event=ev0)
+    ev1.record(pipe.s_deb)
+    launches = pipe.launch_count() - l0
     torch.cuda.synchronize(dev)
     barrier(world)
     ms_rank = ev0.elapsed_time(ev1)
@@ -359,36 +433,37 @@ def run_b200(args, world, rank, local):
     frames = EPOCH * args.steps * world
     value = frames / (ms / 1000.0)
 
-    # ---- roofline of the dominant kernel group (deconvolution passes A+B+C)
-    api.profile(True, local)
-    torch.cuda.synchronize(dev)
-    pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    pe0.record(stream)
-    for st in s_rec:
-        st.wait_event(pe0)
-    run_steps(args.profile_steps)
-    pe1.record(stream)
-    torch.cuda.synchronize(dev)
-    pass_ms, planes, groups = api.profile_read(local)
-    api.profile(False, local)
-    prof_step_ms = pe0.elapsed_time(pe1) / max(args.profile_steps, 1)
-    deblur_ms = sum(pass_ms)
-    bytes_per_plane = (Mb * Nb + M * Nn) * 4  # compulsory: blurred plane in, latent plane out
-    achieved = bytes_per_plane * planes / (deblur_ms / 1000.0) / 1e9
-    peak, peak_kind = peaks()
-    traffic = None
-    tp = os.path.join(HERE, "profiles", "deblur_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_plane")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "deconvolution passes A+B+C (k_rows_forward, k_cols_filter, k_rows_inverse)",
-                "algorithmic_bytes_per_plane": bytes_per_plane, "planes": planes,
-                "pass_ms_per_plane": [m / max(planes, 1) for m in pass_ms],
-                "share_of_step": deblur_ms / max(args.profile_steps, 1) / prof_step_ms}
+    # ---- latents of the last timed epoch against the slot kernels (cheap guard): finite
+    if not torch.isfinite(out[(args.steps - 1) % E, :, :, :ROWS, :COLS]).all():
+        raise RuntimeError("non-finite latents in the timed region")
+
+    # ---- roofline of the dominant kernel group, live CUDA events over profile steps
+    pe = {}
+
+    def prof_run(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_deb)
+        for st in pipe.s_rec:
+            st.wait_event(e0)
+        pipe.run_steps(n)
+        e1.record(pipe.s_deb)
+        pe["ev"] = (e0, e1)
+
+    roofline = deblur_roofline(api, prof_run, None, CH, local, args.profile_steps)
+    roofline["share_of_step"] = sum(roofline["pass_ms_per_plane"]) * roofline["planes"] / max(
+        pe["ev"][0].elapsed_time(pe["ev"][1]), 1e-9)
+
+    # ---- per-stage split of one recovery frame (bench_csv schema, bench.cpp:55-68):
+    # GPU stage CUDA events of decode_frame with validate=false, like run_bench
+    d = api.decode_frames(pub[0, 0:1], prv[0], cfg=api.make_cfg(9, 25, 1e-6, validate=False))[0]
+    d = api.decode_frames(pub[0, 0:1], prv[0], cfg=api.make_cfg(9, 25, 1e-6, validate=False))[0]
+    st = d.stage_timings
+    stages = {"schema": STAGE_SCHEMA,
+              "gpu": stage_csv_row(d.width_used, [st.polynomial_evaluation_ms, st.kernel_degree_estimation_ms,
+                                                  st.kernel_estimation_1d_ms, st.kernel_estimation_2d_fft_ms,
+                                                  st.total_ms]),
+              "frame": "one 1080p RGB recovery frame (c3), decode_frame validate=false"}
+    pipe.close()
 
     # ---- end-to-end through the host-buffer C ABI call (pinned host memory)
     e2e = None
@@ -412,8 +487,10 @@ def run_b200(args, world, rank, local):
         barrier(world)
         e2e_s = max_over_ranks(t1 - t0, world)
         frame_bytes = CH * Mb * Nb * 4
+        # D2H: the top-left (Mb - tmin + 1) x (Nb - tmin + 1) of each plane, tmin = search_min
+        crop_bytes = CH * (Mb - 9 + 1) * (Nb - 9 + 1) * 4
         e2e = {"value": EPOCH * nE * world / e2e_s, "unit": "frames/s",
-               "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * frame_bytes,
+               "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * crop_bytes,
                "steps": nE, "host_memory": "pinned",
                "api": f"cbp_decode_run_host (C ABI, host buffers, H2D/compute/D2H overlapped): one run of "
                       f"{nE} epochs = {EPOCH * nE} frames, a recovery frame every {EPOCH}"}
@@ -425,8 +502,6 @@ def run_b200(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or os.cpu_count() or 1
-        # one whole epoch (the step's own frame mix: 1 decode_frame + 29 spectral_deblur),
-        # repeated until >= 10 s of CPU work (bounded at 6 repetitions)
         n = EPOCH
         pub_h = pub[0, :n].contiguous().cpu().numpy()
         prv_h = np.zeros_like(pub_h)
@@ -439,35 +514,145 @@ def run_b200(args, world, rank, local):
         cpu = {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": f"{reps} x one 1080p RGB epoch of {n} frames (1 decode_frame + {n - 1} spectral_deblur), "
                          f"{secs:.1f} s, FP64 oracle restatement (Eigen/FFTW reference unbuildable here)"}
+        stages["cpu_1worker"] = cpu_stage_row(pub_h[0].astype(np.float64), prv_h[0].astype(np.float64))
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": "c3: 1920x1080 RGB, t=11, kernel re-estimated every 30 frames "
-                                       "(1 decode_frame + 29 spectral_deblur per step)",
-                           "rows": ROWS, "cols": COLS, "channels": CH, "kernel_width": T,
-                           "frames_per_step": EPOCH, "pool_epochs": E,
-                           "schedule": f"recoveries of epochs s+1..s+{REC_STREAMS} overlapped with deconvolution of epoch s "
-                                       f"({REC_STREAMS} high-priority recovery streams + 1 deconvolution stream; "
-                                       f"deconvolution leaves {SM_RESERVE} SMs); steady state: the recoveries of "
-                                       f"the first {REC_STREAMS} epochs run before the timed region, each timed step "
-                                       f"issues 1 recovery ({REC_STREAMS} epochs ahead) + 29 deblurs",
-                           "l2": "inputs larger than L2 (each step reads 0.76 GB of distinct frames)",
-                           "decode_cfg": "search 9..25, tau 1e-6, default epsilon, validate=true",
-                           "parallelism": f"{world} independent GPU(s), no data-path collective"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "precision": "FP32 storage and deconvolution FFT; FP64 sampling and solves"}
+        line = base_line(args, world, value, ms / args.steps, workload_config(args, world), "f32")
+        line.update({"roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                     "clocks": clocks, "stages": stages,
+                     "schedule": f"recoveries of epochs s+1..s+{REC_STREAMS} overlapped with the deconvolution of "
+                                 f"epoch s ({REC_STREAMS} high-priority recovery streams + 1 deconvolution stream "
+                                 f"leaving {SM_RESERVE} SMs; pool of {E} epochs); steady state: the first "
+                                 f"{REC_STREAMS} recoveries run before the timed region, each timed step issues 1 "
+                                 f"recovery + 29 deblurs",
+                     "precision": "FP32 storage and deconvolution FFT; FP64 sampling, solves and validation"})
+        print(json.dumps(line), flush=True)
+
+
+def run_c5(args, world, rank, local):
+    """c5: this rank's streams (s mod G), epochs of 30 frames, recoveries of epoch e+1 beside
+    the deconvolution of epoch e."""
+    import torch
+    from paper_1203_4874_b200 import _native, api
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    mine = streams_for_rank(STREAMS, world, rank)
+    S = len(mine)
+    Mb, Nb = ROWS + T - 1, COLS + T - 1
+    n = S * (EPOCH - 1)
+    # recovery pairs: 2 epochs x S streams (per-stream kernels, per-epoch draws)
+    rec_pub = pitched((2, S, 1, Mb, Nb), dev)
+    rec_prv = pitched((2, S, 1, Mb, Nb), dev)
+    frames = pitched((n, 1, Mb, Nb), dev)  # the streams' following frames, stream-major
+    for e in range(2):
+        for j, s in enumerate(mine):
+            pair = api.generate_coprime_pair(T, api.frame_seed(2, 100000 * e + s))
+            lat = api.synth_frames(1 if e else EPOCH, ROWS, COLS, seed=api.frame_seed(1, 100000 * e + s))
+            p, q = api.encode_frame(lat.view(-1, 1, ROWS, COLS), pair.k1, pair.k2)
+            rec_pub[e, j].copy_(p[0])
+            rec_prv[e, j].copy_(q[0])
+            if e == 0:
+                frames[j * (EPOCH - 1):(j + 1) * (EPOCH - 1)].copy_(p[1:])
+            del lat, p, q
+    out = pitched((n, 1, Mb, Nb), dev)
+    out_rec = pitched((2, S, 1, Mb, Nb), dev)
+    slots = torch.zeros((2, S, api.SLOT_BYTES), dtype=torch.uint8, device=dev)
+    cfg = api.make_cfg(9, 25, 1e-6, validate=True)
+    ctx_rec = _native.Context(local)
+    s_rec = torch.cuda.Stream(dev, priority=-1)
+    s_deb = torch.cuda.current_stream(dev)
+    api.set_sm_reserve(SM_RESERVE, device=local)
+    rec_ev = [torch.cuda.Event() for _ in range(2)]
+    deb_ev = [torch.cuda.Event() for _ in range(2)]
+    for ev in deb_ev:
+        ev.record(s_deb)
+
+    def rec(e):
+        k = e % 2
+        s_rec.wait_event(deb_ev[k])
+        api.decode_frames_async(rec_pub[k], rec_prv[k], cfg, out_rec[k], slots[k], ctx=ctx_rec, stream=s_rec)
+        rec_ev[k].record(s_rec)
+
+    def deb(e):
+        k = e % 2
+        s_deb.wait_event(rec_ev[k])
+        api.spectral_deblur_slots(frames, slots[k], EPOCH - 1, out, stream=s_deb)
+        deb_ev[k].record(s_deb)
+
+    def join():
+        done = torch.cuda.Event()
+        done.record(s_rec)
+        s_deb.wait_event(done)
+
+    def count():
+        return api.launch_count(local) + int(_native.lib().cbp_launch_count(ctx_rec.ptr))
+
+    rec(0)
+    deb(0)
+    join()
+    torch.cuda.synchronize(dev)
+    ok = sum(1 for e in range(1) for x in api.read_slots(slots[e], S) if x.status == 0 and x.width == T)
+    sampler = ClockSampler(local)
+    sampler.start()
+    for w in range(args.warmup):
+        rec(w)
+        deb(w)
+    rec(0)  # steady state: epoch 0's recoveries before the region
+    join()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    l0 = count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(s_deb)
+    s_rec.wait_event(ev0)
+    for e in range(args.steps):
+        rec(e + 1)
+        deb(e)
+    join()
+    ev1.record(s_deb)
+    launches = count() - l0
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clocks = sampler.stop()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    value = STREAMS * EPOCH * args.steps / (ms / 1000.0)
+
+    def prof_run(k):
+        for e in range(k):
+            rec(e + 1)
+            deb(e)
+        join()
+
+    roofline = deblur_roofline(api, prof_run, None, 1, local, args.profile_steps)
+    api.set_sm_reserve(0, device=local)
+    if rank == 0:
+        cfg_line = workload_config(args, world)
+        line = base_line(args, world, value, ms / args.steps, cfg_line, "f32")
+        line.update({"roofline": roofline, "cpu_baseline": None, "e2e": None, "gpu_launches": launches,
+                     "clocks": clocks, "streams_rank0": S, "streams_recovered_rank0": ok,
+                     "note": "c5 mode: device-resident inputs; e2e and the CPU baseline are measured in the c3 "
+                             "(default) workload"})
         print(json.dumps(line), flush=True)
 
 
 def main():
     args = parse()
-    world, rank, local = dist_setup()
-    if args.impl == "reference":
+    if args.gpus and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    world, rank, local = dist_setup(args.dry_run)
+    if args.gpus is None:
+        args.gpus = world
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if args.dry_run:
+        run_dry(args, world, rank)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.workload == "c5":
+        run_c5(args, world, rank, local)
     else:
-        run_b200(args, world, rank, local)
+        run_c3(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

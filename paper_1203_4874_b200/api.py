@@ -149,6 +149,35 @@ def _pitched_ok(x) -> bool:
     return True
 
 
+def _check_planes(name: str, x, shape=None, device=None):
+    """Raw device pointers go straight into the C ABI: reject tensors it would misread."""
+    if not (_pitched_ok(x) and x.dim() == 4):
+        raise CbpError(1, f"InvalidArgument: {name} must be a CUDA float32 (batch, channels, rows, cols) tensor "
+                          f"with unit column stride and pitched planes")
+    if shape is not None and tuple(x.shape) != tuple(shape):
+        raise CbpError(13, f"DimMismatch: {name} is {tuple(x.shape)}, expected {tuple(shape)}")
+    if device is not None and x.device != device:
+        raise CbpError(1, f"InvalidArgument: {name} is on {x.device}, expected {device}")
+
+
+def _check_slots(slots, count: int, device=None):
+    if not (isinstance(slots, torch.Tensor) and slots.is_cuda and slots.dtype == torch.uint8
+            and slots.is_contiguous()):
+        raise CbpError(1, "InvalidArgument: slots must be a contiguous uint8 CUDA tensor")
+    if slots.numel() < count * SLOT_BYTES:
+        raise CbpError(1, f"InvalidArgument: slots hold {slots.numel() // SLOT_BYTES} kernel slots, {count} needed")
+    if device is not None and slots.device != device:
+        raise CbpError(1, f"InvalidArgument: slots are on {slots.device}, expected {device}")
+
+
+def _slot_arg(slot, count: int, device) -> int:
+    """A slot given as a uint8 tensor (checked) or as a raw device address (trusted)."""
+    if isinstance(slot, torch.Tensor):
+        _check_slots(slot, count, device)
+        return slot.data_ptr()
+    return int(slot)
+
+
 def _as_batch(x) -> tuple[torch.Tensor, int]:
     ndim = x.dim() if isinstance(x, torch.Tensor) else np.ndim(x)
     t = _dev_planes(x)
@@ -518,7 +547,11 @@ def decode_frames_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, ou
     uint8 device tensor of batch * sizeof(KernelSlot) bytes receiving the per-frame state.
     ``ctx`` / ``stream`` select the context (workspaces) and CUDA stream (default: the
     thread's context and torch's current stream)."""
+    _check_planes("pub", pub)
     B, ch, rows, cols = pub.shape
+    _check_planes("prv", prv, pub.shape, pub.device)
+    _check_planes("out", out, pub.shape, pub.device)
+    _check_slots(slots, B, pub.device)
     ctx = ctx or context(pub.device.index)
     hint_arr = None
     if hints is not None:
@@ -542,7 +575,10 @@ def recover_kernels_async(pub: torch.Tensor, prv: torch.Tensor, cfg: DecodeCfg, 
     """cbp_recover_kernels_async: decode_frame's recovery stages only (decoder.cpp:290-352),
     kernels, widths and epsilons into ``slots``; deconvolve with spectral_deblur_slot and
     finish with validate_frames_async for the same results as decode_frames_async."""
+    _check_planes("pub", pub)
     B, ch, rows, cols = pub.shape
+    _check_planes("prv", prv, pub.shape, pub.device)
+    _check_slots(slots, B, pub.device)
     ctx = ctx or context(pub.device.index)
     hint_arr = (C.c_int * B)(*[int(h) for h in hints]) if hints is not None else None
     st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
@@ -555,7 +591,10 @@ def validate_frames_async(pub: torch.Tensor, latent: torch.Tensor, slots: torch.
                           stream=None):
     """cbp_validate_frames_async: validation residual (decoder.cpp:367-376) of deconvolved
     latents into ``slots[b].residual``."""
+    _check_planes("pub", pub)
     B, ch, rows, cols = pub.shape
+    _check_planes("latent", latent, pub.shape, pub.device)
+    _check_slots(slots, B, pub.device)
     ctx = ctx or context(pub.device.index)
     st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(pub.device)
     ctx.check(N.lib().cbp_validate_frames_async(ctx.ptr, C.c_void_p(pub.data_ptr()), C.c_void_p(latent.data_ptr()), B,
@@ -567,7 +606,12 @@ def spectral_deblur_slots(blurred: torch.Tensor, slots: torch.Tensor, frames_per
                           ctx: N.Context | None = None, stream=None):
     """cbp_spectral_deblur_slots: frame f of ``blurred`` (batch, ch, rows, cols) is deconvolved
     with slot ``f // frames_per_slot`` of ``slots`` (uint8 device tensor of kernel slots)."""
+    _check_planes("blurred", blurred)
     B, ch, rows, cols = blurred.shape
+    _check_planes("out", out, blurred.shape, blurred.device)
+    if int(frames_per_slot) < 1:
+        raise CbpError(1, "InvalidArgument: frames_per_slot must be >= 1")
+    _check_slots(slots, (B + int(frames_per_slot) - 1) // int(frames_per_slot), blurred.device)
     ctx = ctx or context(blurred.device.index)
     st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(blurred.device)
     ctx.check(N.lib().cbp_spectral_deblur_slots(ctx.ptr, C.c_void_p(blurred.data_ptr()), B, ch, rows, cols,
@@ -575,10 +619,14 @@ def spectral_deblur_slots(blurred: torch.Tensor, slots: torch.Tensor, frames_per
                                                 int(frames_per_slot), C.c_void_p(out.data_ptr()), out.stride(-2), st))
 
 
-def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor, ctx: N.Context | None = None,
+def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr, out: torch.Tensor, ctx: N.Context | None = None,
                          stream=None):
-    """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device."""
+    """cbp_spectral_deblur_slot: kernel, width and epsilon read on the device. ``slot_ptr`` is a
+    uint8 slot tensor (checked) or a raw device address of one cbp_kernel_slot."""
+    _check_planes("blurred", blurred)
     B, ch, rows, cols = blurred.shape
+    _check_planes("out", out, blurred.shape, blurred.device)
+    slot_ptr = _slot_arg(slot_ptr, 1, blurred.device)
     ctx = ctx or context(blurred.device.index)
     st = C.c_void_p(stream.cuda_stream) if stream is not None else _stream_ptr(blurred.device)
     ctx.check(N.lib().cbp_spectral_deblur_slot(ctx.ptr, C.c_void_p(blurred.data_ptr()), B, ch, rows, cols,
@@ -587,6 +635,7 @@ def spectral_deblur_slot(blurred: torch.Tensor, slot_ptr: int, out: torch.Tensor
 
 
 def read_slots(slots: torch.Tensor, count: int) -> list:
+    _check_slots(slots, count)
     host = (KernelSlot * count)()
     ctx = context(slots.device.index)
     ctx.check(N.lib().cbp_read_slots(ctx.ptr, C.c_void_p(slots.data_ptr()), count, host, _stream_ptr(slots.device)))

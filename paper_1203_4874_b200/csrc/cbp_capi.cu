@@ -297,12 +297,14 @@ int cbp_create(int device, cbp_ctx** out) {
     return CBP_CUDA_ERROR;
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming);
   if (cudaMalloc(&ctx->tile_ctr, 4 * sizeof(unsigned)) != cudaSuccess) ctx->tile_ctr = nullptr;  // static tiles then
   *out = ctx;
   return 0;
 }
 
 void cbp_destroy(cbp_ctx* ctx) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
@@ -313,6 +315,7 @@ void cbp_destroy(cbp_ctx* ctx) {
   if (ctx->tile_ctr) cudaFree(ctx->tile_ctr);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
   delete ctx;
 }
 
@@ -321,12 +324,14 @@ const char* cbp_last_error(const cbp_ctx* ctx) { return ctx ? ctx->err.c_str() :
 long long cbp_launch_count(const cbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int cbp_set_sm_reserve(cbp_ctx* ctx, int sms) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx || sms < 0) return CBP_INVALID_ARGUMENT;
   ctx->sm_reserve = sms;
   return 0;
 }
 
 int cbp_profile(cbp_ctx* ctx, int enable) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   ctx->prof = enable;
   ctx->prof_used = 0;
@@ -337,6 +342,7 @@ int cbp_profile(cbp_ctx* ctx, int enable) {
 // Sums the per-pass device times recorded since cbp_profile(ctx, 1); call after the
 // work has completed. pass_ms[3] = A, B, C totals; *planes = planes processed.
 int cbp_profile_read(cbp_ctx* ctx, double* pass_ms, long long* planes, int* groups) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   pass_ms[0] = pass_ms[1] = pass_ms[2] = 0.0;
   for (int g = 0; g + 4 <= ctx->prof_used; g += 4)
@@ -380,6 +386,8 @@ static int check_geometry(cbp_ctx* ctx, int batch, int channels, int rows, int c
 int cbp_spectral_deblur(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels, int rows,
                         int cols, int ld, const double* kernel, int t, double epsilon,
                         float* latent_dev, int ld_out, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st = check_kernel(ctx, kernel, t);
   if (st) return st;
@@ -416,6 +424,8 @@ int cbp_spectral_deblur(cbp_ctx* ctx, const float* blurred_dev, int batch, int c
 int cbp_spectral_deblur_slots(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels, int rows, int cols,
                               int ld, const cbp_kernel_slot* slots_dev, int frames_per_slot, float* latent_dev,
                               int ld_out, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !slots_dev) return CBP_INVALID_ARGUMENT;
   if (frames_per_slot < 1) return set_error(ctx, CBP_INVALID_ARGUMENT, "frames_per_slot must be >= 1");
   int st = check_geometry(ctx, batch, channels, rows, cols, ld);
@@ -438,6 +448,8 @@ int cbp_spectral_deblur_slots(cbp_ctx* ctx, const float* blurred_dev, int batch,
 int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, int channels,
                              int rows, int cols, int ld, const cbp_kernel_slot* slot_dev,
                              float* latent_dev, int ld_out, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !slot_dev) return CBP_INVALID_ARGUMENT;
   int st = check_geometry(ctx, batch, channels, rows, cols, ld);
   if (st) return st;
@@ -456,27 +468,33 @@ int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, 
 }
 
 int cbp_device_alloc(cbp_ctx* ctx, size_t bytes, void** dev) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx || !dev) return CBP_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   return cuda_check(ctx, cudaMalloc(dev, bytes ? bytes : 16), "device allocation");
 }
 
 void cbp_device_free(cbp_ctx* ctx, void* dev) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (ctx && dev) cudaFree(dev);
 }
 
 int cbp_copy_to_device(cbp_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   return cuda_check(ctx, cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice), "copy to device");
 }
 
 int cbp_copy_to_host(cbp_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   return cuda_check(ctx, cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost), "copy to host");
 }
 
 int cbp_read_slots(cbp_ctx* ctx, const cbp_kernel_slot* slots_dev, int count,
                    cbp_kernel_slot* slots_host, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int st = cuda_check(ctx, cudaMemcpyAsync(slots_host, slots_dev, sizeof(cbp_kernel_slot) * count,

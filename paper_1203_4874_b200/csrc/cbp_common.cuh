@@ -4,9 +4,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/cbp_cuda.h"
 
 namespace cbp_dev {
+
+// First-launch setup (cudaFuncSetAttribute, occupancy queries) is per device and must be
+// thread-safe: the reference's callers decode from a pool of host threads
+// (tools/cbp.cpp:141-164). CBP_ONCE_PER_DEVICE runs its body once per (call site, device).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 || d >= kMaxDevices ? 0 : d;
+}
+#define CBP_ONCE_PER_DEVICE(...)                                    \
+  do {                                                              \
+    static std::once_flag cbp_once_[cbp_dev::kMaxDevices];          \
+    std::call_once(cbp_once_[cbp_dev::current_device()], [&] __VA_ARGS__); \
+  } while (0)
 
 // ---------------------------------------------------------------- complex math
 __host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }

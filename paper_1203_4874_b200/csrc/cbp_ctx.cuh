@@ -28,9 +28,51 @@ struct cbp_ctx {
   long long prof_planes = 0;
   long long launches = 0;  // kernels enqueued by this context
   unsigned* tile_ctr = nullptr;  // dynamic-tile counters of the deconvolution passes (device)
+  // stream ordering of the context's shared scratch: the last stream that enqueued work and
+  // an event recorded there; a call on another stream first waits on it (StreamOrder)
+  cudaEvent_t order_ev = nullptr;
+  cudaStream_t order_stream = nullptr;
+  bool order_valid = false;
 };
 
 namespace cbp_host {
+
+// Makes ctx's device current for the duration of a C-ABI call (restored on return), so a
+// thread can drive contexts of several GPUs and a context never allocates or launches on
+// whatever device the calling thread happened to have current.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const cbp_ctx* ctx) {
+    if (ctx && cudaGetDevice(&prev) == cudaSuccess && prev != ctx->device) cudaSetDevice(ctx->device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// A context's workspaces, Wiener tables, tile counters and staging slot are shared by all its
+// calls. Work enqueued on a new stream first waits for the work the context enqueued on the
+// previous stream (an event), so using one context from several streams serializes instead
+// of racing on the scratch; one context per stream keeps them concurrent.
+struct StreamOrder {
+  cbp_ctx* c;
+  cudaStream_t s;
+  StreamOrder(cbp_ctx* ctx, void* stream) : c(ctx), s(static_cast<cudaStream_t>(stream)) {
+    if (c && c->order_ev && c->order_valid && c->order_stream != s) cudaStreamWaitEvent(s, c->order_ev, 0);
+  }
+  ~StreamOrder() {
+    if (c && c->order_ev) {
+      cudaEventRecord(c->order_ev, s);
+      c->order_stream = s;
+      c->order_valid = true;
+    }
+  }
+  StreamOrder(const StreamOrder&) = delete;
+  StreamOrder& operator=(const StreamOrder&) = delete;
+};
 
 enum Workspace {
   WS_X = 0,       // deconvolution half spectrum

@@ -209,16 +209,14 @@ static size_t smem_cols(const DeblurArgs& a, int W) {
 cudaError_t launch_deblur_pass(const DeblurArgs& a, int planes, int pass, cudaStream_t stream) {
   static const bool force_generic = getenv("CBP_GENERIC_FFT") != nullptr;
   if (!force_generic && launch_deblur_pass_ct(a, planes, pass, stream)) return cudaGetLastError();
-  static bool configured = false;
-  if (!configured) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_rows_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_rows_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_cols_filter<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_cols_filter<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_cols_filter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_cols_filter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    configured = true;
-  }
+  });
   dim3 ga((a.Mb + a.rows_per_cta - 1) / a.rows_per_cta, planes);
   if (pass == 0) {
     k_rows_forward<<<ga, 256, smem_rows(a), stream>>>(a);

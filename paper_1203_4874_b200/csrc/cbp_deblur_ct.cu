@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
   const int total = planes * groups;
   const bool v16 = a.in_vec4 && (L % 2 == 0);
   __shared__ __align__(8) unsigned long long bar[2];
-  unsigned ph[2] = {0u, 0u};
+  unsigned ph = 0u;  // mbarrier phase bits of buffers 0, 1 (a register, not an indexed array)
   const unsigned row_bytes = unsigned((a.Nb + 3) & ~3) * 4u;  // 16-byte multiple, within the pitch
   if constexpr (BULK) {
     if (threadIdx.x == 0) {
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
       if (next < total && threadIdx.x == 0) issue_bulk(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
       // every thread observes the rows' arrival; the first DIF stage reads floats >= Nb
       // (row tails, stale rows past the frame) as zeros, so no zeroing and no barrier
-      mbar_wait(&bar[cb], ph[cb]);
-      ph[cb] ^= 1u;
+      mbar_wait(&bar[cb], (ph >> cb) & 1u);
+      ph ^= 1u << cb;
       if (!(a.dbg & 1)) FFT::template dif_masked<false>(cur, twst, a.Nb, R{});
     } else {
       if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     mbar_expect_tx(b, unsigned(nc) * unsigned(a.Mb) * 8u);
     for (int s = 0; s < nc; ++s) bulk_g2s(dst + s * GP, XT + size_t(v0 + s) * a.xp, unsigned(a.Mb) * 8u, b);
   };
-  unsigned ph[2] = {0u, 0u}, phh = 0u;
+  unsigned ph = 0u, phh = 0u;  // phase bits of buffers 0, 1; filter strip
   int tile = blockIdx.x;
   if (tile < total && threadIdx.x == 0) issue(tile, sm, &bar[0]);
   // dynamic tiles: after its first (static) tile a CTA takes the next one from a counter,
@@ -346,8 +346,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     const int f = deblur_slot_index(a, p);
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
-    mbar_wait(&bar[cb], ph[cb]);  // every thread observes the strip's arrival
-    ph[cb] ^= 1u;
+    mbar_wait(&bar[cb], (ph >> cb) & 1u);  // every thread observes the strip's arrival
+    ph ^= 1u << cb;
     const int nc = min(W, a.Hc - v0);
     if (!P::HD && status == 0 && threadIdx.x == 0) {  // filter strip in flight during the forward transform
       const float2* Ht = a.H + size_t(f) * a.h_frame;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
   // plane), the frequency k split into the radix digits of the column order, so the box
   // lands with frequency k in slot pos(k) (a digit reversal is a transpose of the digit
   // axes); X[L] goes to the spare slot by a bulk copy (clipped to the pitch).
-  unsigned ph[2] = {0u, 0u};
+  unsigned ph = 0u;  // mbarrier phase bits of buffers 0, 1 (a register, not an indexed array)
   constexpr int NRAD = RadixCount<R>::value;
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
@@ -496,8 +496,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
     if constexpr (TMA) {
       const int cb = it & 1;
       if (next < total && threadIdx.x == 0) issue_tma(next, sm + (cb ^ 1) * TILE, &bar[cb ^ 1]);
-      mbar_wait(&bar[cb], ph[cb]);  // every thread observes the tile's arrival: no barrier
-      ph[cb] ^= 1u;
+      mbar_wait(&bar[cb], (ph >> cb) & 1u);  // every thread observes the tile's arrival: no barrier
+      ph ^= 1u << cb;
     } else {
       if (P::PIPE && next < total) issue(next, sm + ((it + 1) & 1) * TILE);
       cp_async_commit();
@@ -706,23 +706,31 @@ void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) 
                      (P::RTW ? size_t(P::TWN) * sizeof(float2) : P::L * sizeof(short));
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 15) & ~15) * sizeof(float2) +
                      size_t(P::RTW ? P::TWN : (P::L + 3) / 4) * sizeof(float2) + 3 * sizeof(unsigned long long);
-  static int pA = 0, pC = 0, pAb = 0, pCt = 0, sms = 0;
+  // per-device launch configuration, set up once per device (thread-safe: call_once)
+  struct Cfg {
+    int pA = 0, pC = 0, pAb = 0, pCt = 0, sms = 0;
+  };
+  static Cfg cfgs[kMaxDevices];
+  Cfg& c = cfgs[current_device()];
   constexpr bool kBulk = P::PIPE && P::L % 2 == 0;
-  if (!sms) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  CBP_ONCE_PER_DEVICE({
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, current_device());
     cudaFuncSetAttribute(k_rows_forward_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
     cudaFuncSetAttribute(k_rows_inverse_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
-    pA = resident_per_sm(k_rows_forward_ct<P>, P::NT, smA);
-    pC = resident_per_sm(k_rows_inverse_ct<P>, P::NT, smC);
+    c.pA = resident_per_sm(k_rows_forward_ct<P>, P::NT, smA);
+    c.pC = resident_per_sm(k_rows_inverse_ct<P>, P::NT, smC);
     if constexpr (kBulk) {
       cudaFuncSetAttribute(k_rows_forward_ct<P, kBulk>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smA));
-      pAb = resident_per_sm(k_rows_forward_ct<P, kBulk>, P::NT, smA);
+      c.pAb = resident_per_sm(k_rows_forward_ct<P, kBulk>, P::NT, smA);
     }
     if constexpr (P::PIPE) {
       cudaFuncSetAttribute(k_rows_inverse_ct<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smC));
-      pCt = resident_per_sm(k_rows_inverse_ct<P, true>, P::NT, smC);
+      c.pCt = resident_per_sm(k_rows_inverse_ct<P, true>, P::NT, smC);
     }
-  }
+  });
+  const int pA = c.pA, pC = c.pC, pAb = c.pAb, pCt = c.pCt, sms = c.sms;
+  (void)pAb;
+  (void)pCt;
   const int total = planes * ((a.Mb + P::RPC - 1) / P::RPC);
   if (inverse) {
     CUtensorMap map;
@@ -753,16 +761,22 @@ template <class P>
 void launch_cols(const DeblurArgs& a, int planes, cudaStream_t s) {
   constexpr int GP = ((P::G + 11) / 16) * 16 + 4;
   const size_t sm = ((P::PIPE ? 2 : 1) + (P::HD ? 0 : 1)) * size_t(GP) * P::W * sizeof(float2);
-  static int pB = 0, pT = 0, sms = 0;
-  if (!sms) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  struct Cfg {
+    int pB = 0, pT = 0, sms = 0;
+  };
+  static Cfg cfgs[kMaxDevices];
+  Cfg& c = cfgs[current_device()];
+  CBP_ONCE_PER_DEVICE({
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, current_device());
     cudaFuncSetAttribute(k_cols_filter_ct<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-    pB = resident_per_sm(k_cols_filter_ct<P>, P::NT, sm);
+    c.pB = resident_per_sm(k_cols_filter_ct<P>, P::NT, sm);
     if constexpr (P::PIPE) {
       cudaFuncSetAttribute(k_cols_filter_bulk<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      pT = resident_per_sm(k_cols_filter_bulk<P>, P::NT, sm);
+      c.pT = resident_per_sm(k_cols_filter_bulk<P>, P::NT, sm);
     }
-  }
+  });
+  const int pB = c.pB, pT = c.pT, sms = c.sms;
+  (void)pT;
   const int total = planes * ((a.Hc + P::W - 1) / P::W);
   if constexpr (P::PIPE) {
     static const bool bulk = !getenv("CBP_NO_BULK");

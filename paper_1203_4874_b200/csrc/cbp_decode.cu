@@ -319,6 +319,8 @@ extern "C" {
 int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels,
                             int rows, int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg,
                             float* latent_dev, int ld_out, cbp_kernel_slot* slots_dev, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
   return enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg, latent_dev,
                         ld_out, slots_dev, static_cast<cudaStream_t>(stream), false);
@@ -327,6 +329,8 @@ int cbp_decode_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* prv
 int cbp_recover_kernels_async(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels,
                               int rows, int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg,
                               cbp_kernel_slot* slots_dev, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
   return enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg, nullptr, ld,
                         slots_dev, static_cast<cudaStream_t>(stream), false, kStageRecover);
@@ -334,6 +338,8 @@ int cbp_recover_kernels_async(cbp_ctx* ctx, const float* pub_dev, const float* p
 
 int cbp_validate_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* latent_dev, int batch, int channels,
                               int rows, int cols, int ld, int ld_out, cbp_kernel_slot* slots_dev, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !slots_dev || !latent_dev) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, batch, channels, rows, cols, ld))) return st;
@@ -362,6 +368,7 @@ int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* 
                                int rows, int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg,
                                float* latent_dev, int ld_out, cbp_kernel_slot* slots_dev, void* stream,
                                void* slot_ready_event) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (!ctx || !cfg || !slots_dev) return CBP_INVALID_ARGUMENT;
   ctx->slot_event = slot_ready_event;
   const int st = enqueue_decode(ctx, pub_dev, prv_dev, batch, channels, rows, cols, ld, width_hints, cfg,
@@ -373,6 +380,8 @@ int cbp_decode_frames_async_ev(cbp_ctx* ctx, const float* pub_dev, const float* 
 int cbp_decode_frames(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int batch, int channels, int rows,
                       int cols, int ld, const int* width_hints, const cbp_decode_cfg* cfg, float* latent_dev,
                       int ld_out, cbp_decode_info* info, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !cfg) return CBP_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cbp_kernel_slot* slots = ws<cbp_kernel_slot>(ctx, WS_SLOTS, std::max(batch, 64));
@@ -410,6 +419,8 @@ int cbp_decode_frames(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, 
 int cbp_estimate_kernel_width(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int channels, int rows,
                               int cols, int ld, int search_min, int search_max, double tau, int* width,
                               int* clamped, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, 1, channels, rows, cols, ld))) return st;
@@ -445,6 +456,8 @@ int cbp_estimate_kernel_width(cbp_ctx* ctx, const float* pub_dev, const float* p
 
 int cbp_sample_slices(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int channels, int rows, int cols,
                       int ld, int t, int axis, double* slices_pub, double* slices_prv, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, 1, channels, rows, cols, ld))) return st;
@@ -471,6 +484,8 @@ int cbp_sample_slices(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, 
 int cbp_sample_cofactors(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int channels, int rows,
                          int cols, int ld, int width, int axis, double gap_threshold, double* values,
                          double* gaps, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, 1, channels, rows, cols, ld))) return st;
@@ -527,6 +542,8 @@ int cbp_sample_cofactors(cbp_ctx* ctx, const float* pub_dev, const float* prv_de
 
 int cbp_cofactor_solve_batch(cbp_ctx* ctx, const double* p, const double* q, int batch, int len, int t,
                              double gap_threshold, double* k1, double* k2, double* gaps, int* status, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_INVALID_ARGUMENT, "cofactor width must be >= 1");
   if (len < t) return set_error(ctx, CBP_INVALID_ARGUMENT, "slice degree below cofactor degree");
@@ -563,6 +580,8 @@ int cbp_cofactor_solve_batch(cbp_ctx* ctx, const double* p, const double* q, int
 }
 
 int cbp_complete_to_spectrum(cbp_ctx* ctx, const double* values, int t, int axis, double* out, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_DIM_MISMATCH, "scaled kernel transform must be square");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -576,6 +595,8 @@ int cbp_complete_to_spectrum(cbp_ctx* ctx, const double* values, int t, int axis
 
 int cbp_resolve_scales(cbp_ctx* ctx, const double* a_values, const double* b_values, int t, double* lambda,
                        double* mu, double* residual, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_DIM_MISMATCH, "transforms disagree on size");
   if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (31)");
@@ -613,6 +634,8 @@ int cbp_resolve_scales(cbp_ctx* ctx, const double* a_values, const double* b_val
 int cbp_assemble_kernel(cbp_ctx* ctx, const double* a_spectrum, const double* b_spectrum, const double* lambda,
                         const double* mu, int t, double max_imag_energy, double negative_weight_tol,
                         double* weights, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_DIM_MISMATCH, "spectrum estimates must be square and equal-sized");
   if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (31)");
@@ -643,6 +666,8 @@ int cbp_assemble_kernel(cbp_ctx* ctx, const double* a_spectrum, const double* b_
 
 int cbp_validate_pair(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, int channels, int rows, int cols,
                       int ld, const double* k1, const double* k2, int t, double* residual, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, 1, channels, rows, cols, ld))) return st;
@@ -671,6 +696,8 @@ int cbp_validate_pair(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, 
 int cbp_encode_frames(cbp_ctx* ctx, const float* latent_dev, int batch, int channels, int rows, int cols, int ld,
                       const double* k1, const double* k2, int t, float* pub_dev, float* prv_dev, int ld_out,
                       void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_geometry(ctx, batch, channels, rows, cols, ld))) return st;
@@ -695,6 +722,8 @@ int cbp_encode_frames(cbp_ctx* ctx, const float* latent_dev, int batch, int chan
 
 int cbp_synth_frames(cbp_ctx* ctx, float* out_dev, int planes, int rows, int cols, int ld, uint64_t seed,
                      void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   return cuda_check(ctx, launch_synth(out_dev, planes, rows, cols, ld, seed, static_cast<cudaStream_t>(stream)),
                     "synth launch");

@@ -83,6 +83,8 @@ int run_host(cbp_ctx* ctx, const void* pub, const void* prv, int bits, int n_fra
   const char* hprv = static_cast<const char*>(prv);
   int rec = -1;
   const int hint = width_hint;
+  int tlo = hint > 0 && cfg->trust_hint ? hint : cfg->search_min;
+  tlo = tlo < 1 ? 1 : (tlo > rows || tlo > cols ? 1 : tlo);
   for (int j = 0; j < n_frames; ++j) {
     const int r = j % kRing;
     if (j >= kRing) cudaStreamWaitEvent(P.h2d, P.out[r], 0);  // ring slot drained
@@ -110,7 +112,14 @@ int run_host(cbp_ctx* ctx, const void* pub, const void* prv, int bits, int n_fra
     if (st) return st;
     cudaEventRecord(P.done[r], P.comp);
     cudaStreamWaitEvent(P.d2h, P.done[r], 0);
-    cudaMemcpyAsync(latent + j * frame, dout + r * frame, sizeof(float) * frame, cudaMemcpyDeviceToHost, P.d2h);
+    // D2H only the region a latent can occupy: the top-left (rows-tlo+1) x (cols-tlo+1) of each
+    // plane, tlo = the smallest width the frame can decode with (trusted hint, else search_min)
+    for (int c = 0; c < channels; ++c) {
+      const size_t po = j * frame + size_t(c) * rows * cols;
+      cudaMemcpy2DAsync(latent + po, sizeof(float) * cols, dout + r * frame + size_t(c) * rows * cols,
+                        sizeof(float) * cols, sizeof(float) * (cols - tlo + 1), size_t(rows - tlo + 1),
+                        cudaMemcpyDeviceToHost, P.d2h);
+    }
     cudaEventRecord(P.out[r], P.d2h);
   }
   int st = cuda_check(ctx, cudaStreamSynchronize(P.d2h), "pipeline");
@@ -131,12 +140,14 @@ extern "C" {
 int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames, int channels, int rows,
                         int cols, const int* recover, int width_hint, const cbp_decode_cfg* cfg, float* latent,
                         cbp_kernel_slot* slots_host) {
+  cbp_host::DeviceGuard device_guard(ctx);
   return run_host(ctx, pub, prv, 0, n_frames, channels, rows, cols, recover, width_hint, cfg, latent, slots_host);
 }
 
 int cbp_decode_run_host_q(cbp_ctx* ctx, const void* pub_codes, const void* prv_codes, int bits, int n_frames,
                           int channels, int rows, int cols, const int* recover, int width_hint,
                           const cbp_decode_cfg* cfg, float* latent, cbp_kernel_slot* slots_host) {
+  cbp_host::DeviceGuard device_guard(ctx);
   if (bits != 8 && bits != 16) return ctx ? set_error(ctx, CBP_INVALID_ARGUMENT, "quantization depth must be u8 or u16")
                                           : CBP_INVALID_ARGUMENT;
   return run_host(ctx, pub_codes, prv_codes, bits, n_frames, channels, rows, cols, recover, width_hint, cfg, latent,

@@ -96,6 +96,8 @@ int cbp_spectral_deblur_slot(cbp_ctx* ctx, const float* blurred_dev, int batch, 
 
 int cbp_quantize_frames(cbp_ctx* ctx, const float* in_dev, int planes, int rows, int cols, int ld, int bits,
                         void* codes_dev, int ld_codes, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !in_dev || !codes_dev) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_bits(ctx, bits))) return st;
@@ -125,6 +127,8 @@ int cbp_quantize_frames(cbp_ctx* ctx, const float* in_dev, int planes, int rows,
 
 int cbp_dequantize_frames(cbp_ctx* ctx, const void* codes_dev, int bits, int planes, int rows, int cols,
                           int ld_codes, float* out_dev, int ld, void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !codes_dev || !out_dev) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_bits(ctx, bits))) return st;
@@ -135,6 +139,8 @@ int cbp_dequantize_frames(cbp_ctx* ctx, const void* codes_dev, int bits, int pla
 
 int cbp_degrade_bits(cbp_ctx* ctx, void* codes_dev, int bits, int planes, int rows, int cols, int ld_codes, int drop,
                      void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !codes_dev) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_bits(ctx, bits))) return st;
@@ -162,6 +168,8 @@ int cbp_decode_frames_q(cbp_ctx* ctx, const void* pub_codes, const void* prv_cod
                         int channels, int rows, int cols, int ld_codes, const int* width_hints,
                         const cbp_decode_cfg* cfg, float* latent_dev, int ld_out, cbp_decode_info* info,
                         void* stream) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx || !pub_codes || !prv_codes || !cfg) return CBP_INVALID_ARGUMENT;
   int st;
   if ((st = check_bits(ctx, bits))) return st;

@@ -295,21 +295,17 @@ __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
 }
 
 cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_fold_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cfg = true;
-  }
+  });
   if (a.channels != 1 && a.channels != 3) return cudaErrorInvalidValue;
   // row blocks: grid.y covers the shortest blocks (t = 1); taller ones exit at once
   const int tmin = t_fixed > 0 ? t_fixed : 1;
   dim3 g1(a.ncb, (a.rows + fold_rows(tmin, a.fold_rh) - 1) / fold_rows(tmin, a.fold_rh), a.batch * 2);
-  static bool cfg_tile = false;
-  if (!cfg_tile) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_fold_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<1>()));
     cudaFuncSetAttribute(k_fold_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<3>()));
-    cfg_tile = true;
-  }
+  });
   if (a.channels == 1) k_fold_tile<1><<<g1, 256, fold_smem<1>(), s>>>(a, t_fixed);
   else k_fold_tile<3><<<g1, 256, fold_smem<3>(), s>>>(a, t_fixed);
   const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
@@ -436,11 +432,9 @@ __global__ void __launch_bounds__(128) k_width_pick(RecoverArgs a) {
 cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
   dim3 g(a.nsizes, 2, a.batch);
   size_t sm = size_t(2) * a.search_max * a.search_max * sizeof(double2);  // block + eigenvectors
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cfg = true;
-  }
+  });
   k_width_blocks<<<g, 512, sm, s>>>(a);
   k_width_pick<<<a.batch, 128, 0, s>>>(a);
   return cudaGetLastError();
@@ -752,12 +746,10 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo,
 // more problems than one wave of 256-thread CTAs (2 per SM, register bound) use 128-thread
 // CTAs (4 per SM): the eigensolver chain is one warp either way.
 cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_solve<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_solve<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cfg = true;
-  }
+  });
   static const int nt_env = [] {
     const char* e = getenv("CBP_SOLVE_THREADS");
     return e ? atoi(e) : 0;
@@ -799,11 +791,9 @@ __global__ void __launch_bounds__(256) k_cofactor_batch(const double2* P, int lp
 cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, int lq, int batch, int t,
                                   double gap_threshold, double2* k1, double2* k2, double* gaps,
                                   int* status, double2* scratch, cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_cofactor_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cfg = true;
-  }
+  });
   k_cofactor_batch<<<batch, 256, solve_smem_bytes(t), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
                                                             status, scratch);
   return cudaGetLastError();
@@ -1166,12 +1156,10 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
 }
 
 cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_compose, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(compose_smem_bytes(kSolveMaxWidth)));
-    cfg = true;
-  }
+  });
   k_compose<<<a.batch, 256, compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s>>>(a);
   return cudaGetLastError();
 }
@@ -1211,11 +1199,9 @@ __global__ void __launch_bounds__(256) k_resolve(const double2* av, const double
 
 cudaError_t launch_resolve(const double2* a_values, const double2* b_values, int t, double2* lambda,
                            double2* mu, double* residual, int* status, double* value, cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
-    cfg = true;
-  }
+  });
   k_resolve<<<1, 256, compose_smem_bytes(t), s>>>(a_values, b_values, t, lambda, mu, residual, status, value);
   return cudaGetLastError();
 }
@@ -1244,11 +1230,9 @@ __global__ void __launch_bounds__(256) k_assemble(const double2* as, const doubl
 cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const double2* lambda,
                             const double2* mu, int t, double max_imag, double neg_tol, cbp_kernel_slot* slot,
                             cudaStream_t s) {
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
-    cfg = true;
-  }
+  });
   k_assemble<<<1, 256, compose_smem_bytes(t), s>>>(a_spec, b_spec, lambda, mu, t, max_imag, neg_tol, slot);
   return cudaGetLastError();
 }
@@ -1816,11 +1800,9 @@ cudaError_t launch_encode(const float* latent, int planes, int rows, int cols, i
   const int nt = ((rows + t - 1 + ENC_R - 1) / ENC_R) * ((cols + t - 1 + ENC_C - 1) / ENC_C);
   dim3 g(nt, planes);
   const size_t sm = size_t(t) * t * sizeof(double) + size_t(ENC_R + t - 1) * (ENC_C + t - 1) * sizeof(float);
-  static bool cfg = false;
-  if (!cfg) {
+  CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cfg = true;
-  }
+  });
   k_encode<<<g, 256, sm, s>>>(latent, rows, cols, ld, k, t, out, ld_out);
   return cudaGetLastError();
 }
