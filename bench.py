@@ -487,8 +487,8 @@ def run_c3(args, world, rank, local):
         barrier(world)
         e2e_s = max_over_ranks(t1 - t0, world)
         frame_bytes = CH * Mb * Nb * 4
-        # D2H: the top-left (Mb - tmin + 1) x (Nb - tmin + 1) of each plane, tmin = search_min
-        crop_bytes = CH * (Mb - 9 + 1) * (Nb - 9 + 1) * 4
+        # D2H: the first Mb - tmin + 1 rows of each plane, tmin = search_min (9)
+        crop_bytes = CH * (Mb - 9 + 1) * Nb * 4
         e2e = {"value": EPOCH * nE * world / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * crop_bytes,
                "steps": nE, "host_memory": "pinned",

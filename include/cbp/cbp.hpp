@@ -105,6 +105,9 @@ struct BlurredPair {
 };
 BlurredPair encode_frame(const Frame& latent, const CoprimePair& pair);  // on the GPU
 Frame quantize_frame(const Frame& f, BitDepth depth);
+// zero the `drop` least significant bits of every quantized sample (encoder.hpp:43;
+// device: cbp_degrade_bits on the frame's integer codes)
+Frame degrade_bits(const Frame& f, int drop);
 
 // -------------------------------------------------------------- poly.hpp:14-62
 inline constexpr double kDefaultGapThreshold = 1e-9;
@@ -115,8 +118,32 @@ struct CofactorSolution {
 };
 CofactorSolution cofactor_null_solve(const CVec& p, const CVec& q, int t,
                                      double gap_threshold = kDefaultGapThreshold);
+// 1D restrictions at arbitrary unit-circle points (poly.hpp:16-27; host utility)
+struct SpectralSliceSet {
+  Axis axis = Axis::Z1;
+  std::vector<cplx> points;
+  std::vector<CVec> slices;
+};
+SpectralSliceSet axis_dft(const Mat& plane, Axis axis, const std::vector<cplx>& points);
+// leading size x size Bezout block (poly.hpp:30; device: cbp_bezout_leading_block)
+CMat bezout_leading_block(const CVec& p, const CVec& q, int size);
+struct SingularityResult {
+  bool singular = true;
+  double ratio = 0.0;  // sigma_min / sigma_max, 0 for the zero matrix
+};
+// sigma_min / sigma_max < tau (poly.hpp:38; device: cbp_numerical_singularity)
+SingularityResult numerical_singularity(const CMat& m, double tau);
+// unit-norm minimizer of |A x|, phase-normalized (poly.hpp:55; device: cbp_homogeneous_lsq)
+CVec homogeneous_lsq(const CMat& a);
+CMat sylvester_matrix(const CVec& p, const CVec& q);       // poly.hpp:59 (host utility)
+int numerical_degree(const CVec& p, double rel_tol = 1e-12);  // poly.hpp:62 (host utility)
 
 // --------------------------------------------------------------- fft.hpp:9-18
+// unnormalized forward 2D DFT of any size and its 1/(M N)-normalized inverse (FP64, device:
+// cbp_fft2)
+CMat fft2(const CMat& x);
+CMat fft2(const Mat& x);
+CMat ifft2(const CMat& x);
 CMat axis_roots_dft(const Mat& plane, Axis axis, int t);
 
 // ---------------------------------------------------------- decoder.hpp:10-86

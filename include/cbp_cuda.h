@@ -258,6 +258,25 @@ int cbp_validate_pair(cbp_ctx* ctx, const float* pub_dev, const float* prv_dev, 
                       int rows, int cols, int ld, const double* k1, const double* k2, int t,
                       double* residual, void* stream);
 
+/* ---- polynomial / transform utilities (poly.hpp:30-55, fft.hpp:9-13) -------------
+ * Stand-alone device versions of functions the decode path runs fused inside its kernels.
+ * Complex arrays: interleaved (re, im) FP64, host memory; matrices row-major; synchronous.
+ * cbp_bezout_leading_block: B[i][j] = sum_{k<=min(i,j)} p[i+j+1-k] q[k] - q[i+j+1-k] p[k]
+ *   (poly.cpp:66-79): CBP_DEGENERATE_INPUT for an all-zero p or q.
+ * cbp_numerical_singularity: one-sided Jacobi singular values of the n x n matrix m;
+ *   ratio = sigma_min / sigma_max (0 and singular for the zero matrix), singular = ratio < tau
+ *   (poly.cpp:81-91).
+ * cbp_homogeneous_lsq: the unit right singular vector of the smallest singular value of the
+ *   rows x cols matrix a (rows >= cols), largest |x_i| rotated real positive (poly.cpp:123-130).
+ * cbp_fft2: the rows x cols 2D DFT, exponent -2 pi i (inverse = 0), or +2 pi i with the
+ *   1/(rows cols) normalization (inverse = 1) (fft.cpp:170-195); any size. */
+int cbp_bezout_leading_block(cbp_ctx* ctx, const double* p, int np, const double* q, int nq, int size,
+                             double* out, void* stream);
+int cbp_numerical_singularity(cbp_ctx* ctx, const double* m, int n, double tau, int* singular,
+                              double* ratio, void* stream);
+int cbp_homogeneous_lsq(cbp_ctx* ctx, const double* a, int rows, int cols, double* x, void* stream);
+int cbp_fft2(cbp_ctx* ctx, const double* in, int rows, int cols, int inverse, double* out, void* stream);
+
 /* ---- CBP generation on the device (encoder.hpp:36-37, poly.hpp:14) ----------
  * encode_frame: pub = latent (*) k1, prv = latent (*) k2 per plane, FP64 accumulation,
  * FP32 output of size (rows+t-1) x (cols+t-1) with row pitch ld_out. */
@@ -276,9 +295,9 @@ int cbp_synth_frames(cbp_ctx* ctx, float* out_dev, int planes, int rows, int col
  * (width_hint > 0 with cfg->trust_hint skips the width search); the others reuse the
  * most recent recovered kernel through spectral_deblur on the device. H2D, compute
  * and D2H overlap on internal streams. latent receives frames in the input geometry
- * (top-left (rows-t+1) x (cols-t+1) of each plane; only the top-left
- * (rows-tlo+1) x (cols-tlo+1) of each plane is transferred, tlo = width_hint when
- * cfg->trust_hint, else cfg->search_min; the rest of `latent` is left untouched). slots_host (may be NULL) gets
+ * (top-left (rows-t+1) x (cols-t+1) of each plane; only the first rows-tlo+1 rows of
+ * each plane are transferred, tlo = width_hint when cfg->trust_hint, else
+ * cfg->search_min; the remaining rows of `latent` are left untouched). slots_host (may be NULL) gets
  * one cbp_kernel_slot per recovery frame. Synchronizes before returning.
  * Pinned host memory gives full PCIe bandwidth. recover[0] must be nonzero. */
 int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames,

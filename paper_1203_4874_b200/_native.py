@@ -97,6 +97,10 @@ _SIGS = {
     "cbp_resolve_scales": (_I, [_P, _P, _P, _I, _P, _P, _P, _P]),
     "cbp_assemble_kernel": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _P, _P]),
     "cbp_validate_pair": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _I, _P, _P]),
+    "cbp_bezout_leading_block": (_I, [_P, _P, _I, _P, _I, _I, _P, _P]),
+    "cbp_numerical_singularity": (_I, [_P, _P, _I, _D, _P, _P, _P]),
+    "cbp_homogeneous_lsq": (_I, [_P, _P, _I, _I, _P, _P]),
+    "cbp_fft2": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "cbp_encode_frames": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _I, _P, _P, _I, _P]),
     "cbp_synth_frames": (_I, [_P, _P, _I, _I, _I, _I, C.c_uint64, _P]),
     "cbp_decode_run_host": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _P, _P]),

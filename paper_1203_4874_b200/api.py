@@ -378,6 +378,62 @@ def cofactor_null_solve(p, q, t: int, gap_threshold: float = 1e-9):
     return k1[0], k2[0], float(g[0])
 
 
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def bezout_leading_block(p, q, size: int) -> np.ndarray:
+    """cbp::bezout_leading_block (poly.hpp:30, poly.cpp:66-79) on the device."""
+    p, q = _c128(p), _c128(q)
+    out = np.empty((max(int(size), 0), max(int(size), 0)), np.complex128)
+    ctx = context()
+    ctx.check(N.lib().cbp_bezout_leading_block(ctx.ptr, p.ctypes.data_as(C.c_void_p), len(p),
+                                               q.ctypes.data_as(C.c_void_p), len(q), int(size),
+                                               out.ctypes.data_as(C.c_void_p), _stream_ptr(None)))
+    return out
+
+
+def numerical_singularity(m, tau: float) -> tuple[bool, float]:
+    """cbp::numerical_singularity (poly.hpp:38, poly.cpp:81-91): (singular, sigma_min/sigma_max)."""
+    m = _c128(m)
+    if m.ndim != 2 or m.shape[0] != m.shape[1] or m.shape[0] < 1:
+        raise CbpError(1, "InvalidArgument: singularity test needs a square matrix")
+    sing, ratio = C.c_int(), C.c_double()
+    ctx = context()
+    ctx.check(N.lib().cbp_numerical_singularity(ctx.ptr, m.ctypes.data_as(C.c_void_p), m.shape[0], float(tau),
+                                                C.byref(sing), C.byref(ratio), _stream_ptr(None)))
+    return bool(sing.value), float(ratio.value)
+
+
+def homogeneous_lsq(a) -> np.ndarray:
+    """cbp::homogeneous_lsq (poly.hpp:55, poly.cpp:123-130): unit minimizer of |A x|, phase-normalized."""
+    a = _c128(a)
+    if a.ndim != 2:
+        raise CbpError(1, "InvalidArgument: homogeneous system needs a matrix")
+    x = np.empty(a.shape[1], np.complex128)
+    ctx = context()
+    ctx.check(N.lib().cbp_homogeneous_lsq(ctx.ptr, a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1],
+                                          x.ctypes.data_as(C.c_void_p), _stream_ptr(None)))
+    return x
+
+
+def fft2(x, inverse: bool = False) -> np.ndarray:
+    """cbp::fft2 (fft.hpp:9-10): unnormalized forward 2D DFT of any size, FP64, on the device;
+    ``inverse`` gives cbp::ifft2 (fft.hpp:13, 1/(M N) normalization)."""
+    x = _c128(x)
+    if x.ndim != 2:
+        raise CbpError(1, "InvalidArgument: fft2 needs a matrix")
+    out = np.empty_like(x)
+    ctx = context()
+    ctx.check(N.lib().cbp_fft2(ctx.ptr, x.ctypes.data_as(C.c_void_p), x.shape[0], x.shape[1], int(bool(inverse)),
+                               out.ctypes.data_as(C.c_void_p), _stream_ptr(None)))
+    return out
+
+
+def ifft2(x) -> np.ndarray:
+    return fft2(x, inverse=True)
+
+
 def complete_to_spectrum(values, axis: int) -> np.ndarray:
     """cbp::complete_to_spectrum (decoder.hpp:45)."""
     v = np.ascontiguousarray(values, np.complex128); t = v.shape[0]

@@ -252,6 +252,42 @@ Frame quantize_frame(const Frame& f, BitDepth depth) {  // encoder.cpp:105-120
   return out;
 }
 
+Frame degrade_bits(const Frame& f, int drop) {  // encoder.cpp:124-139
+  validate_frame(f);
+  require(f.bit_depth != BitDepth::f32, Errc::not_quantized, "bit-precision degradation needs a quantized frame");
+  const int bits = bit_depth_bits(f.bit_depth);
+  require(drop >= 0 && drop < bits, Errc::invalid_argument, "drop must lie in [0, bit width)");
+  if (drop == 0) return f;
+  const double maxv = double((1u << bits) - 1);
+  const int r = f.rows(), c = f.cols(), planes = f.channels();
+  const size_t n = size_t(planes) * r * c;
+  // the frame's integer codes (lround(x * maxv), encoder.cpp:134) masked on the device
+  std::vector<unsigned short> c16(bits == 16 ? n : 0);
+  std::vector<unsigned char> c8(bits == 8 ? n : 0);
+  for (int k = 0; k < planes; ++k)
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < c; ++j) {
+        const long code = std::lround(f.planes[k](i, j) * maxv);
+        const size_t at = (size_t(k) * r + i) * c + j;
+        if (bits == 16) c16[at] = static_cast<unsigned short>(code);
+        else c8[at] = static_cast<unsigned char>(code);
+      }
+  const size_t bytes = n * (bits == 16 ? 2 : 1);
+  DevBuf d(bytes);
+  void* host = bits == 16 ? static_cast<void*>(c16.data()) : static_cast<void*>(c8.data());
+  check(cbp_copy_to_device(ctx(), d.p, host, bytes));
+  check(cbp_degrade_bits(ctx(), d.p, bits, planes, r, c, c, drop, nullptr));
+  check(cbp_copy_to_host(ctx(), host, d.p, bytes));
+  Frame out = f;
+  for (int k = 0; k < planes; ++k)
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < c; ++j) {
+        const size_t at = (size_t(k) * r + i) * c + j;
+        out.planes[k](i, j) = double(bits == 16 ? c16[at] : c8[at]) / maxv;
+      }
+  return out;
+}
+
 Mat conv2_full(const Mat& a, const Mat& b) {  // poly.cpp:27-38 (host utility)
   require(a.size() > 0 && b.size() > 0, Errc::dim_mismatch, "conv2_full needs nonempty inputs");
   const Mat& big = a.size() >= b.size() ? a : b;
@@ -286,6 +322,105 @@ CofactorSolution cofactor_null_solve(const CVec& p, const CVec& q, int t, double
   s.gap = gap;
   return s;
 }
+
+SpectralSliceSet axis_dft(const Mat& plane, Axis axis, const std::vector<cplx>& points) {  // poly.cpp:40-64
+  require(plane.size() > 0, Errc::invalid_argument, "axis_dft needs a nonempty plane");
+  for (const cplx& w : points)
+    require(std::abs(std::abs(w) - 1.0) <= 1e-12, Errc::non_unit_sample_point, "sample point off the unit circle");
+  const long d = axis == Axis::Z1 ? plane.rows() : plane.cols();
+  const long len = axis == Axis::Z1 ? plane.cols() : plane.rows();
+  SpectralSliceSet out;
+  out.axis = axis;
+  out.points = points;
+  for (const cplx& w : points) {
+    const double theta = std::arg(w);
+    std::vector<double> pr(static_cast<size_t>(d)), pi(static_cast<size_t>(d));
+    for (long m = 0; m < d; ++m) pr[size_t(m)] = std::cos(theta * double(m)), pi[size_t(m)] = std::sin(theta * double(m));
+    CVec slice(len);
+    for (long n = 0; n < len; ++n) {
+      double re = 0.0, im = 0.0;
+      for (long m = 0; m < d; ++m) {
+        const double x = axis == Axis::Z1 ? plane(m, n) : plane(n, m);
+        re += x * pr[size_t(m)];
+        im += x * pi[size_t(m)];
+      }
+      slice[n] = cplx(re, im);
+    }
+    out.slices.push_back(slice);
+  }
+  return out;
+}
+
+CMat bezout_leading_block(const CVec& p, const CVec& q, int size) {  // poly.cpp:66-79
+  CMat out(size > 0 ? size : 0, size > 0 ? size : 0);
+  std::vector<cplx> o(size_t(size > 0 ? size : 0) * (size > 0 ? size : 0));
+  check(cbp_bezout_leading_block(ctx(), reinterpret_cast<const double*>(p.data()), int(p.size()),
+                                 reinterpret_cast<const double*>(q.data()), int(q.size()), size,
+                                 reinterpret_cast<double*>(o.data()), nullptr));
+  return from_rowmajor(o.data(), size, size);
+}
+
+SingularityResult numerical_singularity(const CMat& m, double tau) {  // poly.cpp:81-91
+  require(m.rows() == m.cols() && m.rows() >= 1, Errc::invalid_argument, "singularity test needs a square matrix");
+  const auto a = rowmajor(m);
+  int singular = 1;
+  double ratio = 0.0;
+  check(cbp_numerical_singularity(ctx(), reinterpret_cast<const double*>(a.data()), int(m.rows()), tau, &singular,
+                                  &ratio, nullptr));
+  return {singular != 0, ratio};
+}
+
+CVec homogeneous_lsq(const CMat& a) {  // poly.cpp:123-130
+  require(a.rows() >= a.cols() && a.cols() >= 1, Errc::invalid_argument, "homogeneous system needs rows >= cols");
+  const auto v = rowmajor(a);
+  std::vector<cplx> x(size_t(a.cols()));
+  check(cbp_homogeneous_lsq(ctx(), reinterpret_cast<const double*>(v.data()), int(a.rows()), int(a.cols()),
+                            reinterpret_cast<double*>(x.data()), nullptr));
+  CVec out(a.cols());
+  for (long i = 0; i < a.cols(); ++i) out[i] = x[size_t(i)];
+  return out;
+}
+
+CMat sylvester_matrix(const CVec& p, const CVec& q) {  // poly.cpp:132-141
+  require(p.size() >= 1 && q.size() >= 1, Errc::invalid_argument, "empty polynomial");
+  const long m = p.size() - 1, n = q.size() - 1;
+  CMat s = CMat::Zero(m + n, m + n);
+  for (long r = 0; r < n; ++r)
+    for (long k = 0; k <= m; ++k) s(r, r + k) = p[m - k];
+  for (long r = 0; r < m; ++r)
+    for (long k = 0; k <= n; ++k) s(n + r, r + k) = q[n - k];
+  return s;
+}
+
+int numerical_degree(const CVec& p, double rel_tol) {  // poly.cpp:143-150
+  if (p.size() == 0) return -1;
+  double mx = 0.0;
+  for (long i = 0; i < p.size(); ++i) mx = std::max(mx, std::abs(p[i]));
+  if (mx == 0.0) return -1;
+  for (long i = p.size() - 1; i >= 0; --i)
+    if (std::abs(p[i]) > rel_tol * mx) return int(i);
+  return -1;
+}
+
+static CMat fft2_device(const CMat& x, int inverse) {
+  require(x.rows() >= 1 && x.cols() >= 1, Errc::invalid_argument, "fft2 needs a nonempty matrix");
+  const auto v = rowmajor(x);
+  std::vector<cplx> o(v.size());
+  check(cbp_fft2(ctx(), reinterpret_cast<const double*>(v.data()), int(x.rows()), int(x.cols()), inverse,
+                 reinterpret_cast<double*>(o.data()), nullptr));
+  return from_rowmajor(o.data(), int(x.rows()), int(x.cols()));
+}
+
+CMat fft2(const CMat& x) { return fft2_device(x, 0); }  // fft.cpp:166-168
+
+CMat fft2(const Mat& x) {  // fft.cpp:170-179
+  CMat c(x.rows(), x.cols());
+  for (long j = 0; j < x.cols(); ++j)
+    for (long i = 0; i < x.rows(); ++i) c(i, j) = cplx(x(i, j), 0.0);
+  return fft2_device(c, 0);
+}
+
+CMat ifft2(const CMat& x) { return fft2_device(x, 1); }  // fft.cpp:191-195
 
 CMat axis_roots_dft(const Mat& plane, Axis axis, int t) {  // fft.cpp:197-213
   require(plane.rows() >= 1 && plane.cols() >= 1, Errc::invalid_argument, "axis_roots_dft needs a nonempty plane");

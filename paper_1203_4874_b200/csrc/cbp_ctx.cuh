@@ -1,6 +1,7 @@
 // Host-side context shared by the C-ABI translation units.
 #pragma once
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -61,6 +62,8 @@ struct StreamOrder {
   cbp_ctx* c;
   cudaStream_t s;
   StreamOrder(cbp_ctx* ctx, void* stream) : c(ctx), s(static_cast<cudaStream_t>(stream)) {
+    static const bool off = getenv("CBP_NO_STREAM_ORDER") != nullptr;  // A/B switch
+    if (off) c = nullptr;
     if (c && c->order_ev && c->order_valid && c->order_stream != s) cudaStreamWaitEvent(s, c->order_ev, 0);
   }
   ~StreamOrder() {

@@ -16,7 +16,7 @@ using namespace cbp_host;
 
 namespace {
 
-constexpr int kDeviceMaxWidth = 31;  // 2t x 2t complex Gram + eigenvectors in shared memory
+constexpr int kDeviceMaxWidth = kWideMaxWidth;  // the reference's bound (decoder.cpp:32-33, 305-306)
 
 const char* stage_name(int s) {
   switch (s) {
@@ -153,8 +153,8 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.has_epsilon = cfg ? cfg->has_epsilon : 0;
   a.epsilon = cfg ? cfg->epsilon : 0.0;
   const size_t B = size_t(batch), T = size_t(t_max), L = size_t(a.lmax);
-  // decode widths are <= min(t_max, 31): the tile count is largest for the widest kernel
-  P.vtiles = want_validate ? validate_tiles(rows, cols, std::min(t_max, 31)) : 0;
+  // the tile count is largest for the widest kernel the batch allows
+  P.vtiles = want_validate ? validate_tiles(rows, cols, std::min(t_max, kDeviceMaxWidth)) : 0;
   // carve one allocation (256-byte aligned pieces)
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -174,6 +174,10 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   const size_t o_vpart = take(B * channels * std::max(P.vtiles, 1) * sizeof(double2) + 64);
   const size_t o_roots = take(size_t(rows + cols) * sizeof(double2));
   const size_t o_epart = take(signed_energy_doubles(batch, rows, cols) * sizeof(double));
+  // widths above the shared-memory solvers: per-CTA global scratch (k_solve_wide, k_compose_wide)
+  a.wide_ctas = t_max > kSmemMaxWidth ? 64 : 0;
+  a.wide_stride = wide_scratch_elems();
+  const size_t o_wide = take(size_t(a.wide_ctas) * a.wide_stride * sizeof(double2));
   char* base = static_cast<char*>(workspace(ctx, WS_MISC, off));
   if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   a.part = reinterpret_cast<double*>(base + o_part);
@@ -188,6 +192,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   P.vpart = reinterpret_cast<double*>(base + o_vpart);
   a.roots = reinterpret_cast<double2*>(base + o_roots);
   a.epart = reinterpret_cast<double*>(base + o_epart);
+  a.wide = a.wide_ctas ? reinterpret_cast<double2*>(base + o_wide) : nullptr;
   a.epart_z2 = size_t(batch) * 2 * ((cols + 31) / 32) * (rows / 2 + 1);  // z1 part (cbp_signed.cu)
   return 0;
 }
@@ -264,7 +269,7 @@ int enqueue_decode(cbp_ctx* ctx, const float* pub, const float* prv, int batch, 
   if (e == cudaSuccess && need_est) e = launch_width(a, s);
   if (need_est) ctx->launches += 5;
   if (record_events) cudaEventRecord(ctx->ev[1], s);
-  // the solve sizes shared memory for min(t_max, 31); wider kernels are flagged in k_solve
+  // widths <= 31 solve in shared memory, wider ones (<= 63) on the per-CTA global scratch
   if (e == cudaSuccess) e = launch_fold(a, 0, s);  // axis_roots_dft x4 (decoder.cpp:323-326)
   ctx->launches += 5;  // fold x3, solve, compose
   if (record_events) cudaEventRecord(ctx->ev[2], s);
@@ -353,7 +358,7 @@ int cbp_validate_frames_async(cbp_ctx* ctx, const float* pub_dev, const float* l
   a.rows = rows;
   a.cols = cols;
   a.ld = ld;
-  a.t_max = kDeviceMaxWidth;  // slot widths are <= 31 (solver limit)
+  a.t_max = kDeviceMaxWidth;  // slot widths are <= 63
   a.slots = slots_dev;
   const int vtiles = validate_tiles(rows, cols, kDeviceMaxWidth);
   double* vpart = ws<double>(ctx, WS_RED, size_t(2) * batch * channels * vtiles + 8);
@@ -493,7 +498,7 @@ int cbp_sample_cofactors(cbp_ctx* ctx, const float* pub_dev, const float* prv_de
   if (rows < width || cols < width)
     return set_error(ctx, CBP_FRAME_TOO_SMALL, "frame smaller than the kernel width");
   if (width > kDeviceMaxWidth)
-    return set_error(ctx, CBP_UNSUPPORTED, "kernel width exceeds the device solver limit (31)");
+    return set_error(ctx, CBP_UNSUPPORTED, "kernel width exceeds the device solver limit (63)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cbp_decode_cfg cfg;
   cbp_decode_cfg_default(&cfg);
@@ -547,11 +552,13 @@ int cbp_cofactor_solve_batch(cbp_ctx* ctx, const double* p, const double* q, int
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_INVALID_ARGUMENT, "cofactor width must be >= 1");
   if (len < t) return set_error(ctx, CBP_INVALID_ARGUMENT, "slice degree below cofactor degree");
-  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "cofactor width exceeds the device limit (31)");
+  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "cofactor width exceeds the device limit (63)");
   if (batch <= 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t nb = size_t(batch);
-  const size_t bytes = (2 * nb * len + 2 * nb * t + nb * (len + t)) * sizeof(double2) + nb * (sizeof(double) + sizeof(int)) + 1024;
+  const size_t wide_bytes = t > kSmemMaxWidth ? nb * wide_scratch_elems() * sizeof(double2) : 0;
+  const size_t bytes = (2 * nb * len + 2 * nb * t + nb * (len + t)) * sizeof(double2) + nb * (sizeof(double) + sizeof(int)) +
+                       1024 + wide_bytes;
   char* base = static_cast<char*>(workspace(ctx, WS_SOLVE, bytes));
   if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   double2* dp = reinterpret_cast<double2*>(base);
@@ -561,9 +568,10 @@ int cbp_cofactor_solve_batch(cbp_ctx* ctx, const double* p, const double* q, int
   double2* sc = d2 + nb * t;
   double* dg = reinterpret_cast<double*>(sc + nb * (len + t));
   int* ds = reinterpret_cast<int*>(dg + nb);
+  double2* wide = wide_bytes ? reinterpret_cast<double2*>(base + ((bytes - wide_bytes) & ~size_t(255))) : nullptr;
   cudaMemcpyAsync(dp, p, sizeof(double2) * nb * len, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dq, q, sizeof(double2) * nb * len, cudaMemcpyHostToDevice, s);
-  int st = cuda_check(ctx, launch_cofactor_batch(dp, len, dq, len, batch, t, gap_threshold, d1, d2, dg, ds, sc, s),
+  int st = cuda_check(ctx, launch_cofactor_batch(dp, len, dq, len, batch, t, gap_threshold, d1, d2, dg, ds, sc, wide, s),
                       "cofactor launch");
   if (st) return st;
   cudaMemcpyAsync(k1, d1, sizeof(double2) * nb * t, cudaMemcpyDeviceToHost, s);
@@ -599,9 +607,12 @@ int cbp_resolve_scales(cbp_ctx* ctx, const double* a_values, const double* b_val
   cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_DIM_MISMATCH, "transforms disagree on size");
-  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (31)");
+  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (63)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  char* base = static_cast<char*>(workspace(ctx, WS_SOLVE, sizeof(double2) * (2 * t * t + 2 * t) + 64));
+  const size_t wide_off = (sizeof(double2) * (2 * t * t + 2 * t) + 64 + 255) & ~size_t(255);
+  char* base = static_cast<char*>(workspace(ctx, WS_SOLVE, wide_off + (t > kSmemMaxWidth ? wide_scratch_elems() * sizeof(double2) : 0)));
+  if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  double2* wide = t > kSmemMaxWidth ? reinterpret_cast<double2*>(base + wide_off) : nullptr;
   double2* da = reinterpret_cast<double2*>(base);
   double2* db = da + t * t;
   double2* dl = db + t * t;
@@ -610,7 +621,7 @@ int cbp_resolve_scales(cbp_ctx* ctx, const double* a_values, const double* b_val
   int* dst = reinterpret_cast<int*>(dr + 2);
   cudaMemcpyAsync(da, a_values, sizeof(double2) * t * t, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(db, b_values, sizeof(double2) * t * t, cudaMemcpyHostToDevice, s);
-  int st = cuda_check(ctx, launch_resolve(da, db, t, dl, dm, dr, dst, dr + 1, s), "resolve launch");
+  int st = cuda_check(ctx, launch_resolve(da, db, t, dl, dm, dr, dst, dr + 1, wide, s), "resolve launch");
   if (st) return st;
   double r[2];
   int status = 0;
@@ -638,9 +649,12 @@ int cbp_assemble_kernel(cbp_ctx* ctx, const double* a_spectrum, const double* b_
   cbp_host::StreamOrder stream_order(ctx, stream);
   if (!ctx) return CBP_INVALID_ARGUMENT;
   if (t < 1) return set_error(ctx, CBP_DIM_MISMATCH, "spectrum estimates must be square and equal-sized");
-  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (31)");
+  if (t > kDeviceMaxWidth) return set_error(ctx, CBP_UNSUPPORTED, "width exceeds the device limit (63)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  char* base = static_cast<char*>(workspace(ctx, WS_SOLVE, sizeof(double2) * (2 * t * t + 2 * t) + sizeof(cbp_kernel_slot) + 64));
+  const size_t wide_off = (sizeof(double2) * (2 * t * t + 2 * t) + sizeof(cbp_kernel_slot) + 64 + 255) & ~size_t(255);
+  char* base = static_cast<char*>(workspace(ctx, WS_SOLVE, wide_off + (t > kSmemMaxWidth ? wide_scratch_elems() * sizeof(double2) : 0)));
+  if (!base) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  double2* wide = t > kSmemMaxWidth ? reinterpret_cast<double2*>(base + wide_off) : nullptr;
   double2* da = reinterpret_cast<double2*>(base);
   double2* db = da + t * t;
   double2* dl = db + t * t;
@@ -650,7 +664,7 @@ int cbp_assemble_kernel(cbp_ctx* ctx, const double* a_spectrum, const double* b_
   cudaMemcpyAsync(db, b_spectrum, sizeof(double2) * t * t, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dl, lambda, sizeof(double2) * t, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dm, mu, sizeof(double2) * t, cudaMemcpyHostToDevice, s);
-  int st = cuda_check(ctx, launch_assemble(da, db, dl, dm, t, max_imag_energy, negative_weight_tol, slot, s),
+  int st = cuda_check(ctx, launch_assemble(da, db, dl, dm, t, max_imag_energy, negative_weight_tol, slot, wide, s),
                       "assemble launch");
   if (st) return st;
   cbp_kernel_slot* h = pinned<cbp_kernel_slot>(ctx, 1);

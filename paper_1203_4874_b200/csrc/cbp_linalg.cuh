@@ -35,7 +35,7 @@ struct JacobiScratch {
 
 // G (n x n, row stride ldg) is overwritten by diag(eigenvalues); V (n x n, stride ldv)
 // receives the eigenvectors as columns. Whole CTA participates.
-__device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc,
+static __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc,
                             int max_sweeps = 40) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int m = (n + 1) & ~1;
@@ -131,10 +131,14 @@ __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int n, Jac
 // orthogonal, robust for dense clusters of tiny eigenvalues), EIG_INVIT (eigenvectors by
 // inverse iteration: faster when the spectrum is well separated)
 enum EigMode { EIG_VALUES = 0, EIG_QL = 1, EIG_INVIT = 2 };
-__device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, int mode) {
+// NMAX: largest n (64; 128 for the kernels of widths t > 32, whose 2t x 2t Grams live in
+// global memory). EIG_INVIT needs n <= 64 (per-lane arrays); NMAX = 128 runs QL for it.
+template <int NMAX = 64>
+static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, int mode) {
+  if (NMAX > 64 && mode == EIG_INVIT) mode = EIG_QL;
   const bool vectors = mode != EIG_VALUES;
-  __shared__ double s_d[64], s_e[64], s_beta[64], s_rc[64], s_rs[64];
-  __shared__ double2 s_ec[64], s_w[64], s_p[64], s_delta[64];
+  __shared__ double s_d[NMAX], s_e[NMAX], s_beta[NMAX], s_rc[NMAX], s_rs[NMAX];
+  __shared__ double2 s_ec[NMAX], s_w[NMAX], s_p[NMAX], s_delta[NMAX];
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   auto wsum = [&](double v) {
@@ -288,7 +292,7 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, i
   // stores; rsqrt/rcp with Newton steps replace hypot and the divisions on the chain.
   // The sweep's Givens rotations are then applied to each lane's rows of Z.
   {
-    __shared__ double s_dn[64], s_en[64];
+    __shared__ double s_dn[NMAX], s_en[NMAX];
     for (int i = lane; i < n * n; i += 32) {  // Z = I in the real part of V
       const int r = i / n, c = i - r * n;
       V[r * ldv + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
@@ -372,7 +376,7 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, i
   }
   for (int k = lane; k < n; k += 32) s_p[k].x = s_d[k];
   __syncwarp();
-  } else {
+  } else if constexpr (NMAX <= 64) {
   // ---- eigenvectors by inverse iteration, one lane per eigenvalue: bisection to full precision,
   // then three inverse-iteration steps (tridiagonal LU with partial pivoting) with
   // Rayleigh-quotient shifts. Eigenvalues closer than 1e-8 |T'| form a cluster that one
@@ -490,13 +494,15 @@ __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, i
 }
 
 // eigenvalues only (G's diagonal), whole CTA
+template <int NMAX = 64>
 __device__ __forceinline__ void herm_eigvals_cta(double2* G, int ldg, double2* V, int ldv, int n) {
-  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, EIG_VALUES);
+  if (threadIdx.x < 32) herm_eig_warp<NMAX>(G, ldg, V, ldv, n, EIG_VALUES);
   __syncthreads();
 }
 
 // whole-CTA entry: the tridiagonal route on warp 0 (the Jacobi solver above is kept as
 // the reference implementation, selectable with -DCBP_JACOBI)
+template <int NMAX = 64>
 __device__ __forceinline__ void herm_jacobi_cta(double2* G, int ldg, double2* V, int ldv, int n, JacobiScratch sc,
                                                 int mode = EIG_QL) {
 #ifdef CBP_JACOBI
@@ -506,7 +512,7 @@ __device__ __forceinline__ void herm_jacobi_cta(double2* G, int ldg, double2* V,
   }
 #endif
   (void)sc;
-  if (threadIdx.x < 32) herm_eig_warp(G, ldg, V, ldv, n, mode);
+  if (threadIdx.x < 32) herm_eig_warp<NMAX>(G, ldg, V, ldv, n, mode);
   __syncthreads();
 }
 
@@ -520,7 +526,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // column-major so each column is contiguous). A is destroyed. Writes sv[0..n-1]
 // (unsorted). Whole CTA participates; warps own column pairs (one pair per warp per
 // round when blockDim >= 32 * n/2) and the four inner products share one shuffle tree.
-__device__ void onesided_sv(double2* A, int lda, int n, double* sv, int* flag, int max_sweeps = 60) {
+static __device__ void onesided_sv(double2* A, int lda, int n, double* sv, int* flag, int max_sweeps = 60) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int m = (n + 1) & ~1;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {

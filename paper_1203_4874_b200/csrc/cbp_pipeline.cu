@@ -3,6 +3,7 @@
 // decode and D2H copies of consecutive frames overlap on three streams through a
 // ring of device frame buffers; recovered kernels stay on the device (slots) and are
 // reused by the following frames (spectral_deblur_slot), with no host round trip.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,13 +113,18 @@ int run_host(cbp_ctx* ctx, const void* pub, const void* prv, int bits, int n_fra
     if (st) return st;
     cudaEventRecord(P.done[r], P.comp);
     cudaStreamWaitEvent(P.d2h, P.done[r], 0);
-    // D2H only the region a latent can occupy: the top-left (rows-tlo+1) x (cols-tlo+1) of each
-    // plane, tlo = the smallest width the frame can decode with (trusted hint, else search_min)
-    for (int c = 0; c < channels; ++c) {
-      const size_t po = j * frame + size_t(c) * rows * cols;
-      cudaMemcpy2DAsync(latent + po, sizeof(float) * cols, dout + r * frame + size_t(c) * rows * cols,
-                        sizeof(float) * cols, sizeof(float) * (cols - tlo + 1), size_t(rows - tlo + 1),
-                        cudaMemcpyDeviceToHost, P.d2h);
+    // D2H only the rows a latent can occupy: the first rows-tlo+1 rows of each plane (one
+    // contiguous run per plane; pitched 2D copies of the column crop measured slower over
+    // PCIe), tlo = the smallest width the frame can decode with (trusted hint, else search_min)
+    static const bool full_d2h = getenv("CBP_E2E_FULL_D2H") != nullptr;  // A/B switch
+    if (full_d2h) {
+      cudaMemcpyAsync(latent + j * frame, dout + r * frame, sizeof(float) * frame, cudaMemcpyDeviceToHost, P.d2h);
+    } else {
+      for (int c = 0; c < channels; ++c) {
+        const size_t po = j * frame + size_t(c) * rows * cols;
+        cudaMemcpyAsync(latent + po, dout + r * frame + size_t(c) * rows * cols,
+                        sizeof(float) * size_t(rows - tlo + 1) * cols, cudaMemcpyDeviceToHost, P.d2h);
+      }
     }
     cudaEventRecord(P.out[r], P.d2h);
   }

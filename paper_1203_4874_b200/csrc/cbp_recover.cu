@@ -12,7 +12,7 @@
 
 namespace cbp_dev {
 
-constexpr int kSolveMaxWidth = 31;  // 2t x 2t complex Gram + eigenvectors in shared memory
+constexpr int kSolveMaxWidth = kSmemMaxWidth;  // 2t x 2t complex Gram + eigenvectors in shared memory
 
 // ----------------------------------------------------------------- slots
 __global__ void k_init_slots(RecoverArgs a, HintChunk hc) {
@@ -517,6 +517,7 @@ struct SolveResult {
 };
 
 // Whole CTA. On return x[0..2t) holds the unit-norm, phase-normalized null vector [k2; k1].
+template <int NMAX = 64>
 __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double2* q, int lq, int t,
                                           double gap_threshold, double2* r, SolveSmem sm) {
   const int n = 2 * t;
@@ -568,7 +569,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
   }
   __syncthreads();
   CBP_PHASE(11, pw);
-  herm_jacobi_cta(sm.G, n, sm.V, n, n, sm.js, EIG_QL);  // smooth p, q: dense tiny eigenvalues
+  herm_jacobi_cta<NMAX>(sm.G, n, sm.V, n, n, sm.js, EIG_QL);  // smooth p, q: dense tiny eigenvalues
   CBP_PHASE(12, pw);
   __shared__ int kmin_s, k2_s;
   __shared__ double lmax_s, lmin_s;
@@ -695,29 +696,14 @@ __device__ SolveSmem carve_solve(void* base, int t) {
   return sm;
 }
 
-// grid (t bound, 2 axes, batch): slice i of axis `axis` of frame b (decoder.cpp:94-123), for
-// the frames whose device-side width lies in (t_lo, t_hi]: the launcher buckets widths so a
-// batch of narrow kernels is not launched with the shared memory of the widest allowed one.
-template <int NT>
-__global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo, int t_hi) {
-  extern __shared__ double2 shs[];
-  const int i = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
-  cbp_kernel_slot* slot = a.slots + b;
-  if (slot->status != 0) return;
-  const int t = slot->width;
-  if (t <= t_lo || t > t_hi) return;
-  if (t > kSolveMaxWidth) {  // the 2t x 2t Gram and eigenvectors must fit in shared memory
-    if (i == 0 && axis == 0 && threadIdx.x == 0)
-      slot_fail(slot, CBP_UNSUPPORTED, CBP_STAGE_KERNEL_ESTIMATION_1D, -1, -1, 0.0, CBP_REASON_WIDTH_LIMIT);
-    return;
-  }
-  if (i >= t) return;
+// Slice i of axis `axis` of frame b (decoder.cpp:94-123) with the solve scratch at sm.
+template <int NMAX>
+__device__ void solve_slice(const RecoverArgs& a, int b, int axis, int i, int t, SolveSmem sm) {
   const int L = axis == 0 ? a.cols : a.rows;
   const double2* p = a.slices + slice_offset(a, b, axis, 0, i);
   const double2* q = a.slices + slice_offset(a, b, axis, 1, i);
   double2* r = a.scratch + ((size_t(b) * 2 + axis) * a.t_max + i) * size_t(a.lmax + a.t_max);
-  SolveSmem sm = carve_solve(shs, t);
-  SolveResult res = cofactor_solve_cta(p, L, q, L, t, a.gap_threshold, r, sm);
+  SolveResult res = cofactor_solve_cta<NMAX>(p, L, q, L, t, a.gap_threshold, r, sm);
   // k1 = tail, unit norm, into row i (z1) or column i (z2)
   __shared__ double nrm;
   if (threadIdx.x == 0) {
@@ -740,11 +726,44 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo,
       else
         vals[k * t + i] = v;
     }
+  __syncthreads();
 }
 
-// Two width buckets, t <= 16 and t > 16 (an empty bucket's CTAs exit at once). Batches with
-// more problems than one wave of 256-thread CTAs (2 per SM, register bound) use 128-thread
-// CTAs (4 per SM): the eigensolver chain is one warp either way.
+// grid (t bound, 2 axes, batch): slice i of axis `axis` of frame b, for the frames whose
+// device-side width lies in (t_lo, t_hi]: the launcher buckets widths so a batch of narrow
+// kernels is not launched with the shared memory of the widest allowed one.
+template <int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo, int t_hi) {
+  extern __shared__ double2 shs[];
+  const int i = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
+  cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0) return;
+  const int t = slot->width;
+  if (t <= t_lo || t > t_hi || t > kSolveMaxWidth || i >= t) return;
+  solve_slice<64>(a, b, axis, i, t, carve_solve(shs, t));
+}
+
+// Widths kSmemMaxWidth < t <= 63 (the reference's bound): the same solve with the 2t x 2t
+// Gram, eigenvectors and vectors in per-CTA global scratch (a.wide); wide_ctas persistent
+// CTAs walk the (slice, axis, frame) problems.
+__global__ void __launch_bounds__(256) k_solve_wide(RecoverArgs a) {
+  const int np = kWideMaxWidth * 2 * a.batch;
+  const SolveSmem sm = carve_solve(a.wide + size_t(blockIdx.x) * a.wide_stride, kWideMaxWidth);
+  for (int pid = blockIdx.x; pid < np; pid += gridDim.x) {
+    const int i = pid % kWideMaxWidth, axis = (pid / kWideMaxWidth) & 1, b = pid / (2 * kWideMaxWidth);
+    const cbp_kernel_slot* slot = a.slots + b;
+    const int t = slot->status == 0 ? slot->width : 0;
+    if (t <= kSolveMaxWidth || i >= t) continue;  // uniform over the CTA
+    SolveSmem w = carve_solve(a.wide + size_t(blockIdx.x) * a.wide_stride, t);
+    (void)sm;
+    solve_slice<128>(a, b, axis, i, t, w);
+  }
+}
+
+// Two width buckets, t <= 16 and 16 < t <= 31 (an empty bucket's CTAs exit at once), plus the
+// wide kernel when the batch allows t > 31. Batches with more problems than one wave of
+// 256-thread CTAs (2 per SM, register bound) use 128-thread CTAs (4 per SM): the eigensolver
+// chain is one warp either way.
 cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
   CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_solve<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -767,17 +786,23 @@ cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
     else
       k_solve<256><<<g, 256, solve_smem_bytes(tb), s>>>(a, lo, hi);
   }
+  if (a.t_max > kSolveMaxWidth) {
+    if (!a.wide) return cudaErrorInvalidValue;
+    k_solve_wide<<<a.wide_ctas, 256, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
+template <int NMAX>
 __global__ void __launch_bounds__(256) k_cofactor_batch(const double2* P, int lp, const double2* Q, int lq,
                                                         int t, double gap_threshold, double2* k1, double2* k2,
-                                                        double* gaps, int* status, double2* scratch) {
+                                                        double* gaps, int* status, double2* scratch, double2* wide,
+                                                        size_t wstride) {
   extern __shared__ double2 shs[];
   const int b = blockIdx.x;
-  SolveSmem sm = carve_solve(shs, t);
-  SolveResult res = cofactor_solve_cta(P + size_t(b) * lp, lp, Q + size_t(b) * lq, lq, t, gap_threshold,
-                                       scratch + size_t(b) * (max(lp, lq) + t), sm);
+  SolveSmem sm = carve_solve(wide ? wide + size_t(b) * wstride : shs, t);
+  SolveResult res = cofactor_solve_cta<NMAX>(P + size_t(b) * lp, lp, Q + size_t(b) * lq, lq, t, gap_threshold,
+                                             scratch + size_t(b) * (max(lp, lq) + t), sm);
   for (int k = threadIdx.x; k < t; k += blockDim.x) {
     k2[size_t(b) * t + k] = sm.x[k];
     k1[size_t(b) * t + k] = sm.x[t + k];
@@ -790,12 +815,18 @@ __global__ void __launch_bounds__(256) k_cofactor_batch(const double2* P, int lp
 
 cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, int lq, int batch, int t,
                                   double gap_threshold, double2* k1, double2* k2, double* gaps,
-                                  int* status, double2* scratch, cudaStream_t s) {
+                                  int* status, double2* scratch, double2* wide, cudaStream_t s) {
   CBP_ONCE_PER_DEVICE({
-    cudaFuncSetAttribute(k_cofactor_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_cofactor_batch<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
-  k_cofactor_batch<<<batch, 256, solve_smem_bytes(t), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
-                                                            status, scratch);
+  if (t > kSolveMaxWidth) {
+    if (!wide) return cudaErrorInvalidValue;
+    k_cofactor_batch<128><<<batch, 256, 0, s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps, status, scratch, wide,
+                                                wide_scratch_elems());
+  } else {
+    k_cofactor_batch<64><<<batch, 256, solve_smem_bytes(t), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
+                                                                 status, scratch, nullptr, 0);
+  }
   return cudaGetLastError();
 }
 
@@ -854,6 +885,12 @@ __host__ __device__ inline size_t compose_smem_bytes(int t) {
          (size_t(t) * t + 32 + 2 * (n / 2 + 1)) * sizeof(double) + 16;
 }
 
+__host__ __device__ inline size_t wide_elems_at(int t) {
+  const size_t b = solve_smem_bytes(t) > compose_smem_bytes(t) ? solve_smem_bytes(t) : compose_smem_bytes(t);
+  return (b + sizeof(double2) - 1) / sizeof(double2);
+}
+size_t wide_scratch_elems() { return wide_elems_at(kWideMaxWidth); }
+
 // sys row i*t+j: col i = -B'(i,j), col t+j = A'(i,j) (decoder.cpp:137-143); r = sys x.
 __device__ double sys_apply(const ComposeSmem& s, int t, const double2* x) {
   for (int idx = threadIdx.x; idx < t * t; idx += blockDim.x) {
@@ -876,6 +913,7 @@ __device__ double sys_apply(const ComposeSmem& s, int t, const double2* x) {
 // resolve_completed (decoder.cpp:133-155) via the 2t x 2t Gram of the t^2 x 2t system
 // plus direct-residual refinement. Returns 0 or CBP_REASON_SCALE_RATIO; x holds
 // [lambda; mu]; *residual = |sys x|, *ratio = min|x|/max|x|.
+template <int NMAX = 64>
 __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* ratio) {
   const int n = 2 * t;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
@@ -904,7 +942,7 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
   }
   __syncthreads();
   CBP_PHASE(25, blockIdx.x == 0);
-  herm_jacobi_cta(s.G, n, s.V, n, n, s.js, EIG_INVIT);  // resolve Gram: separated spectrum
+  herm_jacobi_cta<NMAX>(s.G, n, s.V, n, n, s.js, EIG_INVIT);  // resolve Gram: separated spectrum
   CBP_PHASE(22, blockIdx.x == 0);
   __shared__ int kmin_s;
   __shared__ double lmax_s, lmin_s;
@@ -1095,13 +1133,11 @@ __device__ int assemble_cta(ComposeSmem& s, int t, double max_imag, double neg_t
   return 0;
 }
 
-// One CTA per frame: first failing slice (reference order), complete_to_spectrum x2,
-// resolve, assemble, epsilon (decoder.cpp:333-353).
-__global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
-  extern __shared__ double2 shc[];
-  const int b = blockIdx.x;
+// Frame b: first failing slice (reference order), complete_to_spectrum x2, resolve,
+// assemble, epsilon (decoder.cpp:333-353), with the composition scratch at base.
+template <int NMAX>
+__device__ void compose_frame(const RecoverArgs& a, int b, void* base) {
   cbp_kernel_slot* slot = a.slots + b;
-  if (slot->status != 0) return;
   const int t = slot->width;
   const size_t base0 = size_t(b) * 2 * a.t_max;
   // the reference solves z1 slices 0..t-1 then z2 and stops at the first failure
@@ -1119,7 +1155,7 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   __syncthreads();
   if (slot->status != 0) return;
   CBP_PHASE(20, blockIdx.x == 0);
-  ComposeSmem s = carve_compose(shc, t);
+  ComposeSmem s = carve_compose(base, t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   __syncthreads();
   const double2* v1 = a.values + base0 * a.t_max;
@@ -1129,12 +1165,13 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   __syncthreads();
   double residual = 0.0, ratio = 0.0;
   CBP_PHASE(21, blockIdx.x == 0);
-  const int rs = resolve_cta(s, t, &residual, &ratio);
+  const int rs = resolve_cta<NMAX>(s, t, &residual, &ratio);
   CBP_PHASE(23, blockIdx.x == 0);
   if (rs) {
     if (threadIdx.x == 0) {
       slot_fail(slot, CBP_DEGENERATE_SCALES, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, ratio, rs);
     }
+    __syncthreads();
     return;
   }
   int reason = 0;
@@ -1144,14 +1181,33 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
   if (threadIdx.x == 0) {
     if (st) {
       slot_fail(slot, st, CBP_STAGE_KERNEL_ESTIMATION_2D_FFT, -1, -1, value, reason);
-      return;
+    } else {
+      slot->scale_residual = residual;
+      // epsilon = 1e-8 * peak|K|^2 (decoder.cpp:198-199). The estimate is clamped
+      // nonnegative, so |K(u,v)| <= sum w = K(0,0) and the peak is the weight sum.
+      double sum = 0.0;
+      for (int i = 0; i < t * t; ++i) sum += slot->weights[i];
+      slot->epsilon = a.has_epsilon ? a.epsilon : 1e-8 * sum * sum;
     }
-    slot->scale_residual = residual;
-    // epsilon = 1e-8 * peak|K|^2 (decoder.cpp:198-199). The estimate is clamped
-    // nonnegative, so |K(u,v)| <= sum w = K(0,0) and the peak is the weight sum.
-    double sum = 0.0;
-    for (int i = 0; i < t * t; ++i) sum += slot->weights[i];
-    slot->epsilon = a.has_epsilon ? a.epsilon : 1e-8 * sum * sum;
+  }
+  __syncthreads();
+}
+
+// One CTA per frame (t <= kSolveMaxWidth: shared-memory scratch).
+__global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
+  extern __shared__ double2 shc[];
+  const int b = blockIdx.x;
+  const cbp_kernel_slot* slot = a.slots + b;
+  if (slot->status != 0 || slot->width > kSolveMaxWidth) return;
+  compose_frame<64>(a, b, shc);
+}
+
+// Frames with kSolveMaxWidth < t <= 63: persistent CTAs with global scratch.
+__global__ void __launch_bounds__(256) k_compose_wide(RecoverArgs a) {
+  for (int b = blockIdx.x; b < a.batch; b += gridDim.x) {
+    const cbp_kernel_slot* slot = a.slots + b;
+    if (slot->status != 0 || slot->width <= kSolveMaxWidth) continue;  // uniform over the CTA
+    compose_frame<128>(a, b, a.wide + size_t(blockIdx.x) * a.wide_stride);
   }
 }
 
@@ -1161,6 +1217,10 @@ cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s) {
                          int(compose_smem_bytes(kSolveMaxWidth)));
   });
   k_compose<<<a.batch, 256, compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s>>>(a);
+  if (a.t_max > kSolveMaxWidth) {
+    if (!a.wide) return cudaErrorInvalidValue;
+    k_compose_wide<<<min(a.batch, a.wide_ctas), 256, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
@@ -1177,18 +1237,20 @@ cudaError_t launch_complete(const double2* values, int t, int axis, double2* out
   return cudaGetLastError();
 }
 
+template <int NMAX>
 __global__ void __launch_bounds__(256) k_resolve(const double2* av, const double2* bv, int t, double2* lambda,
-                                                 double2* mu, double* residual, int* status, double* value) {
+                                                 double2* mu, double* residual, int* status, double* value,
+                                                 double2* wide) {
   extern __shared__ double2 shc[];
   CBP_PHASE(20, blockIdx.x == 0);
-  ComposeSmem s = carve_compose(shc, t);
+  ComposeSmem s = carve_compose(wide ? static_cast<void*>(wide) : static_cast<void*>(shc), t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   __syncthreads();
   complete_cta(av, t, 0, s.root, s.A);
   complete_cta(bv, t, 1, s.root, s.B);
   __syncthreads();
   double res = 0.0, ratio = 0.0;
-  const int rs = resolve_cta(s, t, &res, &ratio);
+  const int rs = resolve_cta<NMAX>(s, t, &res, &ratio);
   for (int i = threadIdx.x; i < t; i += blockDim.x) lambda[i] = s.x[i], mu[i] = s.x[t + i];
   if (threadIdx.x == 0) {
     *residual = res;
@@ -1198,20 +1260,28 @@ __global__ void __launch_bounds__(256) k_resolve(const double2* av, const double
 }
 
 cudaError_t launch_resolve(const double2* a_values, const double2* b_values, int t, double2* lambda,
-                           double2* mu, double* residual, int* status, double* value, cudaStream_t s) {
+                           double2* mu, double* residual, int* status, double* value, double2* wide,
+                           cudaStream_t s) {
   CBP_ONCE_PER_DEVICE({
-    cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
+    cudaFuncSetAttribute(k_resolve<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(compose_smem_bytes(kSolveMaxWidth)));
   });
-  k_resolve<<<1, 256, compose_smem_bytes(t), s>>>(a_values, b_values, t, lambda, mu, residual, status, value);
+  if (t > kSolveMaxWidth) {
+    if (!wide) return cudaErrorInvalidValue;
+    k_resolve<128><<<1, 256, 0, s>>>(a_values, b_values, t, lambda, mu, residual, status, value, wide);
+  } else {
+    k_resolve<64><<<1, 256, compose_smem_bytes(t), s>>>(a_values, b_values, t, lambda, mu, residual, status, value,
+                                                         nullptr);
+  }
   return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(256) k_assemble(const double2* as, const double2* bs, const double2* lambda,
                                                   const double2* mu, int t, double max_imag, double neg_tol,
-                                                  cbp_kernel_slot* slot) {
+                                                  cbp_kernel_slot* slot, double2* wide) {
   extern __shared__ double2 shc[];
   CBP_PHASE(20, blockIdx.x == 0);
-  ComposeSmem s = carve_compose(shc, t);
+  ComposeSmem s = carve_compose(wide ? static_cast<void*>(wide) : static_cast<void*>(shc), t);
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.root[i] = zroot(i, t);
   for (int i = threadIdx.x; i < t * t; i += blockDim.x) s.A[i] = as[i], s.B[i] = bs[i];
   for (int i = threadIdx.x; i < t; i += blockDim.x) s.x[i] = lambda[i], s.x[t + i] = mu[i];
@@ -1229,11 +1299,13 @@ __global__ void __launch_bounds__(256) k_assemble(const double2* as, const doubl
 
 cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const double2* lambda,
                             const double2* mu, int t, double max_imag, double neg_tol, cbp_kernel_slot* slot,
-                            cudaStream_t s) {
+                            double2* wide, cudaStream_t s) {
   CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, int(compose_smem_bytes(kSolveMaxWidth)));
   });
-  k_assemble<<<1, 256, compose_smem_bytes(t), s>>>(a_spec, b_spec, lambda, mu, t, max_imag, neg_tol, slot);
+  if (t > kSolveMaxWidth && !wide) return cudaErrorInvalidValue;
+  k_assemble<<<1, 256, t > kSolveMaxWidth ? 0 : compose_smem_bytes(t), s>>>(a_spec, b_spec, lambda, mu, t, max_imag,
+                                                                          neg_tol, slot, t > kSolveMaxWidth ? wide : nullptr);
   return cudaGetLastError();
 }
 
@@ -1520,6 +1592,30 @@ __device__ __forceinline__ void conv_col1T(const double* te, const double* to, i
     }
   }
 }
+// any tap count (kernels wider than 32): taps in chunks of 4 (tp = conv_pad(t) is a multiple
+// of 4) with an (OUT + 3)-value window, same per-output FMA order as conv_col1T
+template <int OUT>
+__device__ __forceinline__ void conv_col1W(const double* te, const double* to, int twh, const double* kt, int t,
+                                           int tp, int li0, int lj, double* acc) {
+#pragma unroll
+  for (int q = 0; q < OUT; ++q) acc[q] = 0.0;
+  for (int b2 = 0; b2 < t; ++b2) {
+    const int c = lj + t - 1 - b2;
+    const double* col = ((c & 1) ? to : te) + (li0 + tp - 1) * twh + (c >> 1);
+    const double* kc = kt + b2 * tp;
+    for (int j0 = 0; j0 < tp; j0 += 4) {
+      double v[OUT + 3];
+#pragma unroll
+      for (int k = 0; k < OUT + 3; ++k) v[k] = col[(OUT - 1 - k - j0) * twh];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double w = kc[j0 + j];
+#pragma unroll
+        for (int q = 0; q < OUT; ++q) acc[q] = fma(w, v[OUT - 1 - q + j], acc[q]);
+      }
+    }
+  }
+}
 __device__ __forceinline__ void conv2_dispatch(const double* te, const double* to, int twh, const double* kt, int t,
                                                int tp, int li0, int l, double* a0, double* a1) {
   switch (tp) {
@@ -1544,9 +1640,12 @@ __device__ __forceinline__ void conv2_dispatch(const double* te, const double* t
     case 28:
       conv_col1T<8, 28>(te, to, twh, kt, t, li0, 2 * l, a0);
       return conv_col1T<8, 28>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
-    default:
+    case 32:
       conv_col1T<8, 32>(te, to, twh, kt, t, li0, 2 * l, a0);
       return conv_col1T<8, 32>(te, to, twh, kt, t, li0, 2 * l + 1, a1);
+    default:  // t > 32 (up to the reference's 63)
+      conv_col1W<8>(te, to, twh, kt, t, tp, li0, 2 * l, a0);
+      return conv_col1W<8>(te, to, twh, kt, t, tp, li0, 2 * l + 1, a1);
   }
 }
 
@@ -1706,8 +1805,8 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.co = ra.cols;
   dim3 g(ntiles_max, ra.batch * ra.channels);
   static const bool two = !getenv("CBP_CONV_ONECOL") && conv_rows(1) == 32;
-  size_t sm = 0;  // the device-side width is <= min(t_max, 31) (solver limit); tile heights vary with t
-  for (int t = 1; t <= std::min(ra.t_max, 31); ++t) sm = std::max(sm, two ? conv2_smem(t) : conv_smem(t, 0));
+  size_t sm = 0;  // the device-side width is <= t_max; tile heights vary with t
+  for (int t = 1; t <= std::min(ra.t_max, kWideMaxWidth); ++t) sm = std::max(sm, two ? conv2_smem(t) : conv_smem(t, 0));
   if (two) {
     if (cudaFuncSetAttribute(k_conv_resid2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
       return cudaErrorInvalidValue;

@@ -38,7 +38,19 @@ struct RecoverArgs {
   double gap_threshold, max_imag_energy, negative_weight_tol;
   int has_epsilon;
   double epsilon;
+  // kernels wider than the shared-memory solvers (t > kSmemMaxWidth): per-CTA scratch for
+  // the 2t x 2t Grams and eigenvectors in global memory (L2-resident), wide_ctas CTAs
+  double2* wide;
+  size_t wide_stride;  // double2 elements per CTA
+  int wide_ctas;
 };
+
+// widest kernel whose solve / composition scratch lives in shared memory; wider ones (up to
+// the reference's 63, decoder.cpp:32-33,305-306) run the same code on global scratch
+constexpr int kSmemMaxWidth = 31;
+constexpr int kWideMaxWidth = 63;
+// double2 elements of global scratch one wide CTA needs (solve and compose at t = 63)
+size_t wide_scratch_elems();
 
 __host__ __device__ inline size_t slice_offset(const RecoverArgs& a, int b, int axis, int q, int i) {
   return ((size_t(b) * 2 + axis) * 2 + q) * size_t(a.t_max) * a.lmax + size_t(i) * a.lmax;
@@ -66,16 +78,18 @@ cudaError_t launch_validate(const RecoverArgs& a, const float* latent, int ld_ou
 int validate_tiles(int rows, int cols, int t);  // t: kernel width (sets the tile height)
 
 // Standalone batched cofactor solve for the stage-level C ABI entry.
+// (t > kSmemMaxWidth: wide = global scratch of wide_scratch_elems() per problem, else null)
 cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, int lq, int batch, int t,
                                   double gap_threshold, double2* k1, double2* k2, double* gaps,
-                                  int* status, double2* scratch, cudaStream_t s);
+                                  int* status, double2* scratch, double2* wide, cudaStream_t s);
 // complete_to_spectrum / resolve_scales / assemble_kernel on one problem (stage entries).
 cudaError_t launch_complete(const double2* values, int t, int axis, double2* out, cudaStream_t s);
 cudaError_t launch_resolve(const double2* a_values, const double2* b_values, int t, double2* lambda,
-                           double2* mu, double* residual, int* status, double* value, cudaStream_t s);
+                           double2* mu, double* residual, int* status, double* value, double2* wide,
+                           cudaStream_t s);
 cudaError_t launch_assemble(const double2* a_spec, const double2* b_spec, const double2* lambda,
                             const double2* mu, int t, double max_imag, double neg_tol,
-                            cbp_kernel_slot* slot, cudaStream_t s);
+                            cbp_kernel_slot* slot, double2* wide, cudaStream_t s);
 // validate_pair (decoder.cpp:380-395): |pub (*) k2 - prv (*) k1| / |pub (*) k2|
 cudaError_t launch_validate_pair(const float* pub, const float* prv, int channels, int rows, int cols,
                                  int ld, const double* k1, const double* k2, int t, double* part,

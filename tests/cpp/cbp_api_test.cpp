@@ -233,6 +233,58 @@ int main(int argc, char** argv) {
     CHECK(s.gap > 1e-3);
     CHECK_THROWS_CODE(cofactor_null_solve(CVec{1, 2, 1}, CVec{1, 2, 1}, 2), Errc::ill_conditioned);
   }
+  // poly_test.cpp:134-287 and fft_test.cpp:32-74: the stand-alone device utilities
+  {
+    const CMat b1 = bezout_leading_block(CVec{1, 2}, CVec{3, 1}, 1);  // resultant of a linear pair
+    CHECK(b1.rows() == 1 && b1(0, 0) == cplx(5, 0));
+    const CMat b2 = bezout_leading_block(CVec{1, 3, 2}, CVec{3, 4, 1}, 2);  // shared root z = -1
+    bool all5 = true;
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) all5 = all5 && b2(i, j) == cplx(5, 0);
+    CHECK(all5);
+    CHECK(numerical_singularity(b2, 1e-8).singular);
+    CHECK_THROWS_CODE(bezout_leading_block(CVec{0, 0}, CVec{1, 2}, 2), Errc::degenerate_input);
+    CMat id = CMat::Zero(3, 3);
+    for (int i = 0; i < 3; ++i) id(i, i) = 1.0;
+    const SingularityResult si = numerical_singularity(id, 1e-8);
+    CHECK(!si.singular && std::abs(si.ratio - 1.0) <= 1e-12);
+    const SingularityResult sf = numerical_singularity(CMat(2, 2, cplx(5, 0)), 1e-8);
+    CHECK(sf.singular && sf.ratio <= 1e-15);
+    const SingularityResult sz = numerical_singularity(CMat::Zero(4, 4), 1e-8);
+    CHECK(sz.singular && sz.ratio == 0.0);
+    CMat a = CMat::Zero(2, 2);
+    a(0, 0) = 1.0;
+    const CVec x = homogeneous_lsq(a);
+    CHECK(std::abs(x[0]) <= 1e-12 && std::abs(std::abs(x[1]) - 1.0) <= 1e-12);
+    CHECK_THROWS_CODE(homogeneous_lsq(CMat::Ones(2, 3)), Errc::invalid_argument);
+    Mat delta = Mat::Zero(3, 4);
+    delta(0, 0) = 1.0;
+    const CMat f = fft2(delta);
+    double err = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 4; ++j) err = std::max(err, std::abs(f(i, j) - cplx(1, 0)));
+    CHECK(err <= 1e-12);
+    const Mat r = random_mat(61, 97, 18);
+    const CMat back = ifft2(fft2(r));
+    double rt = 0.0;
+    for (int j = 0; j < 97; ++j)
+      for (int i = 0; i < 61; ++i) rt = std::max(rt, std::abs(back(i, j) - cplx(r(i, j), 0.0)));
+    CHECK(rt <= 1e-10);
+    const CMat s = sylvester_matrix(CVec{1, 2}, CVec{3, 1});
+    CHECK(std::abs(s(0, 0) * s(1, 1) - s(0, 1) * s(1, 0)) == 5.0);
+    CHECK(numerical_degree(CVec{0, 1, 1e-15}) == 1 && numerical_degree(CVec{0, 0}) == -1);
+    // encoder_test.cpp:190-215 degrade_bits on a u8 frame
+    Frame q;
+    q.bit_depth = BitDepth::u8;
+    q.planes.push_back(Mat(1, 2, 255.0 / 255.0));
+    q.planes[0](0, 1) = 7.0 / 255.0;
+    const Frame d = degrade_bits(q, 2);
+    CHECK(d.planes[0](0, 0) == 252.0 / 255.0 && d.planes[0](0, 1) == 4.0 / 255.0);
+    CHECK_THROWS_CODE(degrade_bits(q, 8), Errc::invalid_argument);
+    Frame f32 = q;
+    f32.bit_depth = BitDepth::f32;
+    CHECK_THROWS_CODE(degrade_bits(f32, 1), Errc::not_quantized);
+  }
   // encoder_test.cpp:28-54 determinism and validation
   {
     const CoprimePair a = generate_coprime_pair(9, 42), b = generate_coprime_pair(9, 42);

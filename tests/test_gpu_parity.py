@@ -619,3 +619,55 @@ def test_deblur_slots_small_groups():
                         "-k", "test_deblur_slots_equals_per_slot_calls"], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------------------------ wide kernels (t > 31)
+@pytest.mark.parametrize("rows,cols,t,lo,hi,trust,lseed,pseed", [
+    (96, 100, 33, 27, 35, True, None, None),     # trusted hint just past the shared-memory solvers
+    (160, 160, 33, 27, 35, False, (11, 3), (12, 3)),  # estimated width 33 (Bezout blocks up to 35)
+    (160, 160, 33, 27, 35, False, (11, 0), (12, 0)),  # estimated: the oracle's InconsistentAxes, same text
+    (80, 90, 63, 61, 63, True, None, None),      # the reference's widest kernel (decoder.cpp:32-33,305-306)
+])
+def test_decode_wide_kernel_parity(oracle, api, rows, cols, t, lo, hi, trust, lseed, pseed):
+    """Kernels wider than 31 run the cofactor solves and the composition on per-CTA global
+    scratch (k_solve_wide, k_compose_wide) and the validation with chunked taps; same
+    parity bar as the narrow kernels."""
+    ls = oracle.frame_seed(*lseed) if lseed else oracle.frame_seed(1, rows + t)
+    ps = oracle.frame_seed(*pseed) if pseed else oracle.frame_seed(2, cols + t)
+    lat, pair, pub, prv = make(oracle, rows, cols, 1, t, ls, ps)
+    hint = t if trust else None
+    try:
+        oracle.decode_frame(pub.astype(np.float64), prv.astype(np.float64), hint=hint,
+                            cfg=oracle.make_cfg(lo, hi, trust_hint=trust))
+    except oracle.OracleError as r:
+        with pytest.raises(api.CbpError) as e:
+            api.decode_frame(torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda(), hint=hint,
+                             cfg=api.make_cfg(lo, hi, trust_hint=trust))
+        assert e.value.code == r.code and str(e.value) == str(r)
+        return
+    d, _ = check_decode(oracle, api, lat, pub, prv, lo, hi, hint=hint, trust=trust)
+    assert d.width_used == t
+    assert krel(d.kernel_estimate, pair.k1) <= 1e-4
+
+
+def test_wide_stage_entry_points(oracle, api):
+    """cofactor_null_solve / resolve_scales / assemble_kernel at t = 40 through the stage-level
+    C ABI (global-scratch kernels)."""
+    rng = np.random.default_rng(40)
+    t = 40
+    l = rng.uniform(-1, 1, 90) + 1j * rng.uniform(-1, 1, 90)
+    u = rng.uniform(-1, 1, t) + 1j * rng.uniform(-1, 1, t)
+    v = rng.uniform(-1, 1, t) + 1j * rng.uniform(-1, 1, t)
+    k1, k2, gap = api.cofactor_null_solve(np.convolve(l, u), np.convolve(l, v), t)
+    r1, r2, rg = oracle.cofactor_null_solve(np.convolve(l, u), np.convolve(l, v), t)
+    assert aligned(k1, k2, r1, r2) <= 1e-8 and abs(gap - rg) <= 1e-6 * rg
+    lat, pair, pub, prv = make(oracle, 72, 76, 1, 35, 71, 72)
+    P, Q = torch.from_numpy(pub).cuda(), torch.from_numpy(prv).cuda()
+    vals = [api.sample_cofactors(P, Q, 35, axis)[0] for axis in (0, 1)]
+    lam, mu, res = api.resolve_scales(vals[0], vals[1])
+    rl, rm, rr = oracle.resolve_scales(vals[0], vals[1])
+    assert aligned(lam, mu, rl, rm) <= 1e-9
+    A, B = api.complete_to_spectrum(vals[0], 0), api.complete_to_spectrum(vals[1], 1)
+    w = api.assemble_kernel(A, B, lam, mu)
+    assert np.abs(w - oracle.assemble_kernel(A, B, rl, rm)).max() <= 1e-9
+    assert krel(w, pair.k1) <= 1e-4
