@@ -201,9 +201,6 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   a.frames_per_slot = fps;
   if (fps > 1 && frames_per_group >= fps) frames_per_group -= frames_per_group % fps;  // groups start on a slot
   const int group_planes = frames_per_group * ch;
-  float2* X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * group_planes));
-  if (!X) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
-  a.X = X;
   a.x_plane = size_t(a.Hc) * a.xp;
   a.in_plane = in_plane_stride;
   a.out_plane = out_plane_stride;
@@ -216,6 +213,130 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   if (!a.S || !a.H) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
   if (int st = cuda_check(ctx, launch_wiener_tables(a, nslots, stream), "filter table launch")) return st;
   ctx->launches += 2;
+  // Fused persistent launch (one kernel for passes A, B, C over the whole batch, the
+  // spectrum in an L2-resident ring of plane slots), where the grid has a fused plan
+  static const bool fused_off = getenv("CBP_FUSED") == nullptr;  // measured slower: opt-in experiment
+  int nA = 0, nB = 0, nC = 0;
+  if (!fused_off && planes > 0 && deblur_fused_shape(a, nA, nB, nC)) {
+    static const int lag_b = getenv("CBP_FUSED_LAG") ? std::max(1, atoi(getenv("CBP_FUSED_LAG"))) : 2;
+    static const int ring_env = getenv("CBP_FUSED_RING") ? atoi(getenv("CBP_FUSED_RING")) : 0;
+    FusedCtl f{};
+    f.planes = planes;
+    f.lag_b = lag_b;
+    f.lag_c = 2 * lag_b;
+    f.ring = std::min(std::max(ring_env > 0 ? ring_env : f.lag_c + 2, f.lag_c + 2), planes);
+    f.nA = nA, f.nB = nB, f.nC = nC;
+    a.X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * f.ring));
+    unsigned* ctl = static_cast<unsigned*>(workspace(ctx, WS_FUSED, sizeof(unsigned) * (3 * size_t(planes) + 1)));
+    if (!a.X || !ctl) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+    f.ticket = ctl;
+    f.done = ctl + 1;
+    a.frame0 = 0;
+    a.in_vec2 = (reinterpret_cast<uintptr_t>(a.in) % 8 == 0) && a.in_ld % 2 == 0 && in_plane_stride % 2 == 0;
+    a.out_vec2 = (reinterpret_cast<uintptr_t>(a.out) % 8 == 0) && a.out_ld % 2 == 0 && out_plane_stride % 2 == 0;
+    a.in_vec4 = (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) && a.in_ld % 4 == 0 && in_plane_stride % 4 == 0;
+    cudaEvent_t* ev = nullptr;
+    if (ctx->prof) {
+      if (ctx->prof_used + 4 > int(ctx->prof_ev.size())) {
+        for (int k = 0; k < 256; ++k) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          ctx->prof_ev.push_back(e);
+        }
+      }
+      ev = &ctx->prof_ev[ctx->prof_used];
+      ctx->prof_used += 4;
+      ctx->prof_planes += planes;
+    }
+    cudaMemsetAsync(ctl, 0, sizeof(unsigned) * (3 * size_t(planes) + 1), stream);
+    if (ev) cudaEventRecord(ev[0], stream);
+    if (launch_deblur_fused(a, f, stream)) {
+      if (ev)  // one launch: the whole duration is reported as pass A, B and C as zero
+        for (int k = 1; k < 4; ++k) cudaEventRecord(ev[k], stream);
+      ++ctx->launches;
+      return cuda_check(ctx, cudaGetLastError(), "deconvolution launch");
+    }
+    if (ev) cudaEventRecord(ev[1], stream), cudaEventRecord(ev[2], stream), cudaEventRecord(ev[3], stream);
+  }
+  // Several launch groups in flight on side streams: each group's spectrum (1 frame by
+  // default) stays L2-resident between its passes, and the fill/drain of one group's
+  // persistent passes overlaps the passes of the group on the other stream.
+  static const int side_env = getenv("CBP_DEBLUR_STREAMS") ? atoi(getenv("CBP_DEBLUR_STREAMS")) : 1;
+  static const int group_mb = getenv("CBP_GROUP_MB") ? atoi(getenv("CBP_GROUP_MB")) : 28;
+  int ns = std::min(std::max(side_env, 1), cbp_ctx::kSideStreams);
+  int gp = group_planes;
+  if (ns > 1) {
+    const int fpg = std::max(1, int((size_t(std::max(group_mb, 1)) << 20) / (plane_bytes * ch)));
+    gp = std::min(fpg, std::max(frames, 1));
+    if (fps > 1 && gp >= fps) gp -= gp % fps;
+    gp *= ch;
+    if (planes <= gp) ns = 1, gp = group_planes;  // one group: no fork
+  }
+  for (int k = 0; ns > 1 && k < ns; ++k) {
+    if (!ctx->side[k] && cudaStreamCreateWithFlags(&ctx->side[k], cudaStreamNonBlocking) != cudaSuccess) ns = 1;
+    if (!ctx->side_ev[k] && cudaEventCreateWithFlags(&ctx->side_ev[k], cudaEventDisableTiming) != cudaSuccess) ns = 1;
+  }
+  if (ns > 1 && !ctx->side_ev[cbp_ctx::kSideStreams] &&
+      cudaEventCreateWithFlags(&ctx->side_ev[cbp_ctx::kSideStreams], cudaEventDisableTiming) != cudaSuccess)
+    ns = 1;
+  if (ns == 1) gp = group_planes;
+  float2* X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * gp * ns));
+  if (!X) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
+  a.X = X;
+  if (ns > 1) {
+    const int fpg = gp / ch;
+    cudaEvent_t* ev = nullptr;
+    if (ctx->prof) {
+      if (ctx->prof_used + 4 > int(ctx->prof_ev.size())) {
+        for (int k = 0; k < 256; ++k) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          ctx->prof_ev.push_back(e);
+        }
+      }
+      ev = &ctx->prof_ev[ctx->prof_used];
+      ctx->prof_used += 4;
+      ctx->prof_planes += planes;
+      cudaEventRecord(ev[0], stream);
+    }
+    cudaEventRecord(ctx->side_ev[cbp_ctx::kSideStreams], stream);  // fork: inputs and filter tables ready
+    for (int k = 0; k < ns; ++k) cudaStreamWaitEvent(ctx->side[k], ctx->side_ev[cbp_ctx::kSideStreams], 0);
+    const float* in0 = a.in;
+    float* out0 = a.out;
+    const cbp_kernel_slot* slot0 = a.slot;
+    float2* const H0 = a.H;
+    int used = 0;
+    for (int p0 = 0, g = 0; p0 < planes; p0 += gp, ++g) {
+      const int k = g % ns;
+      cudaStream_t sk = ctx->side[k];
+      used = std::max(used, k + 1);
+      const int np = std::min(gp, planes - p0);
+      a.in = in0 + size_t(p0) * in_plane_stride;
+      a.out = out0 + size_t(p0) * out_plane_stride;
+      const int s0 = a.slot_per_frame && fpg % fps == 0 ? (p0 / ch) / fps : 0;
+      a.slot = slot0 + s0;
+      a.H = H0 + size_t(s0) * (a.slot_per_frame ? a.h_frame : 0);
+      a.frame0 = a.slot_per_frame && fpg % fps != 0 ? p0 / ch : 0;
+      a.X = X + size_t(k) * gp * a.x_plane;
+      a.tile_ctr = ctx->tile_ctr && a.tile_ctr ? ctx->tile_ctr + 4 * k : nullptr;
+      a.in_vec2 = (reinterpret_cast<uintptr_t>(a.in) % 8 == 0) && a.in_ld % 2 == 0 && in_plane_stride % 2 == 0;
+      a.out_vec2 = (reinterpret_cast<uintptr_t>(a.out) % 8 == 0) && a.out_ld % 2 == 0 && out_plane_stride % 2 == 0;
+      a.in_vec4 = (reinterpret_cast<uintptr_t>(a.in) % 16 == 0) && a.in_ld % 4 == 0 && in_plane_stride % 4 == 0;
+      if (a.tile_ctr) cudaMemsetAsync(a.tile_ctr, 0, 3 * sizeof(unsigned), sk);
+      for (int pass = 0; pass < 3; ++pass) {
+        int st = cuda_check(ctx, launch_deblur_pass(a, np, pass, sk), "deconvolution launch");
+        if (st) return st;
+        ++ctx->launches;
+      }
+    }
+    for (int k = 0; k < used; ++k) {  // join
+      cudaEventRecord(ctx->side_ev[k], ctx->side[k]);
+      cudaStreamWaitEvent(stream, ctx->side_ev[k], 0);
+    }
+    if (ev)
+      for (int k = 1; k < 4; ++k) cudaEventRecord(ev[k], stream);
+    return 0;
+  }
   const float* in0 = a.in;
   float* out0 = a.out;
   const cbp_kernel_slot* slot0 = a.slot;
@@ -298,7 +419,8 @@ int cbp_create(int device, cbp_ctx** out) {
   }
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming);
-  if (cudaMalloc(&ctx->tile_ctr, 4 * sizeof(unsigned)) != cudaSuccess) ctx->tile_ctr = nullptr;  // static tiles then
+  if (cudaMalloc(&ctx->tile_ctr, 4 * cbp_ctx::kSideStreams * sizeof(unsigned)) != cudaSuccess)
+    ctx->tile_ctr = nullptr;  // static tiles then
   *out = ctx;
   return 0;
 }
@@ -316,6 +438,10 @@ void cbp_destroy(cbp_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
+  for (auto& st : ctx->side)
+    if (st) cudaStreamDestroy(st);
+  for (auto& e : ctx->side_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

@@ -15,8 +15,8 @@ struct cbp_ctx {
   std::string err;
   std::map<int, float2*> tw;  // n -> exp(-2 pi i k / n), k < n (device, FP64-rounded)
   // device workspaces, grown on demand (never inside a launch sequence)
-  void* ws[16] = {};
-  size_t ws_bytes[16] = {};
+  void* ws[20] = {};
+  size_t ws_bytes[20] = {};
   cbp_kernel_slot* host_slot = nullptr;  // pinned staging
   cudaEvent_t ev[8] = {};
   int num_sms = 148;
@@ -28,7 +28,12 @@ struct cbp_ctx {
   int prof_used = 0;
   long long prof_planes = 0;
   long long launches = 0;  // kernels enqueued by this context
-  unsigned* tile_ctr = nullptr;  // dynamic-tile counters of the deconvolution passes (device)
+  unsigned* tile_ctr = nullptr;  // dynamic-tile counters of the deconvolution passes (device), 4 per side stream
+  // side streams of the deconvolution (launch groups alternate between them, so one group's
+  // launch tails overlap the next group's passes); created on first use
+  static constexpr int kSideStreams = 4;
+  cudaStream_t side[kSideStreams] = {};
+  cudaEvent_t side_ev[kSideStreams + 1] = {};
   // stream ordering of the context's shared scratch: the last stream that enqueued work and
   // an event recorded there; a call on another stream first waits on it (StreamOrder)
   cudaEvent_t order_ev = nullptr;
@@ -93,6 +98,7 @@ enum Workspace {
   WS_QPUB = 13,   // dequantized frames (cbp_decode_frames_q)
   WS_QPRV = 14,
   WS_QCODES = 15, // host-pipeline code rings (cbp_decode_run_host_q)
+  WS_FUSED = 16,  // fused deconvolution ticket and per-plane completion counters
 };
 
 const char* errc_name(int status);

@@ -63,6 +63,17 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
 bool deblur_has_ct(int Gr, int Gc, int pass);
 bool ct_radices(int n, bool column, std::vector<int>& r);
 int ct_pos(const std::vector<int>& rad, int n);
+struct FusedCtl {
+  unsigned* ticket;  // [0]: next ticket (zeroed per launch)
+  unsigned* done;    // [0, P): A tiles done per plane, [P, 2P): B strips, [2P, 3P): C tiles
+  int planes, ring, lag_b, lag_c;
+  int nA, nB, nC;    // items per plane of each pass
+};
+
+// Fused persistent deconvolution (cbp_deblur_ct.cu): items per plane of each pass for this
+// grid (false: no fused plan), and the launch (false: this geometry cannot use it)
+bool deblur_fused_shape(const DeblurArgs& a, int& nA, int& nB, int& nC);
+bool launch_deblur_fused(const DeblurArgs& a, const FusedCtl& f, cudaStream_t stream);
 // Wiener filter tables of `frames` slots: S (column transforms) then H (cbp_deblur_ct.cu)
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s);
 

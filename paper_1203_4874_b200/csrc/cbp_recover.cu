@@ -1749,14 +1749,18 @@ __host__ inline size_t conv_smem(int t, int mode) {
 }
 
 // Per frame: fixed-order (deterministic) block reduction of the tile partials.
-__global__ void __launch_bounds__(256) k_resid_reduce(const double2* part, int ntiles, int channels,
+// `used` tiles per plane at a plane stride of `stride` partials: the summation order depends
+// on the frame geometry only (not on how many tile slots the workspace reserves), so every
+// entry point that validates a frame returns the same bits.
+__global__ void __launch_bounds__(256) k_resid_reduce(const double2* part, int stride, int used, int channels,
                                                       cbp_kernel_slot* slots, double* out, int batch) {
   const int b = blockIdx.x;
   if (slots && slots[b].status != 0) return;
   double num = 0.0, den = 0.0;
-  const int total = channels * ntiles;
+  const int total = channels * used;
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const double2 v = part[size_t(b) * total + i];
+    const int c = i / used, tile = i - c * used;
+    const double2 v = part[(size_t(b) * channels + c) * stride + tile];
     num += v.x;
     den += v.y;
   }
@@ -1797,26 +1801,21 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   a.mode = 0;
   a.part = reinterpret_cast<double2*>(part);
   a.ntiles = ntiles_max;
-  cudaMemsetAsync(part, 0, sizeof(double2) * size_t(ntiles_max) * ra.batch * ra.channels, s);
   // the latent extent depends on the device-side t; the kernel derives it from xr/xc
   a.xr = ra.rows;
   a.xc = ra.cols;
   a.ro = ra.rows;
   a.co = ra.cols;
-  dim3 g(ntiles_max, ra.batch * ra.channels);
-  static const bool two = !getenv("CBP_CONV_ONECOL") && conv_rows(1) == 32;
-  size_t sm = 0;  // the device-side width is <= t_max; tile heights vary with t
-  for (int t = 1; t <= std::min(ra.t_max, kWideMaxWidth); ++t) sm = std::max(sm, two ? conv2_smem(t) : conv_smem(t, 0));
-  if (two) {
-    if (cudaFuncSetAttribute(k_conv_resid2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
-      return cudaErrorInvalidValue;
-    k_conv_resid2<<<g, CONV2_THREADS, sm, s>>>(a);
-  } else {
-    if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
-      return cudaErrorInvalidValue;
-    k_conv_resid<<<g, 256, sm, s>>>(a);
-  }
-  k_resid_reduce<<<ra.batch, 256, 0, s>>>(a.part, ntiles_max, ra.channels, ra.slots, nullptr, ra.batch);
+  // k_conv_resid2 tiles are 32 rows x 64 columns for every width
+  const int used = ((ra.rows + 31) / 32) * ((ra.cols + VT_C - 1) / VT_C);
+  if (used > ntiles_max) return cudaErrorInvalidValue;
+  dim3 g(used, ra.batch * ra.channels);
+  size_t sm = 0;  // the device-side width is <= t_max
+  for (int t = 1; t <= std::min(ra.t_max, kWideMaxWidth); ++t) sm = std::max(sm, conv2_smem(t));
+  if (cudaFuncSetAttribute(k_conv_resid2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
+    return cudaErrorInvalidValue;
+  k_conv_resid2<<<g, CONV2_THREADS, sm, s>>>(a);
+  k_resid_reduce<<<ra.batch, 256, 0, s>>>(a.part, ntiles_max, used, ra.channels, ra.slots, nullptr, ra.batch);
   return cudaGetLastError();
 }
 
@@ -1847,7 +1846,7 @@ cudaError_t launch_validate_pair(const float* pub, const float* prv, int channel
   if (cudaFuncSetAttribute(k_conv_resid, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
   k_conv_resid<<<g, conv_rows(t) / conv_out(t) * VT_C, sm, s>>>(a);
-  k_resid_reduce<<<1, 256, 0, s>>>(a.part, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
+  k_resid_reduce<<<1, 256, 0, s>>>(a.part, nt, nt, channels, nullptr, part + 2 * size_t(nt) * channels, 1);
   return cudaGetLastError();
 }
 
