@@ -910,11 +910,12 @@ __device__ double sys_apply(const ComposeSmem& s, int t, const double2* x) {
   return v;
 }
 
-// resolve_completed (decoder.cpp:133-155) via the 2t x 2t Gram of the t^2 x 2t system
+// Fallback of resolve_cta for systems whose smallest singular value is not well separated
+// (inverse iteration would converge slowly): resolve_completed (decoder.cpp:133-155) via the 2t x 2t Gram of the t^2 x 2t system
 // plus direct-residual refinement. Returns 0 or CBP_REASON_SCALE_RATIO; x holds
 // [lambda; mu]; *residual = |sys x|, *ratio = min|x|/max|x|.
 template <int NMAX = 64>
-__device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* ratio) {
+__device__ int resolve_eig_cta(ComposeSmem& s, int t, double* residual, double* ratio) {
   const int n = 2 * t;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int j = idx / n, k = idx - j * n;
@@ -1039,35 +1040,343 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
   return (mx == 0.0 || mn < 1e-10 * mx) ? CBP_REASON_SCALE_RATIO : 0;
 }
 
-// realize_kernel (decoder.cpp:159-176) on s.K (t x t complex, serial on thread 0).
-// Returns 0 or a CBP_REASON_* of non_real_kernel; writes s.w.
-__device__ int realize_serial(ComposeSmem& s, int t, double max_imag, double neg_tol, double* value) {
-  double2 mass = make_double2(0.0, 0.0);
-  for (int i = 0; i < t * t; ++i) mass = zadd(mass, s.K[i]);
-  const double am = zabs(mass);
+// resolve_completed (decoder.cpp:133-155): the smallest right singular vector x = [lambda; mu]
+// of the t^2 x 2t system sys (row i*t+j: -B(i,j) in column i, A(i,j) in column t+j). Its
+// Gram is structured: G = [[D1, -C], [-C^H, D2]] with D1 = diag(sum_j |B_ij|^2),
+// D2 = diag(sum_i |A_ij|^2) and C_ij = conj(B_ij) A_ij, so (G + delta I) y = r is solved by
+// block elimination through the t x t Schur complement S = D2 + delta - C^H (D1 + delta)^-1 C
+// (one Cholesky on one warp) instead of a 2t x 2t eigendecomposition. Inverse iteration
+// with that solver finds the null direction; residual-corrected refinement with the direct
+// system (r = sys x, g = sys^H r, x -= P (G + delta I)^-1 g) then removes the squared
+// conditioning of the Gram, like the eigenbasis refinement it replaces.
+// Returns 0 or CBP_REASON_SCALE_RATIO; x holds [lambda; mu]; *residual = |sys x|,
+// *ratio = min|x| / max|x|.
+struct ResolveWarp {
+  double2* C;   // t x t, row i (lambda index), column j (mu index)
+  double2* L;   // t x t lower Cholesky factor of S (row-major)
+  double* e1;   // 1 / (D1_i + delta)
+  double* id;   // 1 / L_jj
+  double2* y;   // 2t work vector
+  double2* w;   // t work vector
+};
+
+// (G + delta I) y = r for r = [r1; r2] (2t), one warp: y may alias r.
+__device__ void resolve_solve(const ResolveWarp& W, int t, const double2* r, double2* y) {
+  const int lane = threadIdx.x & 31;
+  // w = r2 + C^H (E r1)
+  for (int j = lane; j < t; j += 32) {
+    double2 acc = r[t + j];
+    for (int i = 0; i < t; ++i) acc = zadd(acc, zscale(zcmul(W.C[i * t + j], r[i]), W.e1[i]));
+    W.w[j] = acc;
+  }
+  __syncwarp();
+  // forward: L z = w (in place in W.w; lane-parallel axpy after each pivot)
+  for (int k = 0; k < t; ++k) {
+    const double2 zk = zscale(W.w[k], W.id[k]);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < t; i += 32) W.w[i] = zsub(W.w[i], zmul(W.L[i * t + k], zk));
+    if (lane == 0) W.w[k] = zk;
+    __syncwarp();
+  }
+  // backward: L^H y2 = z
+  for (int k = t - 1; k >= 0; --k) {
+    const double2 yk = zscale(W.w[k], W.id[k]);
+    __syncwarp();
+    for (int i = lane; i < k; i += 32) W.w[i] = zsub(W.w[i], zcmul(W.L[k * t + i], yk));
+    if (lane == 0) W.w[k] = yk;
+    __syncwarp();
+  }
+  // y1 = E (r1 + C y2); y2 = w
+  for (int i = lane; i < t; i += 32) {
+    double2 acc = r[i];
+    for (int j = 0; j < t; ++j) acc = zadd(acc, zmul(W.C[i * t + j], W.w[j]));
+    W.y[i] = zscale(acc, W.e1[i]);
+  }
+  for (int j = lane; j < t; j += 32) W.y[t + j] = W.w[j];
+  __syncwarp();
+  for (int i = lane; i < 2 * t; i += 32) y[i] = W.y[i];
+  __syncwarp();
+}
+
+// warp-wide sums (one value per lane)
+__device__ __forceinline__ double warp_sum_w(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// x /= |x| (2t entries, one warp)
+__device__ __forceinline__ void resolve_normalize(double2* x, int n) {
+  const int lane = threadIdx.x & 31;
+  double s2 = 0.0;
+  for (int i = lane; i < n; i += 32) s2 += zabs2(x[i]);
+  const double inv = rsqrt(warp_sum_w(s2));
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) x[i] = zscale(x[i], inv);
+  __syncwarp();
+}
+
+// r = sys x into s.r (t^2), returns |r|^2; g = sys^H r (2t) if g != null. One warp.
+__device__ double resolve_residual(const ComposeSmem& s, int t, const double2* x, double2* g) {
+  const int lane = threadIdx.x & 31;
+  double loc = 0.0;
+  for (int idx = lane; idx < t * t; idx += 32) {
+    const int i = idx / t, j = idx - i * t;
+    const double2 u = zmul(s.B[idx], x[i]), v = zmul(s.A[idx], x[t + j]);
+    const double2 rr = make_double2(v.x - u.x, v.y - u.y);
+    s.r[idx] = rr;
+    loc += zabs2(rr);
+  }
+  const double tot = warp_sum_w(loc);
+  __syncwarp();
+  if (g) {
+    for (int j = lane; j < 2 * t; j += 32) {
+      double2 acc = make_double2(0.0, 0.0);
+      if (j < t) {
+        for (int jj = 0; jj < t; ++jj) acc = zsub(acc, zcmul(s.B[j * t + jj], s.r[j * t + jj]));
+      } else {
+        for (int ii = 0; ii < t; ++ii) acc = zadd(acc, zcmul(s.A[ii * t + (j - t)], s.r[ii * t + (j - t)]));
+      }
+      g[j] = acc;
+    }
+    __syncwarp();
+  }
+  return tot;
+}
+
+template <int NMAX = 64>
+__device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* ratio) {
+  const int n = 2 * t;
+  __shared__ int st_s;
+  __shared__ double res_s, ratio_s;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    ResolveWarp W;
+    W.C = s.G;
+    W.L = s.G + t * t;
+    W.y = s.coef;  // 2t
+    W.w = s.K;     // t (s.K is free until the assembly)
+    W.e1 = reinterpret_cast<double*>(s.V);
+    W.id = W.e1 + t;
+    double* d2 = W.id + t;
+    // diagonal blocks and their scale
+    double dmax = 0.0, dmin = 1e300;
+    for (int i = lane; i < t; i += 32) {
+      double a1 = 0.0, a2 = 0.0;
+      for (int k = 0; k < t; ++k) a1 += zabs2(s.B[i * t + k]), a2 += zabs2(s.A[k * t + i]);
+      W.e1[i] = a1;
+      d2[i] = a2;
+      dmax = fmax(dmax, fmax(a1, a2));
+      dmin = fmin(dmin, fmin(a1, a2));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+      dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    }
+    __syncwarp();
+    int st = 0;
+    if (!(dmin > 0.0)) {
+      // a zero column of sys: that unit vector is an exact null vector, min|x| = 0
+      int k0 = -1;
+      for (int i = 0; i < t && k0 < 0; ++i)
+        if (!(W.e1[i] > 0.0)) k0 = i;
+      for (int i = 0; i < t && k0 < 0; ++i)
+        if (!(d2[i] > 0.0)) k0 = t + i;
+      for (int i = lane; i < n; i += 32) s.x[i] = make_double2(i == k0 ? 1.0 : 0.0, 0.0);
+      __syncwarp();
+      st = CBP_REASON_SCALE_RATIO;
+    } else {
+      const double delta = 1e-13 * dmax;
+      for (int i = lane; i < t; i += 32) W.e1[i] = 1.0 / (W.e1[i] + delta);
+      for (int idx = lane; idx < t * t; idx += 32) W.C[idx] = zcmul(s.B[idx], s.A[idx]);
+      __syncwarp();
+      // S = D2 + delta - C^H E C (lower triangle, row-major)
+      for (int idx = lane; idx < t * t; idx += 32) {
+        const int j = idx / t, k = idx - j * t;
+        if (k > j) continue;
+        double2 acc = make_double2(j == k ? d2[j] + delta : 0.0, 0.0);
+        for (int i = 0; i < t; ++i)
+          acc = zsub(acc, zscale(zcmul(W.C[i * t + j], W.C[i * t + k]), W.e1[i]));
+        W.L[idx] = acc;
+      }
+      __syncwarp();
+      // Cholesky S = L L^H (right-looking, lanes on rows)
+      for (int k = 0; k < t; ++k) {
+        const double piv = fmax(W.L[k * t + k].x, 1e-300);
+        const double inv = rsqrt(piv);
+        __syncwarp();
+        for (int i = k + 1 + lane; i < t; i += 32) W.L[i * t + k] = zscale(W.L[i * t + k], inv);
+        if (lane == 0) {
+          W.L[k * t + k] = make_double2(piv * inv, 0.0);
+          W.id[k] = inv;
+        }
+        __syncwarp();
+        for (int i = k + 1 + lane; i < t; i += 32) {
+          const double2 lik = W.L[i * t + k];
+          for (int j = k + 1; j <= i; ++j) W.L[i * t + j] = zsub(W.L[i * t + j], zmul(lik, zconj(W.L[j * t + k])));
+        }
+        __syncwarp();
+      }
+      // inverse iteration from a generic start vector
+      for (int i = lane; i < n; i += 32) {
+        unsigned h = 0x9e3779b9u * unsigned(i + 1);
+        h ^= h << 13, h ^= h >> 17, h ^= h << 5;
+        s.x[i] = make_double2(1.0 + double(h & 0xffff) * (1.0 / 65536.0), 0.0);
+      }
+      __syncwarp();
+      // (until the direction settles: noisy systems have lambda_min / lambda_2 far from 0)
+      bool settled = false;
+      for (int it = 0; it < 16 && !settled; ++it) {
+        for (int i = lane; i < n; i += 32) s.g[i] = s.x[i];
+        __syncwarp();
+        resolve_solve(W, t, s.x, s.x);
+        resolve_normalize(s.x, n);
+        double pr = 0.0, pi = 0.0;  // |x_old^H x_new| -> 1
+        for (int i = lane; i < n; i += 32) {
+          const double2 u = zcmul(s.g[i], s.x[i]);
+          pr += u.x, pi += u.y;
+        }
+        pr = warp_sum_w(pr), pi = warp_sum_w(pi);
+        settled = 1.0 - sqrt(pr * pr + pi * pi) < 1e-13;  // angle ~4e-7: the refinement takes over
+      }
+      if (!settled) st = -1;  // poorly separated null direction: full eigendecomposition below
+      // residual-corrected refinement with the direct system: with rho = |sys x|^2 (the
+      // Rayleigh quotient of the exact Gram), x -= P (G + delta I)^-1 (sys^H sys x - rho x)
+      // contracts every other eigen-component by ~(lambda_min / lambda_k) per step
+      double c2 = 0.0;
+      for (int it = 0, more = settled; it < 6 && more; ++it) {
+        const double rho = resolve_residual(s, t, s.x, s.g);
+        for (int i = lane; i < n; i += 32) s.g[i] = zsub(s.g[i], zscale(s.x[i], rho));
+        __syncwarp();
+        resolve_solve(W, t, s.g, s.g);
+        double pr = 0.0, pi = 0.0;  // x^H c
+        for (int i = lane; i < n; i += 32) {
+          const double2 u = zcmul(s.x[i], s.g[i]);
+          pr += u.x, pi += u.y;
+        }
+        const double2 xc = make_double2(warp_sum_w(pr), warp_sum_w(pi));
+        c2 = 0.0;  // |P c|^2
+        for (int i = lane; i < n; i += 32) {
+          const double2 d = zsub(s.g[i], zmul(xc, s.x[i]));
+          c2 += zabs2(d);
+          s.x[i] = zsub(s.x[i], d);
+        }
+        c2 = warp_sum_w(c2);
+        __syncwarp();
+        resolve_normalize(s.x, n);
+        more = it < 1 || c2 > 1e-28;  // at least two steps, then until the correction vanishes
+      }
+      if (settled && c2 > 1e-20) st = -1;  // refinement did not converge: full eigendecomposition
+    }
+    // normalize_phase (poly.cpp:18-23): the first entry of largest modulus real positive
+    if (lane == 0) {
+      int im = 0;
+      double best = -1.0;
+      for (int i = 0; i < n; ++i) {
+        const double v = zabs(s.x[i]);
+        if (v > best) best = v, im = i;
+      }
+      const double a = zabs(s.x[im]);
+      if (a > 0.0) {
+        const double2 rot = zscale(zconj(s.x[im]), 1.0 / a);
+        for (int i = 0; i < n; ++i) s.x[i] = zmul(s.x[i], rot);
+      }
+    }
+    __syncwarp();
+    const double rr = sqrt(resolve_residual(s, t, s.x, nullptr));
+    double mx = 0.0, mn = 1e300;
+    for (int i = lane; i < n; i += 32) {
+      const double v = zabs(s.x[i]);
+      mx = fmax(mx, v);
+      mn = fmin(mn, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+      res_s = rr;
+      ratio_s = mx == 0.0 ? 0.0 : mn / mx;
+      st_s = st < 0 ? -1 : (st || mx == 0.0 || mn < 1e-10 * mx) ? CBP_REASON_SCALE_RATIO : 0;
+    }
+  }
+  __syncthreads();
+  if (st_s < 0) return resolve_eig_cta<NMAX>(s, t, residual, ratio);
+  *residual = res_s;
+  *ratio = ratio_s;
+  return st_s;
+}
+
+// Block-wide sums / extrema of one value pair per thread, in a fixed order (deterministic);
+// every thread gets the result. Contains __syncthreads.
+__device__ __forceinline__ double2 block_sum2(double a, double b) {
+  __shared__ double ra[32], rb[32];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) ra[warp] = a, rb[warp] = b;
+  __syncthreads();
+  double sa = 0.0, sb = 0.0;
+  for (int w = 0; w < nw; ++w) sa += ra[w], sb += rb[w];
+  return make_double2(sa, sb);
+}
+__device__ __forceinline__ double2 block_maxmin(double mx, double mn) {
+  __shared__ double ra[32], rb[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) ra[warp] = mx, rb[warp] = mn;
+  __syncthreads();
+  mx = -1e300, mn = 1e300;
+  for (int w = 0; w < nw; ++w) mx = fmax(mx, ra[w]), mn = fmin(mn, rb[w]);
+  return make_double2(mx, mn);
+}
+
+// realize_kernel (decoder.cpp:159-176) on s.K (t x t complex), whole CTA: rotate to a real
+// positive mass, check the imaginary energy and the negative weights, clamp, normalize.
+// Returns 0 or a CBP_REASON_* of non_real_kernel (uniform over the CTA); writes s.w.
+__device__ int realize_cta(ComposeSmem& s, int t, double max_imag, double neg_tol, double* value) {
+  const int tid = threadIdx.x, nt = blockDim.x, n2 = t * t;
+  double mr = 0.0, mi = 0.0;
+  for (int i = tid; i < n2; i += nt) mr += s.K[i].x, mi += s.K[i].y;
+  const double2 mass = block_sum2(mr, mi);
+  const double am = hypot(mass.x, mass.y);
   if (!(am > 0.0)) return CBP_REASON_VANISHING_MASS;
   const double2 rot = zscale(zconj(mass), 1.0 / am);
-  double total = 0.0, imag = 0.0;
-  for (int i = 0; i < t * t; ++i) {
-    s.K[i] = zmul(s.K[i], rot);
-    total += zabs2(s.K[i]);
-    imag += s.K[i].y * s.K[i].y;
+  double tot = 0.0, im = 0.0, mx = -1e300, mn = 1e300;
+  for (int i = tid; i < n2; i += nt) {
+    const double2 k = zmul(s.K[i], rot);
+    s.K[i] = k;
+    tot += zabs2(k);
+    im += k.y * k.y;
+    mx = fmax(mx, k.x);
+    mn = fmin(mn, k.x);
   }
-  if (!(total > 0.0)) return CBP_REASON_ZERO_KERNEL;
-  if (imag > max_imag * total) {
-    *value = imag / total;
+  const double2 ti = block_sum2(tot, im);
+  const double2 ext = block_maxmin(mx, mn);
+  if (!(ti.x > 0.0)) return CBP_REASON_ZERO_KERNEL;
+  if (ti.y > max_imag * ti.x) {
+    *value = ti.y / ti.x;
     return CBP_REASON_IMAG_ENERGY;
   }
-  double mx = -1e300, mn = 1e300;
-  for (int i = 0; i < t * t; ++i) mx = fmax(mx, s.K[i].x), mn = fmin(mn, s.K[i].x);
-  if (!(mx > 0.0)) return CBP_REASON_NO_POSITIVE;
-  if (mn < -neg_tol * mx) {
-    *value = mn / mx;
+  if (!(ext.x > 0.0)) return CBP_REASON_NO_POSITIVE;
+  if (ext.y < -neg_tol * ext.x) {
+    *value = ext.y / ext.x;
     return CBP_REASON_NEGATIVE_WEIGHT;
   }
-  double sum = 0.0;
-  for (int i = 0; i < t * t; ++i) sum += fmax(s.K[i].x, 0.0);
-  for (int i = 0; i < t * t; ++i) s.w[i] = fmax(s.K[i].x, 0.0) / sum;
+  double sm = 0.0;
+  for (int i = tid; i < n2; i += nt) sm += fmax(s.K[i].x, 0.0);
+  const double sum = block_sum2(sm, 0.0).x;
+  const double inv = 1.0 / sum;
+  for (int i = tid; i < n2; i += nt) s.w[i] = fmax(s.K[i].x, 0.0) * inv;
+  __syncthreads();
   return 0;
 }
 
@@ -1114,14 +1423,12 @@ __device__ int assemble_cta(ComposeSmem& s, int t, double max_imag, double neg_t
     }
     __syncthreads();
     ifft2_small(s, t);
-    if (threadIdx.x == 0) {
-      double v = 0.0;
-      int r = realize_serial(s, t, max_imag, neg_tol, &v);
-      if (r) {
-        st_s = CBP_NON_REAL_KERNEL, rs_s = r, val_s = v;
-      } else {
-        for (int i = 0; i < t * t; ++i) out[i] = pass == 0 ? 0.5 * s.w[i] : out[i] + 0.5 * s.w[i];
-      }
+    double v = 0.0;
+    const int r = realize_cta(s, t, max_imag, neg_tol, &v);
+    if (r) {
+      if (threadIdx.x == 0) st_s = CBP_NON_REAL_KERNEL, rs_s = r, val_s = v;
+    } else {
+      for (int i = threadIdx.x; i < t * t; i += blockDim.x) out[i] = pass == 0 ? 0.5 * s.w[i] : out[i] + 0.5 * s.w[i];
     }
     __syncthreads();
     if (st_s) {
