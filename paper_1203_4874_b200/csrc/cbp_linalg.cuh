@@ -130,15 +130,133 @@ static __device__ void herm_jacobi(double2* G, int ldg, double2* V, int ldv, int
 // mode: EIG_VALUES (eigenvalues only, bisection), EIG_QL (eigenvectors by implicit QL: exactly
 // orthogonal, robust for dense clusters of tiny eigenvalues), EIG_INVIT (eigenvectors by
 // inverse iteration: faster when the spectrum is well separated)
-enum EigMode { EIG_VALUES = 0, EIG_QL = 1, EIG_INVIT = 2 };
+// EIG_LOW2: eigenvalues 0, 1 and n-1 only (G[0][0], G[1][1], G[n-1][n-1]) and the eigenvectors
+// of the two smallest (V columns 0 and 1): the cofactor solve needs no more.
+// EIG_RATIO: G[0][0] <- min|lambda| / max|lambda| (0 if max|lambda| = 0), nothing else: the
+// singularity test of a Hermitian block (numerical_singularity, poly.cpp:81-91).
+enum EigMode { EIG_VALUES = 0, EIG_QL = 1, EIG_INVIT = 2, EIG_LOW2 = 3, EIG_RATIO = 4 };
 // NMAX: largest n (64; 128 for the kernels of widths t > 32, whose 2t x 2t Grams live in
 // global memory). EIG_INVIT needs n <= 64 (per-lane arrays); NMAX = 128 runs QL for it.
+// Shared state of the tridiagonal eigensolver (one instance per kernel and NMAX), so the
+// CTA-wide tridiagonalization and the one-warp remainder can be split.
+template <int NMAX>
+struct EigShared {
+  double d[NMAX], e[NMAX], beta[NMAX], rc[NMAX], rs[NMAX];
+  double2 ec[NMAX], w[NMAX], p[NMAX], delta[NMAX];
+};
+template <int NMAX>
+__device__ __forceinline__ EigShared<NMAX>& eig_shared() {
+  __shared__ EigShared<NMAX> st;
+  return st;
+}
+
+// Householder tridiagonalization G = Q T Q^H by the whole CTA (same outputs as the one-warp
+// loop in herm_eig_warp: v_k in column k below the diagonal, beta_k, the new subdiagonal
+// alpha_k, the diagonal): per step one warp forms the reflector, every warp takes a slice
+// of the rows for p = beta S v, and the rank-2 update S -= v w^H + w v^H is spread over the
+// CTA. Afterwards call herm_eig_warp(..., tri_done = true) on one warp. `part` is scratch for
+// n x n complex values (the partial sums of p).
 template <int NMAX = 64>
-static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, int mode) {
-  if (NMAX > 64 && mode == EIG_INVIT) mode = EIG_QL;
-  const bool vectors = mode != EIG_VALUES;
-  __shared__ double s_d[NMAX], s_e[NMAX], s_beta[NMAX], s_rc[NMAX], s_rs[NMAX];
-  __shared__ double2 s_ec[NMAX], s_w[NMAX], s_p[NMAX], s_delta[NMAX];
+__device__ void herm_tridiag_cta(double2* G, int ldg, int n, double2* part) {
+  EigShared<NMAX>& ES = eig_shared<NMAX>();
+  __shared__ double sc_beta;
+  __shared__ int sc_skip;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warps in the p = beta S v partial sums (more would cost warp 0 more partials to add)
+  const int nw = min(min(int(blockDim.x >> 5), 4), n);
+  const unsigned full = 0xffffffffu;
+  auto wsum = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(full, v, o);
+    return v;
+  };
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m = n - k - 1;
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int i = lane; i < m; i += 32) s2 += zabs2(G[(k + 1 + i) * ldg + k]);
+      s2 = wsum(s2);
+      const double2 x0 = G[(k + 1) * ldg + k];
+      const double xn = sqrt(s2);
+      __syncwarp();
+      if (lane == 0) {
+        ES.d[k] = G[k * ldg + k].x;
+        if (xn == 0.0) {
+          ES.beta[k] = 0.0, ES.ec[k] = make_double2(0.0, 0.0);
+          sc_skip = 1;
+        } else {
+          // rsqrt / rcp with Newton steps instead of hypot and divisions (FP64 division and
+          // hypot cost 130-160 cycles of latency on this serial chain)
+          const double a2 = zabs2(x0);
+          double ia = 0.0;
+          if (a2 > 0.0) {
+            ia = rsqrt(a2);
+            ia = ia * fma(-0.5 * a2 * ia, ia, 1.5);  // one Newton step
+          }
+          const double ax0 = a2 * ia;
+          const double2 ph = a2 > 0.0 ? zscale(x0, ia) : make_double2(1.0, 0.0);
+          const double den = xn * (xn + ax0);
+          double beta;  // 2 / |v|^2 = 1 / den
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(beta) : "d"(den));
+          beta = fma(beta, fma(-den, beta, 1.0), beta);
+          beta = fma(beta, fma(-den, beta, 1.0), beta);
+          G[(k + 1) * ldg + k] = zscale(ph, ax0 + xn);  // v_0 = x_0 - alpha
+          ES.beta[k] = beta;
+          ES.ec[k] = zscale(ph, -xn);  // alpha: the new subdiagonal entry
+          sc_beta = beta;
+          sc_skip = 0;
+        }
+      }
+    }
+    __syncthreads();
+    if (sc_skip) continue;  // uniform
+    const double beta = sc_beta;
+    // partial p_i = sum over this warp's rows j of conj(S[j][i]) v_j
+    if (warp < nw) {
+      const int j0 = (m * warp) / nw, j1 = (m * (warp + 1)) / nw;
+      for (int i = lane; i < m; i += 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int j = j0; j < j1; ++j) acc = zadd(acc, zcmul(G[(k + 1 + j) * ldg + k + 1 + i], G[(k + 1 + j) * ldg + k]));
+        part[warp * n + i] = acc;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double kr = 0.0, ki = 0.0;
+      for (int i = lane; i < m; i += 32) {
+        double2 acc = part[i];
+        for (int w = 1; w < nw; ++w) acc = zadd(acc, part[w * n + i]);
+        acc = zscale(acc, beta);
+        ES.p[i] = acc;
+        const double2 u = zcmul(G[(k + 1 + i) * ldg + k], acc);
+        kr += u.x;
+        ki += u.y;
+      }
+      const double2 K = zscale(make_double2(wsum(kr), wsum(ki)), 0.5 * beta);  // K = beta/2 v^H p
+      for (int i = lane; i < m; i += 32) ES.w[i] = zsub(ES.p[i], zmul(K, G[(k + 1 + i) * ldg + k]));
+    }
+    __syncthreads();
+    // S <- S - v w^H - w v^H
+    for (int idx = tid; idx < m * m; idx += blockDim.x) {
+      const int j = idx / m, i = idx - j * m;
+      const double2 vj = G[(k + 1 + j) * ldg + k], wj = ES.w[j];
+      const double2 vi = G[(k + 1 + i) * ldg + k], wi = ES.w[i];
+      double2& sji = G[(k + 1 + j) * ldg + k + 1 + i];
+      sji = zsub(sji, zadd(zmul(vj, zconj(wi)), zmul(wj, zconj(vi))));
+    }
+    __syncthreads();
+  }
+}
+
+template <int NMAX = 64>
+static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, int n, int mode,
+                                     bool tri_done = false) {
+  if (NMAX > 64 && (mode == EIG_INVIT || mode == EIG_LOW2)) mode = EIG_QL;
+  const bool low2 = mode == EIG_LOW2;
+  const bool vectors = mode != EIG_VALUES && mode != EIG_RATIO;
+  EigShared<NMAX>& ES = eig_shared<NMAX>();
+  double *s_d = ES.d, *s_e = ES.e, *s_beta = ES.beta, *s_rc = ES.rc, *s_rs = ES.rs;
+  double2 *s_ec = ES.ec, *s_w = ES.w, *s_p = ES.p, *s_delta = ES.delta;
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   auto wsum = [&](double v) {
@@ -149,7 +267,7 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
   const bool pw = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
   CBP_PHASE(30, pw);
   // ---- tridiagonalization G = Q T Q^H; v_k is kept in column k below the diagonal
-  for (int k = 0; k + 2 < n; ++k) {
+  for (int k = 0; k + 2 < n && !tri_done; ++k) {
     const int m = n - k - 1;
     double s2 = 0.0;
     for (int i = lane; i < m; i += 32) s2 += zabs2(G[(k + 1 + i) * ldg + k]);
@@ -268,6 +386,39 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
     r = fma(r, fma(-v, r, 1.0), r);
     return r;
   };
+  // Multisection: the warp splits into ng groups of lanes; group g refines eigenvalue kg
+  // (ascending index), each lane evaluating one interior point per step, so an interval
+  // shrinks (size+1)x per Sturm-count latency instead of 2x. Returns the group's eigenvalue
+  // (of the scaled T'). Warp-uniform (ballot); `its` steps reach the bisection's precision.
+  auto multisect = [&](int ng, int kg, int its) {
+    const int gsz = 32 / ng, grp = min(lane / gsz, ng - 1), g0 = grp * gsz;
+    const int size = grp == ng - 1 ? 32 - g0 : gsz, j = lane - g0;
+    double lo = lo0, hi = hi0;
+    for (int it = 0; it < its; ++it) {
+      const double w = (hi - lo) / double(size + 1);
+      const bool above = count_below(fma(double(j + 1), w, lo)) > kg;  // lambda_kg < x_j
+      const unsigned gb = (__ballot_sync(full, above) >> g0) & (size == 32 ? ~0u : ((1u << size) - 1u));
+      const int f = gb ? __ffs(gb) - 1 : size;  // first point above lambda_kg
+      const double nlo = f == 0 ? lo : fma(double(f), w, lo);
+      const double nhi = f == size ? hi : fma(double(f + 1), w, lo);
+      if (nhi - nlo < hi - lo) lo = nlo, hi = nhi;
+    }
+    return 0.5 * (lo + hi);
+  };
+  if (mode == EIG_RATIO) {
+    // min|lambda| / max|lambda| from four eigenvalues: the extremes and the two around 0
+    const int k0 = count_below(0.0);  // eigenvalues < 0
+    const int grp = lane >> 3;
+    const int kg = grp == 0 ? 0 : (grp == 1 ? n - 1 : (grp == 2 ? max(k0 - 1, 0) : min(k0, n - 1)));
+    const double lam = fabs(multisect(4, kg, 21));
+    const double l0 = __shfl_sync(full, lam, 0), l1 = __shfl_sync(full, lam, 8);
+    const double l2 = __shfl_sync(full, lam, 16), l3 = __shfl_sync(full, lam, 24);
+    const double mx = fmax(l0, l1), mn = fmin(l2, l3);
+    __syncwarp();
+    if (lane == 0) G[0] = make_double2(mx == 0.0 ? 0.0 : mn / mx, 0.0);
+    __syncwarp();
+    return;
+  }
   for (int k = lane; k < n && !vectors; k += 32) {
     double lo = lo0, hi = hi0;
     for (int it = 0; it < 62; ++it) {
@@ -383,6 +534,13 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
   // lane handles in turn, orthogonalizing each member against the previous ones (LAPACK
   // stein's scheme with a tighter cluster threshold: separated eigenvectors come out
   // orthogonal to ~1e-8 and accurate to ~1e-16 / gap).
+  if (low2) {
+    // three eigenvalues (k = 0, 1, n-1) by multisection: lanes 0-9, 10-19, 20-31
+    const int grp = min(lane / 10, 2);
+    const int k = grp == 0 ? 0 : (grp == 1 ? min(1, n - 1) : n - 1);
+    const double lam = multisect(3, k, 20);
+    if (lane == grp * 10 && (grp < 2 || k > 1)) s_p[k].x = lam;
+  } else {
   for (int k = lane; k < n; k += 32) {
     double lo = lo0, hi = hi0;
     for (int it = 0; it < 62; ++it) {  // to full precision: the shifts must resolve close pairs
@@ -393,13 +551,19 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
     }
     s_p[k].x = 0.5 * (lo + hi);  // ascending in k
   }
+  }
   __syncwarp();
   __shared__ int s_cl[65], s_ncl;
   if (lane == 0) {
     int nc = 0;
-    for (int k = 0; k < n; ++k)
-      if (k == 0 || s_p[k].x - s_p[k - 1].x > 1e-8) s_cl[nc++] = k;
-    s_cl[nc] = n;
+    const int nv = low2 ? min(n, 2) : n;  // eigenvectors wanted: 0 .. nv-1
+    // LOW2: the two vectors run in separate lanes unless their eigenvalues are within 1e-13
+    // of |T'| (inverse iteration at full-precision shifts still separates them by >= 1e6
+    // per step); otherwise members of a 1e-8 cluster share a lane and are orthogonalized
+    const double cl_tol = low2 ? 1e-13 : 1e-8;
+    for (int k = 0; k < nv; ++k)
+      if (k == 0 || s_p[k].x - s_p[k - 1].x > cl_tol) s_cl[nc++] = k;
+    s_cl[nc] = nv;
     s_ncl = nc;
   }
   __syncwarp();
@@ -469,6 +633,46 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
   for (int k = lane; k < n; k += 32) s_d[k] = s_p[k].x / sc;
   __syncwarp();
   CBP_PHASE(32, pw);
+  if (low2) {
+    // ---- the two wanted columns of V = Q D Z: reflectors in reverse order, lanes on rows
+    const int nv = min(n, 2);
+    for (int i = lane; i < n * nv; i += 32) {
+      const int r = i / nv, c = i - r * nv;
+      V[r * ldv + c] = zscale(s_delta[r], V[r * ldv + c].x);
+    }
+    __syncwarp();
+    for (int k = n - 3; k >= 0; --k) {
+      const double beta = s_beta[k];
+      if (beta == 0.0) continue;
+      const int m = n - k - 1;
+      double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+      for (int j = lane; j < m; j += 32) {
+        const double2 vj = G[(k + 1 + j) * ldg + k];
+        const double2 u0 = zcmul(vj, V[(k + 1 + j) * ldv + 0]);
+        a0r += u0.x, a0i += u0.y;
+        if (nv > 1) {
+          const double2 u1 = zcmul(vj, V[(k + 1 + j) * ldv + 1]);
+          a1r += u1.x, a1i += u1.y;
+        }
+      }
+      const double2 c0 = zscale(make_double2(wsum(a0r), wsum(a0i)), beta);
+      const double2 c1 = zscale(make_double2(wsum(a1r), wsum(a1i)), beta);
+      for (int j = lane; j < m; j += 32) {
+        const double2 vj = G[(k + 1 + j) * ldg + k];
+        V[(k + 1 + j) * ldv + 0] = zsub(V[(k + 1 + j) * ldv + 0], zmul(vj, c0));
+        if (nv > 1) V[(k + 1 + j) * ldv + 1] = zsub(V[(k + 1 + j) * ldv + 1], zmul(vj, c1));
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      G[0] = make_double2(s_d[0], 0.0);
+      if (n > 1) G[ldg + 1] = make_double2(s_d[1], 0.0);
+      G[(n - 1) * ldg + n - 1] = make_double2(s_d[n - 1], 0.0);
+    }
+    __syncwarp();
+    CBP_PHASE(33, pw);
+    return;
+  }
   // ---- eigenvectors V = Q D Z: Householders applied in reverse order, lanes on columns
   for (int i = lane; i < n * n; i += 32) {
     const int r = i / n, c = i - r * n;
@@ -491,6 +695,49 @@ static __device__ void herm_eig_warp(double2* G, int ldg, double2* V, int ldv, i
   for (int k = lane; k < n; k += 32) G[k * ldg + k] = make_double2(s_d[k], 0.0);
   __syncwarp();
   CBP_PHASE(33, pw);
+}
+
+// Cholesky A = L L^H of a Hermitian positive definite n x n matrix (lower triangle, row-major,
+// stride n), in place, by one warp (lanes on rows). id[k] = 1 / L_kk. A pivot that rounding
+// drove to <= 0 is floored (the factor then amplifies that direction, which inverse
+// iteration tolerates).
+__device__ __forceinline__ void warp_cholesky(double2* L, int n, double* id) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < n; ++k) {
+    const double piv = fmax(L[k * n + k].x, 1e-300);
+    const double inv = rsqrt(piv);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < n; i += 32) L[i * n + k] = zscale(L[i * n + k], inv);
+    if (lane == 0) {
+      L[k * n + k] = make_double2(piv * inv, 0.0);
+      id[k] = inv;
+    }
+    __syncwarp();
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      const double2 lik = L[i * n + k];
+      for (int j = k + 1; j <= i; ++j) L[i * n + j] = zsub(L[i * n + j], zmul(lik, zconj(L[j * n + k])));
+    }
+    __syncwarp();
+  }
+}
+
+// w <- A^-1 w with the factor from warp_cholesky, one warp (w in shared or global memory).
+__device__ __forceinline__ void warp_chol_solve(const double2* L, const double* id, int n, double2* w) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < n; ++k) {  // L z = w
+    const double2 zk = zscale(w[k], id[k]);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < n; i += 32) w[i] = zsub(w[i], zmul(L[i * n + k], zk));
+    if (lane == 0) w[k] = zk;
+    __syncwarp();
+  }
+  for (int k = n - 1; k >= 0; --k) {  // L^H y = z
+    const double2 yk = zscale(w[k], id[k]);
+    __syncwarp();
+    for (int i = lane; i < k; i += 32) w[i] = zsub(w[i], zcmul(L[k * n + i], yk));
+    if (lane == 0) w[k] = yk;
+    __syncwarp();
+  }
 }
 
 // eigenvalues only (G's diagonal), whole CTA

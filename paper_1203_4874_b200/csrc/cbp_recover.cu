@@ -364,18 +364,22 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
   for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) cplx |= A[idx].y != 0.0;
   cplx = __syncthreads_or(cplx);
   if (!cplx) {
+    // singular values = |eigenvalues|: CTA tridiagonalization, then min|lambda| / max|lambda|
+    // from four multisected eigenvalues (the extremes and the two around zero)
     double2* V = A + s * s;
-    herm_eigvals_cta(A, s, V, s, s);
-    for (int i = threadIdx.x; i < s; i += blockDim.x) sv[i] = fabs(A[i * s + i].x);
+    herm_tridiag_cta<64>(A, s, s, V);
+    if (threadIdx.x < 32) herm_eig_warp<64>(A, s, V, s, s, EIG_RATIO, true);
     __syncthreads();
+    CBP_PHASE(2, pw);
+    if (threadIdx.x == 0) a.ratios[(size_t(b) * 2 + axis) * a.nsizes + si] = A[0].x;
   } else {
     onesided_sv(A, s, s, sv, &flag);
-  }
-  CBP_PHASE(2, pw);
-  if (threadIdx.x == 0) {
-    double mx = 0.0, mn = 1e300;
-    for (int i = 0; i < s; ++i) mx = fmax(mx, sv[i]), mn = fmin(mn, sv[i]);
-    a.ratios[(size_t(b) * 2 + axis) * a.nsizes + si] = mx == 0.0 ? 0.0 : mn / mx;
+    CBP_PHASE(2, pw);
+    if (threadIdx.x == 0) {
+      double mx = 0.0, mn = 1e300;
+      for (int i = 0; i < s; ++i) mx = fmax(mx, sv[i]), mn = fmin(mn, sv[i]);
+      a.ratios[(size_t(b) * 2 + axis) * a.nsizes + si] = mx == 0.0 ? 0.0 : mn / mx;
+    }
   }
 }
 
@@ -450,6 +454,8 @@ cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
 struct SolveSmem {
   double2* G;     // n x n
   double2* V;     // n x n
+  double2* L;     // n x n Cholesky factor of G + delta I (refinement solves)
+  double* id;     // n: 1 / L_kk
   double2* corr;  // 4t-1 lags: pp[0..t-1], qq[0..t-1], pq[-(t-1)..t-1]
   double2* x;     // n
   double2* g;     // n
@@ -511,6 +517,21 @@ __device__ void apply_AH(const double2* p, int lp, const double2* q, int lq, int
   __syncthreads();
 }
 
+// normalize_phase (poly.cpp:18-23): the first entry of largest modulus made real positive.
+__device__ __forceinline__ void normalize_phase_serial(double2* x, int n) {
+  int im = 0;
+  double best = -1.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = zabs(x[i]);
+    if (v > best) best = v, im = i;
+  }
+  const double a = zabs(x[im]);
+  if (a > 0.0) {
+    const double2 rot = zscale(zconj(x[im]), 1.0 / a);
+    for (int i = 0; i < n; ++i) x[i] = zmul(x[i], rot);
+  }
+}
+
 struct SolveResult {
   double gap;
   int status;  // 0, CBP_REASON_GAP
@@ -569,6 +590,83 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
   }
   __syncthreads();
   CBP_PHASE(11, pw);
+  if constexpr (NMAX <= 64) {
+    // Warp 0: tridiagonalization, bisection for lambda_0, lambda_1, lambda_max, inverse
+    // iteration for the two smallest eigenvectors (EIG_LOW2). Warp 1 meanwhile factors
+    // G + delta I (Cholesky) for the refinement solves below.
+    __shared__ double dl_s;
+    if (tid == 0) {
+      double mx = 0.0;
+      for (int k = 0; k < n; ++k) mx = fmax(mx, sm.G[k * n + k].x);
+      dl_s = 1e-13 * mx;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += blockDim.x) {
+      const int j = idx / n, k = idx - j * n;
+      sm.L[idx] = j == k ? make_double2(sm.G[idx].x + dl_s, 0.0) : sm.G[idx];
+    }
+    __syncthreads();
+    herm_tridiag_cta<NMAX>(sm.G, n, n, sm.V);  // V: scratch until the eigenvectors
+    if (warp == 0) herm_eig_warp<NMAX>(sm.G, n, sm.V, n, n, EIG_LOW2, true);
+    if (warp == (nw > 1 ? 1 : 0)) warp_cholesky(sm.L, n, sm.id);
+    __syncthreads();
+    CBP_PHASE(12, pw);
+    const int R = max(lp, lq) + t - 1;
+    const double lmax = sm.G[(n - 1) * n + n - 1].x;
+    for (int i = tid; i < n; i += blockDim.x) sm.x[i] = sm.V[i * n + 0];
+    __syncthreads();
+    // residual-corrected refinement with the direct residual r = A x: with rho = |A x|^2,
+    // x -= P (G + delta I)^-1 (A^H A x - rho x) (P: projection off x) contracts the other
+    // eigen-components by ~lambda_min / lambda_k per step and undoes the Gram's squared
+    // conditioning (the eigenbasis form of this correction needed every eigenvector)
+    __shared__ double c2_s;
+    for (int it = 0; it < 6 && n > 1; ++it) {
+      const double rho = apply_A(p, lp, q, lq, t, sm.x, r, R, sm.red);
+      apply_AH(p, lp, q, lq, t, r, sm.g);
+      if (warp == 0) {
+        for (int i = lane; i < n; i += 32) sm.g[i] = zsub(sm.g[i], zscale(sm.x[i], rho));
+        __syncwarp();
+        warp_chol_solve(sm.L, sm.id, n, sm.g);
+        double pr = 0.0, pi = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          const double2 u = zcmul(sm.x[i], sm.g[i]);
+          pr += u.x, pi += u.y;
+        }
+        const double2 xc = make_double2(warp_sum(pr), warp_sum(pi));
+        double c2 = 0.0, s2 = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          const double2 d = zsub(sm.g[i], zmul(xc, sm.x[i]));
+          c2 += zabs2(d);
+          const double2 xn = zsub(sm.x[i], d);
+          sm.x[i] = xn;
+          s2 += zabs2(xn);
+        }
+        c2 = warp_sum(c2);
+        const double inv = rsqrt(warp_sum(s2));
+        __syncwarp();
+        for (int i = lane; i < n; i += 32) sm.x[i] = zscale(sm.x[i], inv);
+        if (lane == 0) c2_s = c2;
+      }
+      __syncthreads();
+      if (it >= 1) break;  // two steps (the correction reaches its rounding floor eps / gap^2)
+    }
+    CBP_PHASE(13, pw);
+    // gap = sigma_{2t-2} / sigma_0 (poly.cpp:105-110) with sigma_{2t-2} = |A v_2|
+    double sig2 = 0.0;
+    if (n >= 2) {
+      for (int i = tid; i < n; i += blockDim.x) sm.g[i] = sm.V[i * n + 1];
+      __syncthreads();
+      sig2 = sqrt(apply_A(p, lp, q, lq, t, sm.g, r, R, sm.red));
+    }
+    CBP_PHASE(14, pw);
+    const double sig0 = sqrt(fmax(lmax, 0.0));
+    SolveResult res;
+    res.gap = sig0 == 0.0 ? 0.0 : sig2 / sig0;
+    res.status = res.gap < gap_threshold ? CBP_REASON_GAP : 0;
+    if (tid == 0) normalize_phase_serial(sm.x, n);
+    __syncthreads();
+    return res;
+  }
   herm_jacobi_cta<NMAX>(sm.G, n, sm.V, n, n, sm.js, EIG_QL);  // smooth p, q: dense tiny eigenvalues
   CBP_PHASE(12, pw);
   __shared__ int kmin_s, k2_s;
@@ -663,8 +761,8 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
 
 __host__ __device__ inline size_t solve_smem_bytes(int t) {
   const int n = 2 * t;
-  return (size_t(2) * n * n + (4 * t - 1) + 3 * n + (n / 2 + 1)) * sizeof(double2) +
-         (32 + 2 * (n / 2 + 1)) * sizeof(double) + 16;
+  return (size_t(3) * n * n + (4 * t - 1) + 3 * n + (n / 2 + 1)) * sizeof(double2) +
+         (32 + n + 2 * (n / 2 + 1)) * sizeof(double) + 16;
 }
 
 __device__ SolveSmem carve_solve(void* base, int t) {
@@ -674,6 +772,8 @@ __device__ SolveSmem carve_solve(void* base, int t) {
   sm.G = z;
   z += n * n;
   sm.V = z;
+  z += n * n;
+  sm.L = z;
   z += n * n;
   sm.corr = z;
   z += 4 * t - 1;
@@ -688,6 +788,8 @@ __device__ SolveSmem carve_solve(void* base, int t) {
   double* d = reinterpret_cast<double*>(z);
   sm.red = d;
   d += 32;
+  sm.id = d;
+  d += n;
   sm.js.cs = d;
   d += n / 2 + 1;
   sm.js.sn = d;
@@ -1218,6 +1320,7 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
         }
         __syncwarp();
       }
+      CBP_PHASE(25, blockIdx.x == 0);
       // inverse iteration from a generic start vector
       for (int i = lane; i < n; i += 32) {
         unsigned h = 0x9e3779b9u * unsigned(i + 1);
@@ -1240,6 +1343,7 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
         pr = warp_sum_w(pr), pi = warp_sum_w(pi);
         settled = 1.0 - sqrt(pr * pr + pi * pi) < 1e-13;  // angle ~4e-7: the refinement takes over
       }
+      CBP_PHASE(22, blockIdx.x == 0);
       if (!settled) st = -1;  // poorly separated null direction: full eigendecomposition below
       // residual-corrected refinement with the direct system: with rho = |sys x|^2 (the
       // Rayleigh quotient of the exact Gram), x -= P (G + delta I)^-1 (sys^H sys x - rho x)
@@ -1265,9 +1369,9 @@ __device__ int resolve_cta(ComposeSmem& s, int t, double* residual, double* rati
         c2 = warp_sum_w(c2);
         __syncwarp();
         resolve_normalize(s.x, n);
-        more = it < 1 || c2 > 1e-28;  // at least two steps, then until the correction vanishes
+        more = it < 1;  // two steps (the correction reaches its rounding floor eps / gap^2)
       }
-      if (settled && c2 > 1e-20) st = -1;  // refinement did not converge: full eigendecomposition
+      if (settled && c2 > 1e-12) st = -1;  // refinement did not converge: full eigendecomposition
     }
     // normalize_phase (poly.cpp:18-23): the first entry of largest modulus real positive
     if (lane == 0) {

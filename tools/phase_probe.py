@@ -22,6 +22,6 @@ def d(a, b):
 print(json.dumps({
     "width_blocks_us": {"fill": d(0, 1), "eig": d(1, 2)},
     "solve_us": {"corr+gram": d(10, 11), "eig": d(11, 12), "refine": d(12, 13), "gap": d(13, 14)},
-    "compose_us": {"complete": d(20, 21), "resolve_fill": d(21, 25), "resolve_eig": d(25, 22),
-                   "resolve_rest": d(22, 23), "assemble": d(23, 24)},
+    "compose_us": {"complete": d(20, 21), "resolve_chol": d(21, 25), "resolve_invit": d(25, 22),
+                   "resolve_refine": d(22, 23), "assemble": d(23, 24)},
     "eig_last_us": {"tridiag": d(30, 31), "ql": d(31, 32), "back": d(32, 33)}}))
