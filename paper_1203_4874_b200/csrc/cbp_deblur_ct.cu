@@ -37,6 +37,9 @@ struct RowPlan {
   static constexpr bool RTW = RTW_;
   static constexpr int TWN = RTW_ ? L_ / 2 + 1 + TwUsed<L_, Rs>::count : 0;  // shared float2 entries
   static constexpr int L = L_;
+  // pass A row stride in the tile: rows 2j and 2j + 2 (read by one split warp) fall 16 banks
+  // apart only if the stride is 4 (mod 8) complex values, so L = 0 (mod 8) is padded
+  static constexpr int SPA = L_ % 8 == 0 ? L_ + 4 : L_;
   static constexpr int RPC = RPC_;
   static constexpr int NT = NT_;
   static constexpr bool PIPE = PIPE_;
@@ -83,9 +86,9 @@ __device__ __forceinline__ const cbp_kernel_slot* plane_slot(const DeblurArgs& a
 template <class P, bool BULK = false>
 __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a, int planes) {
   constexpr int NT = P::NT;
-  constexpr int L = P::L, RPC = P::RPC, TILE = RPC * L;
+  constexpr int L = P::L, RPC = P::RPC, SPA = P::SPA, TILE = RPC * SPA;
   using R = typename P::R;
-  using FFT = FftIP<L, RPC, L, 1, NT, false, P::RTW>;
+  using FFT = FftIP<L, RPC, SPA, 1, NT, false, P::RTW>;
   static_assert(!BULK || (P::PIPE && L % 2 == 0), "bulk rows need two buffers and 16-byte row starts");
   extern __shared__ __align__(16) float2 sm[];
   short* pos = reinterpret_cast<short*>(sm + (P::PIPE ? 2 : 1) * TILE);
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     const int nr = min(RPC, a.Mb - r0);
     fence_proxy_async();
     mbar_expect_tx(b, unsigned(nr) * row_bytes);
-    for (int s = 0; s < nr; ++s) bulk_g2s(dst + s * L, src + size_t(s) * a.in_ld, row_bytes, b);
+    for (int s = 0; s < nr; ++s) bulk_g2s(dst + s * SPA, src + size_t(s) * a.in_ld, row_bytes, b);
   };
   auto issue = [&](int tile, float2* dst) {
     const int p = tile / groups, r0 = (tile - p * groups) * RPC;
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
     for (int s = 0; s < RPC; ++s) {
       const bool ok = r0 + s < a.Mb;
       const float* row = src + size_t(s) * a.in_ld;
-      float2* d = dst + s * L;
+      float2* d = dst + s * SPA;
       if (v16) {
         const int full = ok ? a.Nb / 4 : 0;  // whole 16-byte chunks inside the row
 #pragma unroll 1
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_forward_ct(DeblurArgs a
       float2 xk[2], xc[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const float2* z = cur + (2 * j + h) * L;
+        const float2* z = cur + (2 * j + h) * SPA;
         const float2 zk = z[pk], zc = cconj(z[pc]);
         const float2 e = cscale(cadd(zk, zc), 0.5f);
         const float2 d = csub(zk, zc);
@@ -539,15 +542,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
       const int N = a.Nb - (a.Mb - M);  // Nb - t + 1
       float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
       if (a.out_vec2 && N % 2 == 0) {
-        const int h = N / 2;
-        for (int n = threadIdx.x; n < h; n += NT) {
-#pragma unroll
-          for (int s2 = 0; s2 < RPC; s2 += 2) {
-            const float4 z = reinterpret_cast<const float4*>(cur + n * RPC)[s2 / 2];
-            if (s2 < nrows) __stcs(reinterpret_cast<float2*>(dst + size_t(s2) * a.out_ld) + n, make_float2(z.x, z.y));
-            if (s2 + 1 < nrows)
-              __stcs(reinterpret_cast<float2*>(dst + size_t(s2 + 1) * a.out_ld) + n, make_float2(z.z, z.w));
-          }
+        // consecutive threads read consecutive 16-byte chunks (conflict-free shared loads):
+        // chunk f holds rows 2c, 2c+1 of column n (f = n * RPC/2 + c); each store instruction
+        // still writes 128-byte runs of two rows
+        constexpr int CH = RPC / 2;
+        const int nf = (N / 2) * CH;
+        for (int f = threadIdx.x; f < nf; f += NT) {
+          const int n = f / CH, s2 = 2 * (f - n * CH);
+          const float4 z = reinterpret_cast<const float4*>(cur)[f];
+          if (s2 < nrows) __stcs(reinterpret_cast<float2*>(dst + size_t(s2) * a.out_ld) + n, make_float2(z.x, z.y));
+          if (s2 + 1 < nrows)
+            __stcs(reinterpret_cast<float2*>(dst + size_t(s2 + 1) * a.out_ld) + n, make_float2(z.z, z.w));
         }
       } else {
         for (int s = 0; s < nrows; ++s)
@@ -702,7 +707,7 @@ bool rows_inverse_tmap(const DeblurArgs& a, int planes, CUtensorMap* map) {
 template <class P>
 void launch_rows(const DeblurArgs& a, int planes, bool inverse, cudaStream_t s) {
   constexpr int NB = P::PIPE ? 2 : 1;
-  const size_t smA = NB * size_t(P::RPC) * P::L * sizeof(float2) +
+  const size_t smA = NB * size_t(P::RPC) * P::SPA * sizeof(float2) +
                      (P::RTW ? size_t(P::TWN) * sizeof(float2) : P::L * sizeof(short));
   const size_t smC = NB * size_t(((P::L + 1) * P::RPC + 15) & ~15) * sizeof(float2) +
                      size_t(P::RTW ? P::TWN : (P::L + 3) / 4) * sizeof(float2) + 3 * sizeof(unsigned long long);
@@ -803,13 +808,43 @@ using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
 // 4K: Gc = 3888. Four rows per tile (one CTA of 512 threads per SM): a tile then writes whole
 // 32-byte XT sectors (4 rows of one frequency); with two rows per tile every pass-A store was
 // a half sector (pass A 41.4 -> 26.8 us per 4K plane)
-using Row1944 = RowPlan<1944, CBP_ROW1944_RPC, Radices<27, 8, 9>, CBP_ROW1944_RPC == 4 ? 512 : 256>;
+#ifndef CBP_ROW1944_NT
+#define CBP_ROW1944_NT (CBP_ROW1944_RPC == 4 ? 512 : 256)
+#endif
+#ifndef CBP_ROW1944_PIPE
+#define CBP_ROW1944_PIPE true
+#endif
+#ifndef CBP_ROW1944_MINB
+#define CBP_ROW1944_MINB 1
+#endif
+#ifndef CBP_ROW1944_RTW
+#define CBP_ROW1944_RTW false
+#endif
+// radices (27, 9, 8): the last radix 8 makes the digit-reversal stride N/8 = 243 odd, so the
+// split steps' pos(k) accesses of consecutive frequencies spread over the banks (with
+// (27, 8, 9) the stride 216 put every fourth frequency on one bank: 45% of the passes' shared
+// wavefronts were conflicts)
+using Row1944 = RowPlan<1944, CBP_ROW1944_RPC, Radices<27, 9, 8>, CBP_ROW1944_NT, CBP_ROW1944_PIPE, CBP_ROW1944_MINB,
+                        CBP_ROW1944_RTW>;
 using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
 using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
 using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;  // 1080p: Gr = 1120, filter from L2
 using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;        // staged filter strip
 using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false, 4, true>;
-using Col2187 = ColPlan<2187, 2, Radices<27, 9, 9>, 256>;  // 4K: Gr = 2187
+#ifndef CBP_COL2187_W
+#define CBP_COL2187_W 2
+#endif
+#ifndef CBP_COL2187_NT
+#define CBP_COL2187_NT 256
+#endif
+#ifndef CBP_COL2187_MINB
+#define CBP_COL2187_MINB 1
+#endif
+#ifndef CBP_COL2187_HD
+#define CBP_COL2187_HD false
+#endif
+using Col2187 = ColPlan<2187, CBP_COL2187_W, Radices<27, 9, 9>, CBP_COL2187_NT, true, CBP_COL2187_MINB,
+                        CBP_COL2187_HD>;  // 4K: Gr = 2187
 using Col490 = ColPlan<490, 8, Radices<35, 14>, 288, true, 2>;      // 640x480: Gr = 490
 using Col270 = ColPlan<270, 8, Radices<27, 10>, 224>;      // 256x256: Gr = 270
 
@@ -826,7 +861,7 @@ bool ct_radices(int n, bool column, std::vector<int>& r) {
   }
   switch (n) {
     case 972: r = {27, 36}; return true;
-    case 1944: r = {27, 8, 9}; return true;
+    case 1944: r = {27, 9, 8}; return true;
     case 324: r = {27, 12}; return true;
     case 135: r = {27, 5}; return true;
   }

@@ -606,14 +606,14 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
       sm.L[idx] = j == k ? make_double2(sm.G[idx].x + dl_s, 0.0) : sm.G[idx];
     }
     __syncthreads();
-    herm_tridiag_cta<NMAX>(sm.G, n, n, sm.V);  // V: scratch until the eigenvectors
-    if (warp == 0) herm_eig_warp<NMAX>(sm.G, n, sm.V, n, n, EIG_LOW2, true);
+    herm_tridiag_cta<NMAX>(sm.G, n, n, sm.V);  // V: scratch until the eigenvectors (4n partials)
+    if (warp == 0) herm_eig_warp<NMAX>(sm.G, n, sm.V, 2, n, EIG_LOW2, true);  // V: n x 2
     if (warp == (nw > 1 ? 1 : 0)) warp_cholesky(sm.L, n, sm.id);
     __syncthreads();
     CBP_PHASE(12, pw);
     const int R = max(lp, lq) + t - 1;
     const double lmax = sm.G[(n - 1) * n + n - 1].x;
-    for (int i = tid; i < n; i += blockDim.x) sm.x[i] = sm.V[i * n + 0];
+    for (int i = tid; i < n; i += blockDim.x) sm.x[i] = sm.V[i * 2 + 0];
     __syncthreads();
     // residual-corrected refinement with the direct residual r = A x: with rho = |A x|^2,
     // x -= P (G + delta I)^-1 (A^H A x - rho x) (P: projection off x) contracts the other
@@ -654,7 +654,7 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
     // gap = sigma_{2t-2} / sigma_0 (poly.cpp:105-110) with sigma_{2t-2} = |A v_2|
     double sig2 = 0.0;
     if (n >= 2) {
-      for (int i = tid; i < n; i += blockDim.x) sm.g[i] = sm.V[i * n + 1];
+      for (int i = tid; i < n; i += blockDim.x) sm.g[i] = sm.V[i * 2 + 1];
       __syncthreads();
       sig2 = sqrt(apply_A(p, lp, q, lq, t, sm.g, r, R, sm.red));
     }
@@ -759,22 +759,25 @@ __device__ SolveResult cofactor_solve_cta(const double2* p, int lp, const double
   return res;
 }
 
-__host__ __device__ inline size_t solve_smem_bytes(int t) {
+// full: V holds all n eigenvectors (the QL route of the wide solves, n x n); otherwise (the
+// EIG_LOW2 route) V is n x 2 plus the tridiagonalization's partial sums (4n entries).
+__host__ __device__ inline size_t solve_smem_bytes(int t, bool full = true) {
   const int n = 2 * t;
-  return (size_t(3) * n * n + (4 * t - 1) + 3 * n + (n / 2 + 1)) * sizeof(double2) +
+  return (size_t(2) * n * n + (full ? size_t(n) * n : 4 * size_t(n)) + (4 * t - 1) + 3 * n + (n / 2 + 1)) *
+             sizeof(double2) +
          (32 + n + 2 * (n / 2 + 1)) * sizeof(double) + 16;
 }
 
-__device__ SolveSmem carve_solve(void* base, int t) {
+__device__ SolveSmem carve_solve(void* base, int t, bool full = true) {
   const int n = 2 * t;
   SolveSmem sm;
   double2* z = static_cast<double2*>(base);
   sm.G = z;
   z += n * n;
-  sm.V = z;
-  z += n * n;
   sm.L = z;
   z += n * n;
+  sm.V = z;
+  z += full ? n * n : 4 * n;
   sm.corr = z;
   z += 4 * t - 1;
   sm.x = z;
@@ -842,7 +845,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo,
   if (slot->status != 0) return;
   const int t = slot->width;
   if (t <= t_lo || t > t_hi || t > kSolveMaxWidth || i >= t) return;
-  solve_slice<64>(a, b, axis, i, t, carve_solve(shs, t));
+  solve_slice<64>(a, b, axis, i, t, carve_solve(shs, t, false));
 }
 
 // Widths kSmemMaxWidth < t <= 63 (the reference's bound): the same solve with the 2t x 2t
@@ -884,9 +887,9 @@ cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
     dim3 g(tb, 2, a.batch);
     const int nt = nt_env ? nt_env : (size_t(2) * tb * a.batch > 2 * 148 ? 128 : 256);
     if (nt == 128)
-      k_solve<128><<<g, 128, solve_smem_bytes(tb), s>>>(a, lo, hi);
+      k_solve<128><<<g, 128, solve_smem_bytes(tb, false), s>>>(a, lo, hi);
     else
-      k_solve<256><<<g, 256, solve_smem_bytes(tb), s>>>(a, lo, hi);
+      k_solve<256><<<g, 256, solve_smem_bytes(tb, false), s>>>(a, lo, hi);
   }
   if (a.t_max > kSolveMaxWidth) {
     if (!a.wide) return cudaErrorInvalidValue;
@@ -902,7 +905,7 @@ __global__ void __launch_bounds__(256) k_cofactor_batch(const double2* P, int lp
                                                         size_t wstride) {
   extern __shared__ double2 shs[];
   const int b = blockIdx.x;
-  SolveSmem sm = carve_solve(wide ? wide + size_t(b) * wstride : shs, t);
+  SolveSmem sm = carve_solve(wide ? wide + size_t(b) * wstride : shs, t, NMAX > 64);
   SolveResult res = cofactor_solve_cta<NMAX>(P + size_t(b) * lp, lp, Q + size_t(b) * lq, lq, t, gap_threshold,
                                              scratch + size_t(b) * (max(lp, lq) + t), sm);
   for (int k = threadIdx.x; k < t; k += blockDim.x) {
@@ -926,7 +929,7 @@ cudaError_t launch_cofactor_batch(const double2* p, int lp, const double2* q, in
     k_cofactor_batch<128><<<batch, 256, 0, s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps, status, scratch, wide,
                                                 wide_scratch_elems());
   } else {
-    k_cofactor_batch<64><<<batch, 256, solve_smem_bytes(t), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
+    k_cofactor_batch<64><<<batch, 256, solve_smem_bytes(t, false), s>>>(p, lp, q, lq, t, gap_threshold, k1, k2, gaps,
                                                                  status, scratch, nullptr, 0);
   }
   return cudaGetLastError();
