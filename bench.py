@@ -393,6 +393,8 @@ def run_c3(args, world, rank, local):
     for s in range(E):
         pipe.run_steps(1, s)
     torch.cuda.synchronize(dev)
+    guard = {"epochs": E, "frames": E * EPOCH, "max_kernel_rel_err": 0.0, "min_latent_psnr_db": 1e9,
+             "max_validation_residual": 0.0}
     for e, sl in enumerate(api.read_slots(slots, E)):
         if sl.status != 0 or sl.width != T:
             raise RuntimeError(f"epoch {e}: recovery failed (status {sl.status}, width {sl.width})")
@@ -400,6 +402,21 @@ def run_c3(args, world, rank, local):
         err = np.linalg.norm(k - pairs[e].k1) / np.linalg.norm(pairs[e].k1)
         if err > 1e-4:
             raise RuntimeError(f"epoch {e}: kernel error {err:.2e}")
+        if not (0.0 <= sl.residual <= 1e-4):
+            raise RuntimeError(f"epoch {e}: validation residual {sl.residual:.3e}")
+        # every latent of the epoch (the recovery frame and the 29 deblurred ones, as the
+        # timed schedule produces them) against the synthetic ground truth: PSNR >= 40 dB
+        # (acceptance.cpp:78); the device regenerates the epoch's latents from their seed
+        lat = api.synth_frames(EPOCH * CH, ROWS, COLS, seed=api.frame_seed(1, epoch_seed(e, rank)))
+        lat = lat.view(EPOCH, CH, ROWS, COLS)
+        mse = ((out[e, :, :, :ROWS, :COLS] - lat) ** 2).flatten(1).mean(1)
+        psnr_min = float((10.0 * torch.log10(1.0 / mse.clamp_min(1e-30))).min())
+        del lat
+        if not psnr_min >= 40.0:
+            raise RuntimeError(f"epoch {e}: latent PSNR {psnr_min:.1f} dB against the ground truth")
+        guard["max_kernel_rel_err"] = max(guard["max_kernel_rel_err"], float(err))
+        guard["min_latent_psnr_db"] = min(guard["min_latent_psnr_db"], psnr_min)
+        guard["max_validation_residual"] = max(guard["max_validation_residual"], float(sl.residual))
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -525,7 +542,10 @@ def run_c3(args, world, rank, local):
                                  f"leaving {SM_RESERVE} SMs; pool of {E} epochs); steady state: the first "
                                  f"{REC_STREAMS} recoveries run before the timed region, each timed step issues 1 "
                                  f"recovery + 29 deblurs",
-                     "precision": "FP32 storage and deconvolution FFT; FP64 sampling, solves and validation"})
+                     "precision": "FP32 storage and deconvolution FFT; FP64 sampling, solves and validation",
+                     "guard": dict(guard, note="every pool epoch through the timed schedule before the region: "
+                                               "kernel vs truth <= 1e-4, residual <= 1e-4, every latent >= 40 dB "
+                                               "PSNR vs the synthetic ground truth")})
         print(json.dumps(line), flush=True)
 
 

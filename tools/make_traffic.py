@@ -1,14 +1,15 @@
 """profiles/deblur_traffic.json from an `ncu --set full` report of tools/prof_deblur.py
-(12 planes per launch): per-pass duration, DRAM bytes and instructions, and DRAM bytes per
-plane (bench.py reads `dram_bytes_per_plane` for roofline.traffic). Profiling aid.
-usage: make_traffic.py report.ncu-rep source-note"""
+(PLANES planes per launch, default 87 = bench.py's launches): per-pass duration, DRAM bytes
+and instructions, and DRAM bytes per plane (bench.py reads `dram_bytes_per_plane` for
+roofline.traffic). Profiling aid.
+usage: make_traffic.py report.ncu-rep source-note [planes]"""
 import csv, io, json, subprocess, sys
 
 rep, note = sys.argv[1], sys.argv[2]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
-PLANES = 12
+PLANES = int(sys.argv[3]) if len(sys.argv) > 3 else 87
 scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "B": 1e-6, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
 tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 out, tot = {}, 0.0
@@ -26,7 +27,7 @@ for r in rows[2:]:
                 "registers": int(float(d["launch__registers_per_thread"])),
                 "issue_active_pct": round(float(d["sm__inst_issued.avg.pct_of_peak_sustained_active"]), 1)}
     tot += (rd + wr) * 1e6
-res = {"source": note, "per_launch_12_planes": out, "dram_bytes_per_plane": int(tot / PLANES),
+res = {"source": note, f"per_launch_{PLANES}_planes": out, "dram_bytes_per_plane": int(tot / PLANES),
        "algorithmic_bytes_per_plane": 16709200,
        "note": "One launch per pass covers the whole batch, so the transposed half spectrum (8.5 MB per plane) "
                "round-trips through HBM: A writes it, B reads and rewrites it (the filter table is read from L2, "
