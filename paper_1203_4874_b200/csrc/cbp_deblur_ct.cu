@@ -327,8 +327,12 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
     mbar_init_fence();
   }
   __syncthreads();
+  // planes in reverse order: pass A wrote the last planes most recently, so the first strips
+  // read here still sit in L2 (and pass C, in forward order, starts on the planes this pass
+  // wrote last)
+  auto plane_of = [&](int tile) { return planes - 1 - tile / strips; };
   auto issue = [&](int tile, float2* dst, unsigned long long* b) {  // thread 0
-    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const int p = plane_of(tile), v0 = (tile % strips) * W;
     const float2* XT = a.X + size_t(p) * a.x_plane;
     const int nc = min(W, a.Hc - v0);
     fence_proxy_async();
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
   for (int it = 0; tile < total; ++it) {
     const int cb = it & 1;
     float2* cur = sm + cb * TILE;
-    const int p = tile / strips, v0 = (tile - p * strips) * W;
+    const int p = plane_of(tile), v0 = (tile % strips) * W;
     const int f = deblur_slot_index(a, p);
     const cbp_kernel_slot* slot = a.slot + f;
     const int status = slot->status;
@@ -590,10 +594,19 @@ __global__ void k_wiener_s(DeblurArgs a, int frames) {
 }
 
 // H[f][u][v] = conj(K)/(|K|^2 + eps) / (Gr*Gc), K(u,v) = sum_a S[v][a] exp(-2 pi i u a / Gr)
-// in FP64 (decoder.cpp:209-211, fft.cpp:268). Thread = one u and WH_V consecutive v: the
-// powers of W_Gr^u (recurrence from one sincos; drift ~t ulp, far below the float2 the
-// table is stored in) are shared by the WH_V sums. grid (ceil(Gr/128), ceil(Hc/WH_V), frames).
-constexpr int WH_V = 8;
+// in FP64 (decoder.cpp:209-211, fft.cpp:268). A thread owns WH_U table slots (rows u, at a
+// stride of the block size so stores stay coalesced) and WH_V consecutive v: per tap a it
+// reads WH_V values of S (shared-memory broadcasts) and updates WH_U x WH_V accumulators,
+// the powers of W_Gr^u advancing by one complex product per slot (recurrence from one
+// sincos; drift ~t ulp, far below the float2 the table is stored in).
+// grid (ceil(Gr / (128 WH_U)), ceil(Hc / WH_V), frames).
+#ifndef CBP_WH_V
+#define CBP_WH_V 8
+#endif
+#ifndef CBP_WH_U
+#define CBP_WH_U 1
+#endif
+constexpr int WH_V = CBP_WH_V, WH_U = CBP_WH_U;
 __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
   __shared__ double2 Ss[WH_V * CBP_MAX_WIDTH];
   const int f = blockIdx.z;
@@ -607,31 +620,50 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
     Ss[ai * WH_V + vv] = v0 + vv < a.Hc ? S[size_t(v0 + vv) * t + ai] : make_double2(0.0, 0.0);
   }
   __syncthreads();
-  // thread = table slot su (consecutive threads, consecutive addresses); u = the row whose
+  // thread = table slots su (consecutive threads, consecutive addresses); u = the row whose
   // filter value the column plan expects there (inverse of a.hpos, stored after it)
-  const int su = blockIdx.x * blockDim.x + threadIdx.x;
-  if (su >= a.Gr) return;
-  const int u = a.hpos ? int(a.hpos[a.Gr + su]) : su;
-  const double2 wu = zroot(u, a.Gr);
-  double2 w = make_double2(1.0, 0.0);
-  double2 acc[WH_V];
+  const int su0 = blockIdx.x * blockDim.x * WH_U + threadIdx.x;
+  if (su0 >= a.Gr) return;
+  double2 wu[WH_U], w[WH_U];
+  bool live[WH_U];
 #pragma unroll
-  for (int vv = 0; vv < WH_V; ++vv) acc[vv] = make_double2(0.0, 0.0);
+  for (int k = 0; k < WH_U; ++k) {
+    const int su = su0 + k * blockDim.x;
+    live[k] = su < a.Gr;
+    const int u = live[k] ? (a.hpos ? int(a.hpos[a.Gr + su]) : su) : 0;
+    wu[k] = zroot(u, a.Gr);
+    w[k] = make_double2(1.0, 0.0);
+  }
+  double2 acc[WH_U][WH_V];
+#pragma unroll
+  for (int k = 0; k < WH_U; ++k)
+#pragma unroll
+    for (int vv = 0; vv < WH_V; ++vv) acc[k][vv] = make_double2(0.0, 0.0);
   for (int ai = 0; ai < t; ++ai) {
+    double2 sv[WH_V];
 #pragma unroll
-    for (int vv = 0; vv < WH_V; ++vv) acc[vv] = zadd(acc[vv], zmul(Ss[ai * WH_V + vv], w));
-    w = zmul(w, wu);
+    for (int vv = 0; vv < WH_V; ++vv) sv[vv] = Ss[ai * WH_V + vv];
+#pragma unroll
+    for (int k = 0; k < WH_U; ++k) {
+#pragma unroll
+      for (int vv = 0; vv < WH_V; ++vv) acc[k][vv] = zadd(acc[k][vv], zmul(sv[vv], w[k]));
+      w[k] = zmul(w[k], wu[k]);
+    }
   }
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
   // transposed table HT[v][slot(u)]: slot(u) = pos(u) of the column plan (a.hpos), so pass B
   // multiplies element-wise in its DIF output order
-  float2* H = a.H + size_t(f) * a.h_frame + su;
 #pragma unroll
-  for (int vv = 0; vv < WH_V; ++vv) {
-    const int v = v0 + vv;
-    if (v < a.Hc) {
-      const double g = sc / (acc[vv].x * acc[vv].x + acc[vv].y * acc[vv].y + slot->epsilon);
-      H[size_t(v) * a.hp] = make_float2(float(acc[vv].x * g), float(-acc[vv].y * g));
+  for (int k = 0; k < WH_U; ++k) {
+    if (!live[k]) continue;
+    float2* H = a.H + size_t(f) * a.h_frame + su0 + k * blockDim.x;
+#pragma unroll
+    for (int vv = 0; vv < WH_V; ++vv) {
+      const int v = v0 + vv;
+      if (v < a.Hc) {
+        const double g = sc / (acc[k][vv].x * acc[k][vv].x + acc[k][vv].y * acc[k][vv].y + slot->epsilon);
+        H[size_t(v) * a.hp] = make_float2(float(acc[k][vv].x * g), float(-acc[k][vv].y * g));
+      }
     }
   }
 }
@@ -639,7 +671,7 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s) {
   dim3 g1((a.Hc * CBP_MAX_WIDTH + 255) / 256, frames);
   k_wiener_s<<<g1, 256, 0, s>>>(a, frames);
-  dim3 g2((a.Gr + 127) / 128, (a.Hc + WH_V - 1) / WH_V, frames);
+  dim3 g2((a.Gr + 128 * WH_U - 1) / (128 * WH_U), (a.Hc + WH_V - 1) / WH_V, frames);
   k_wiener_h<<<g2, 128, 0, s>>>(a, frames);
   return cudaGetLastError();
 }

@@ -469,20 +469,40 @@ __device__ __forceinline__ double2 ld_or0(const double2* v, int i, int len) {
 }
 
 // r = A x for x (length 2t in smem); returns |r|^2 (block-reduced), r stored in scratch.
+// A thread owns OUT consecutive rows: the operand windows p[nn - j], q[nn - j] of its rows
+// slide by one element per tap j, so each tap costs one load of p and one of q for OUT rows
+// (instead of one per row); terms outside the slices are zeros (same sums, same order).
 __device__ double apply_A(const double2* p, int lp, const double2* q, int lq, int t, const double2* x,
                           double2* r, int R, double* red) {
+  constexpr int OUT = 4;
   double loc = 0.0;
-  for (int nn = threadIdx.x; nn < R; nn += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    const int j0 = max(0, nn - max(lp, lq) + 1), j1 = min(t - 1, nn);
-    for (int j = j0; j <= j1; ++j) {
-      const double2 pv = ld_or0(p, nn - j, lp), qv = ld_or0(q, nn - j, lq);
-      const double2 a = zmul(pv, x[j]), c = zmul(qv, x[t + j]);
-      acc.x += a.x - c.x;
-      acc.y += a.y - c.y;
+  for (int n0 = threadIdx.x * OUT; n0 < R; n0 += blockDim.x * OUT) {
+    double2 acc[OUT], wp[OUT], wq[OUT];
+#pragma unroll
+    for (int o = 0; o < OUT; ++o) {
+      acc[o] = make_double2(0.0, 0.0);
+      wp[o] = ld_or0(p, n0 + o, lp);
+      wq[o] = ld_or0(q, n0 + o, lq);
     }
-    r[nn] = acc;
-    loc += zabs2(acc);
+    for (int j = 0; j < t; ++j) {
+      const double2 xj = x[j], yj = x[t + j];
+#pragma unroll
+      for (int o = 0; o < OUT; ++o) {
+        const double2 a = zmul(wp[o], xj), c = zmul(wq[o], yj);
+        acc[o].x += a.x - c.x;
+        acc[o].y += a.y - c.y;
+      }
+#pragma unroll
+      for (int o = OUT - 1; o > 0; --o) wp[o] = wp[o - 1], wq[o] = wq[o - 1];
+      wp[0] = ld_or0(p, n0 - j - 1, lp);
+      wq[0] = ld_or0(q, n0 - j - 1, lq);
+    }
+#pragma unroll
+    for (int o = 0; o < OUT; ++o)
+      if (n0 + o < R) {
+        r[n0 + o] = acc[o];
+        loc += zabs2(acc[o]);
+      }
   }
   loc = warp_sum(loc);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
