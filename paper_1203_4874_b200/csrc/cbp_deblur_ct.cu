@@ -858,7 +858,23 @@ using Row972c = RowPlan<972, 4, Radices<27, 36>, 160, false, 4>;
 // wavefronts were conflicts)
 using Row1944 = RowPlan<1944, CBP_ROW1944_RPC, Radices<27, 9, 8>, CBP_ROW1944_NT, CBP_ROW1944_PIPE, CBP_ROW1944_MINB,
                         CBP_ROW1944_RTW>;
-using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;      // 640x480: Gc = 648
+#ifndef CBP_C2_ROWS
+#define CBP_C2_ROWS 0
+#endif
+#if CBP_C2_ROWS == 1
+using Row324 = RowPlan<324, 8, Radices<27, 12>, 96, true, 4, true>;
+#elif CBP_C2_ROWS == 2
+using Row324 = RowPlan<324, 8, Radices<27, 12>, 128, true, 3, true>;
+#elif CBP_C2_ROWS == 3
+using Row324 = RowPlan<324, 4, Radices<27, 12>, 64, true, 6, true>;
+#elif CBP_C2_ROWS == 4
+using Row324 = RowPlan<324, 8, Radices<27, 12>, 224>;
+#else
+// 640x480: Gc = 648. 8 rows per tile on 3 warps (the 96 radix-27 butterflies of a tile, one
+// per thread), 3 CTAs per SM, stage twiddles in shared memory: 0.67 -> 0.55 us (A) and
+// 0.66 -> 0.50 us (C) per plane against 7 warps per tile, 1 CTA per SM
+using Row324 = RowPlan<324, 8, Radices<27, 12>, 96, true, 3, true>;
+#endif
 using Row135 = RowPlan<135, 8, Radices<27, 5>, 224>;       // 256x256: Gc = 270
 using Col1120 = ColPlan<1120, 4, Radices<35, 32>, 160, true, 3, true>;  // 1080p: Gr = 1120, filter from L2
 using Col1120a = ColPlan<1120, 4, Radices<35, 32>, 160, true, 2>;        // staged filter strip
@@ -877,7 +893,23 @@ using Col1120c = ColPlan<1120, 4, Radices<35, 32>, 160, false, 4, true>;
 #endif
 using Col2187 = ColPlan<2187, CBP_COL2187_W, Radices<27, 9, 9>, CBP_COL2187_NT, true, CBP_COL2187_MINB,
                         CBP_COL2187_HD>;  // 4K: Gr = 2187
-using Col490 = ColPlan<490, 8, Radices<35, 14>, 288, true, 2>;      // 640x480: Gr = 490
+#ifndef CBP_C2_COLS
+#define CBP_C2_COLS 0
+#endif
+#if CBP_C2_COLS == 1
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 288, true, 2>;
+#elif CBP_C2_COLS == 2
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 160, true, 3, true>;
+#elif CBP_C2_COLS == 3
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 128, true, 3>;
+#elif CBP_C2_COLS == 4
+using Col490 = ColPlan<490, 8, Radices<14, 35>, 288, true, 2>;
+#else
+// 640x480: Gr = 490. 8 columns per strip on 4 warps (the 112 radix-35 butterflies of the
+// fused filter stage fit one round), filter read from L2, 3 CTAs per SM: 0.91 -> 0.82 us per
+// plane against 9 warps per strip, 2 CTAs per SM with a staged filter strip
+using Col490 = ColPlan<490, 8, Radices<35, 14>, 128, true, 3, true>;
+#endif
 using Col270 = ColPlan<270, 8, Radices<27, 10>, 224>;      // 256x256: Gr = 270
 
 // Radix plans of the specialisations above (host mirror; DIT stage order).
@@ -886,7 +918,10 @@ bool ct_radices(int n, bool column, std::vector<int>& r) {
     switch (n) {
       case 1120: r = {35, 32}; return true;
       case 2187: r = {27, 9, 9}; return true;
-      case 490: r = {35, 14}; return true;
+      case 490:
+        if (CBP_C2_COLS == 4) r = {14, 35};
+        else r = {35, 14};
+        return true;
       case 270: r = {27, 10}; return true;
     }
     return false;
