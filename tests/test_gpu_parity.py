@@ -671,3 +671,48 @@ def test_wide_stage_entry_points(oracle, api):
     w = api.assemble_kernel(A, B, lam, mu)
     assert np.abs(w - oracle.assemble_kernel(A, B, rl, rm)).max() <= 1e-9
     assert krel(w, pair.k1) <= 1e-4
+
+
+@pytest.mark.parametrize("noise", [0.0, 1e-4, 1e-2, 0.3, 1.0])
+def test_resolve_scales_noisy_and_degenerate(oracle, api, noise):
+    """resolve_completed (decoder.cpp:133-155) on the device: Schur-complement inverse
+    iteration with direct-residual refinement, falling back to the full eigendecomposition
+    when the null direction is poorly separated (large noise). Planted scales
+    (decoder_test.cpp:158-177) plus noise of growing size: the smallest right singular
+    vector and the residual match the oracle's SVD."""
+    rng = np.random.default_rng(int(noise * 1e4) + 5)
+    for t in (3, 7, 11):
+        pair = oracle.generate_coprime_pair(t, 131 + t)
+        a = oracle.axis_roots_dft(pair.k1, 0, t)
+        b = oracle.axis_roots_dft(pair.k1, 1, t)
+        s = (0.5 + rng.random(t)) * np.exp(1j * rng.random(t) * 6)
+        r = (0.5 + rng.random(t)) * np.exp(1j * rng.random(t) * 6)
+        A = a * s[:, None] + noise * (rng.standard_normal((t, t)) + 1j * rng.standard_normal((t, t))) * np.abs(a).mean()
+        B = b * r[None, :] + noise * (rng.standard_normal((t, t)) + 1j * rng.standard_normal((t, t))) * np.abs(b).mean()
+        try:
+            rl, rm, rr = oracle.resolve_scales(A, B)
+        except oracle.OracleError as e:
+            with pytest.raises(api.CbpError) as ge:
+                api.resolve_scales(A, B)
+            assert ge.value.code == e.code
+            continue
+        lam, mu, res = api.resolve_scales(A, B)
+        tol = 1e-9 if noise < 1e-3 else 1e-7
+        assert aligned(lam, mu, rl, rm) <= tol, (t, noise)
+        assert abs(res - rr) <= tol * max(1.0, rr)
+    # zeroed slices (decoder_test.cpp degenerate cases): the same outcome as the oracle, an
+    # error with the same code or the same scales
+    pair = oracle.generate_coprime_pair(5, 121)
+    for axis, row in ((0, 0), (1, 2), (0, 4)):
+        a = oracle.axis_roots_dft(pair.k1, 0, 5)
+        b = oracle.axis_roots_dft(pair.k1, 1, 5)
+        (a if axis == 0 else b)[row] = 0
+        try:
+            rl, rm, rr = oracle.resolve_scales(a, b)
+        except oracle.OracleError as e:
+            with pytest.raises(api.CbpError) as ge:
+                api.resolve_scales(a, b)
+            assert ge.value.code == e.code == "DegenerateScales"
+            continue
+        lam, mu, res = api.resolve_scales(a, b)
+        assert aligned(lam, mu, rl, rm) <= 1e-9 and abs(res - rr) <= 1e-9
