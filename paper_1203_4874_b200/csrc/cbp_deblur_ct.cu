@@ -387,10 +387,9 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_cols_filter_bulk(DeblurArgs 
         phh ^= 1u;
         FFT::filter_stage(cur, Hs, R{});
       }
-      FFT::dit_tail(cur, a.twst_col, R{});
+      FFT::template dit_tail<true>(cur, a.twst_col, R{});  // every writer fences before the last barrier
       const int M = a.Mb - t + 1;  // even: Mb even, t odd
       if (threadIdx.x == 0) {
-        fence_proxy_async();
         float2* XT = a.X + size_t(p) * a.x_plane;
         for (int s = 0; s < nc; ++s) bulk_s2g(XT + size_t(v0 + s) * a.xp, cur + s * GP, unsigned(M) * 8u);
         bulk_commit();
@@ -1202,9 +1201,7 @@ __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a,
         const int t = slot->width;
         FFTB::dif_head_masked(buf, a.twst_col, 2 * a.Mb, RC{});
         FFTB::filter_stage_g(buf, a.H + size_t(fs) * a.h_frame + size_t(v0) * a.hp, a.hp, nc, RC{});
-        FFTB::dit_tail(buf, a.twst_col, RC{});
-        fence_proxy_async();  // every writer: its shared-memory writes before the bulk stores
-        __syncthreads();
+        FFTB::template dit_tail<true>(buf, a.twst_col, RC{});  // every writer fences before the last barrier
         if (threadIdx.x == 0) {
           const int M = a.Mb - t + 1;  // even: Mb even, t odd
           float2* XT = xt(p);

@@ -158,7 +158,9 @@ struct FftIP {
   // MASK (first DIF stage only): input element n of a sequence holds floats 2n, 2n+1 of a
   // real row of nf valid floats; floats >= nf are read as zero, so the tile's row tails
   // (and any rows past the frame, whose outputs are discarded) need no zeroing.
-  template <bool DIT, bool INV, int R, int PP, bool MASK = false>
+  // FENCE: every thread orders its shared-memory writes before later async-proxy (bulk
+  // copy) reads of them, ahead of the stage's closing barrier
+  template <bool DIT, bool INV, int R, int PP, bool MASK = false, bool FENCE = false>
   __device__ __forceinline__ static void stage(float2* buf, const float2* __restrict__ twst, int nf = 0) {
     constexpr int NB = N / R;
     static_assert(!MASK || (!DIT && PP > 1), "masked loads: first DIF stage of a multi-stage plan");
@@ -218,15 +220,16 @@ struct FftIP {
         for (int i = 0; i < R; ++i) sb[(base + i * PP) * ES] = v[i];
       }
     }
+    if constexpr (FENCE) fence_proxy_async();
     __syncthreads();
   }
 
-  template <bool INV, int PP>
+  template <bool INV, int PP, bool FENCE = false>
   __device__ __forceinline__ static void dit_impl(float2*, const float2*, Radices<>) {}
-  template <bool INV, int PP, int R, int... Rest>
+  template <bool INV, int PP, bool FENCE = false, int R, int... Rest>
   __device__ __forceinline__ static void dit_impl(float2* buf, const float2* tw, Radices<R, Rest...>) {
-    stage<true, INV, R, PP>(buf, tw);
-    dit_impl<INV, PP * R>(buf, tw + (R - 1) * (N / R), Radices<Rest...>{});
+    stage<true, INV, R, PP, false, FENCE && sizeof...(Rest) == 0>(buf, tw);
+    dit_impl<INV, PP * R, FENCE>(buf, tw + (R - 1) * (N / R), Radices<Rest...>{});
   }
   template <bool INV, int PP>
   __device__ __forceinline__ static void dif_impl(float2*, const float2*, Radices<>) {}
@@ -253,9 +256,11 @@ struct FftIP {
     static_assert(sizeof...(Rest) > 0, "masked head needs a second radix");
     dif_impl_m<false, R1>(buf, tw + (R1 - 1) * (N / R1), nf, Radices<Rest...>{});
   }
-  template <int R1, int... Rest>
+  // FENCE: the last stage fences every writer before its barrier (the tile then leaves
+  // shared memory by bulk copies)
+  template <bool FENCE = false, int R1, int... Rest>
   __device__ __forceinline__ static void dit_tail(float2* buf, const float2* tw, Radices<R1, Rest...>) {
-    dit_impl<true, R1>(buf, tw + (R1 - 1) * (N / R1), Radices<Rest...>{});
+    dit_impl<true, R1, FENCE>(buf, tw + (R1 - 1) * (N / R1), Radices<Rest...>{});
   }
   template <int R1, int... Rest>
   __device__ __forceinline__ static void filter_stage(float2* buf, const float2* hbuf, Radices<R1, Rest...>) {

@@ -2110,7 +2110,10 @@ __global__ void __launch_bounds__(CONV2_THREADS, 4) k_conv_resid2(ConvResidArgs 
   }
   const float* X = a.X + size_t(plane) * a.x_plane;
   const float* Y = a.Y + size_t(plane) * a.y_plane;
-  constexpr int LB = 8;
+  #ifndef CBP_CONV2_LB
+#define CBP_CONV2_LB 8
+#endif
+  constexpr int LB = CBP_CONV2_LB;
   for (int base = threadIdx.x; base < th * tw; base += LB * blockDim.x) {
     float xv[LB];
 #pragma unroll
