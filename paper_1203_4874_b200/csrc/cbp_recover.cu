@@ -246,7 +246,12 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
 // Sum the partials in a fixed order (Z1: row blocks of column n; Z2: column strips of row
 // m), then the t x t DFT epilogue: slice_i[x] = sum_r W(i, r) fold[r][x],
 // W(i, r) = exp(-2 pi i ((i r) mod t) / t) (fft.cpp:203-212). One launch for both axes:
-// blocks [0, ceil(cols/128)) do Z1, the rest Z2. grid (.., batch*2), smem t_max*128 doubles + roots.
+// blocks [0, ceil(cols/32)) do Z1, the rest Z2 (128 columns / rows per block). A Z1 block
+// owns 32 columns; its 4 warps sum interleaved quarters of the row blocks (loads batched 4
+// deep) and warp 0 adds the four quarter sums in a fixed order: the Z1 fold is a long sum
+// (~75 row blocks at 1080p) that one thread per column left latency-bound.
+// grid (.., batch*2), smem t_max*128 doubles + roots.
+constexpr int FD_Z1 = 32;  // columns per Z1 block
 __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
   extern __shared__ double sh[];
   const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
@@ -258,20 +263,46 @@ __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
   double* fold = sh + 2 * a.t_max;
   for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
   __syncthreads();
-  const int nb1 = (a.cols + 127) / 128;
+  const int nb1 = (a.cols + FD_Z1 - 1) / FD_Z1;
   const bool z1 = int(blockIdx.x) < nb1;
-  const int x = (z1 ? blockIdx.x : blockIdx.x - nb1) * blockDim.x + threadIdx.x;
-  if (x >= (z1 ? a.cols : a.rows)) return;
   if (z1) {
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;  // 4 quarter sums per column
+    const int x = blockIdx.x * FD_Z1 + lane;
     const int RB = fold_rows(t, a.fold_rh);
     const int nrb = (a.rows + RB - 1) / RB;
     const double* part = a.part + (size_t(b) * 2 + q) * a.part_stride + x;
+    double* quarter = fold + t * blockDim.x;  // [r][g][lane]
+    if (x < a.cols)
+      for (int r = 0; r < t; ++r) {
+        double acc = 0.0;
+#pragma unroll 4
+        for (int rb = g; rb < nrb; rb += 4) acc += part[(size_t(rb) * t + r) * a.cols];
+        quarter[(r * 4 + g) * 32 + lane] = acc;
+      }
+    __syncthreads();
+    if (g != 0 || x >= a.cols) return;
     for (int r = 0; r < t; ++r) {
-      double acc = 0.0;
-      for (int rb = 0; rb < nrb; ++rb) acc += part[(size_t(rb) * t + r) * a.cols];
-      fold[r * blockDim.x + threadIdx.x] = acc;
+      const double* qv = quarter + r * 4 * 32 + lane;
+      fold[r * blockDim.x + threadIdx.x] = (qv[0] + qv[32]) + (qv[64] + qv[96]);
     }
-  } else {
+    double2* out = a.slices + slice_offset(a, b, 0, q, 0) + x;
+    for (int i = 0; i < t; ++i) {
+      double re = 0.0, im = 0.0;
+      int idx = 0;
+      for (int r = 0; r < t; ++r) {
+        const double f = fold[r * blockDim.x + threadIdx.x];
+        re = fma(root[idx].x, f, re);
+        im = fma(root[idx].y, f, im);
+        idx += i;
+        if (idx >= t) idx -= t;
+      }
+      out[size_t(i) * a.lmax] = make_double2(re, im);
+    }
+    return;
+  }
+  const int x = (blockIdx.x - nb1) * blockDim.x + threadIdx.x;
+  if (x >= a.rows) return;
+  {
     const double* part = a.part2 + (size_t(b) * 2 + q) * a.ncb * size_t(a.t_max) * a.rows + x;
     for (int r = 0; r < t; ++r) {
       double acc = 0.0;
@@ -279,7 +310,7 @@ __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
       fold[r * blockDim.x + threadIdx.x] = acc;
     }
   }
-  double2* out = a.slices + slice_offset(a, b, z1 ? 0 : 1, q, 0) + x;
+  double2* out = a.slices + slice_offset(a, b, 1, q, 0) + x;
   for (int i = 0; i < t; ++i) {
     double re = 0.0, im = 0.0;
     int idx = 0;
@@ -308,8 +339,8 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
   });
   if (a.channels == 1) k_fold_tile<1><<<g1, 256, fold_smem<1>(), s>>>(a, t_fixed);
   else k_fold_tile<3><<<g1, 256, fold_smem<3>(), s>>>(a, t_fixed);
-  const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128) * sizeof(double);
-  dim3 g2((a.cols + 127) / 128 + (a.rows + 127) / 128, a.batch * 2);
+  const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128 * 2) * sizeof(double);  // folds + Z1 quarter sums
+  dim3 g2((a.cols + FD_Z1 - 1) / FD_Z1 + (a.rows + 127) / 128, a.batch * 2);
   k_fold_dft<<<g2, 128, smf, s>>>(a, t_fixed);
   return cudaGetLastError();
 }
@@ -385,21 +416,40 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
 
 // Per frame: all-zero check, first singular size per axis, axis agreement
 // (decoder.cpp:38-44, 83-89).
-__global__ void __launch_bounds__(128) k_width_pick(RecoverArgs a) {
+__global__ void __launch_bounds__(512) k_width_pick(RecoverArgs a) {
   const int b = blockIdx.x;
   cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0 || slot->width > 0) return;
   __shared__ int nz[4];
-  if (threadIdx.x < 4) nz[threadIdx.x] = 0;
-  __syncthreads();
-  for (int axis = 0; axis < 2; ++axis) {
-    const int L = axis == 0 ? a.cols : a.rows;
-    for (int q = 0; q < 2; ++q) {
-      const double2* v = a.slices + slice_offset(a, b, axis, q, 0);
-      bool any = false;
-      for (int i = threadIdx.x; i < L; i += blockDim.x) any |= (v[i].x != 0.0 || v[i].y != 0.0);
-      if (__syncthreads_or(any) && threadIdx.x == 0) nz[axis * 2 + q] = 1;
-    }
+  // all-zero test of the four DC slices in one pass: every thread's loads of all four are
+  // in flight together (the four dependent loops before took ~30 us of load latency)
+  bool any[4] = {false, false, false, false};
+  constexpr int U = 4;
+  const double2* v[4];
+  int len[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = a.slices + slice_offset(a, b, k >> 1, k & 1, 0);
+    len[k] = (k >> 1) == 0 ? a.cols : a.rows;
+  }
+  for (int i0 = threadIdx.x; i0 < max(a.rows, a.cols); i0 += U * blockDim.x) {
+    double2 x[4][U];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        x[k][u] = i < len[k] ? v[k][i] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int u = 0; u < U; ++u) any[k] |= (x[k][u].x != 0.0 || x[k][u].y != 0.0);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = __syncthreads_or(any[k]);
+    if (threadIdx.x == 0) nz[k] = r ? 1 : 0;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -440,7 +490,7 @@ cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   });
   k_width_blocks<<<g, 512, sm, s>>>(a);
-  k_width_pick<<<a.batch, 128, 0, s>>>(a);
+  k_width_pick<<<a.batch, 512, 0, s>>>(a);
   return cudaGetLastError();
 }
 
