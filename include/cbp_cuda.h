@@ -354,6 +354,10 @@ int cbp_copy_to_host(cbp_ctx* ctx, void* host, const void* dev, size_t bytes);
  * video pipeline) can leave `sms` SMs to that stream. No reference counterpart
  * (the reference parallelizes frames over host threads, tools/cbp.cpp:141-164). */
 int cbp_set_sm_reserve(cbp_ctx* ctx, int sms);
+/* Programmatic dependent launch of the context's small latency-chain kernels (kernel
+ * recovery, Wiener tables, validation reduction): on (default) each kernel is scheduled as
+ * its predecessor drains instead of after it (c1 decode_frame 0.290 -> 0.255 ms). */
+int cbp_set_launch_chaining(cbp_ctx* ctx, int on);
 
 /* ---- instrumentation ----------------------------------------------------------
  * Kernels enqueued by this context so far; optional CUDA-event timing of the three

@@ -117,6 +117,7 @@ _SIGS = {
     "cbp_launch_count": (C.c_longlong, [_P]),
     "cbp_profile": (_I, [_P, _I]),
     "cbp_set_sm_reserve": (_I, [_P, _I]),
+    "cbp_set_launch_chaining": (_I, [_P, _I]),
     "cbp_profile_read": (_I, [_P, _P, _P, _P]),
 }
 

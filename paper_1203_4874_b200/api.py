@@ -712,6 +712,13 @@ def set_sm_reserve(sms: int, ctx: N.Context | None = None, device: int | None = 
     ctx.check(N.lib().cbp_set_sm_reserve(ctx.ptr, int(sms)))
 
 
+def set_launch_chaining(on: bool, ctx: N.Context | None = None, device: int | None = None):
+    """cbp_set_launch_chaining: programmatic dependent launch of this context's small
+    latency-chain kernels (default on)."""
+    ctx = ctx or context(device)
+    ctx.check(N.lib().cbp_set_launch_chaining(ctx.ptr, int(bool(on))))
+
+
 def profile(enable: bool, device: int | None = None):
     N.lib().cbp_profile(context(device).ptr, int(enable))
 

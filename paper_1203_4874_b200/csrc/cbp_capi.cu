@@ -9,6 +9,13 @@
 
 using namespace cbp_dev;
 
+namespace cbp_dev {
+bool pdl_enabled() {
+  static const bool on = getenv("CBP_NO_PDL") == nullptr;  // A/B switch
+  return on;
+}
+}  // namespace cbp_dev
+
 namespace cbp_host {
 
 const char* errc_name(int status) {  // error.cpp:5-27, status = 1 + Errc
@@ -167,6 +174,7 @@ int deblur_setup(cbp_ctx* ctx, int Mb, int Nb, DeblurArgs& a) {
   a.rows_per_cta = rpc;
   a.col_width = deblur_col_width(a.Gr, CBP_MAX_WIDTH);
   a.sm_reserve = ctx->sm_reserve;
+  a.chain = ctx->chain;
   a.tw_row = twiddles(ctx, L);
   a.tw_post = twiddles(ctx, a.Gc);
   a.tw_col = twiddles(ctx, a.Gr);
@@ -448,6 +456,13 @@ void cbp_destroy(cbp_ctx* ctx) {
 const char* cbp_last_error(const cbp_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 long long cbp_launch_count(const cbp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cbp_set_launch_chaining(cbp_ctx* ctx, int on) {
+  cbp_host::DeviceGuard device_guard(ctx);
+  if (!ctx) return CBP_INVALID_ARGUMENT;
+  ctx->chain = on ? 1 : 0;
+  return 0;
+}
 
 int cbp_set_sm_reserve(cbp_ctx* ctx, int sms) {
   cbp_host::DeviceGuard device_guard(ctx);

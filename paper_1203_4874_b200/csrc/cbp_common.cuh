@@ -25,6 +25,40 @@ inline int current_device() {
     std::call_once(cbp_once_[cbp_dev::current_device()], [&] __VA_ARGS__); \
   } while (0)
 
+// Programmatic dependent launch for the latency-bound recovery chain (a dozen dependent
+// kernels of one or a few CTAs each): kernels launched with launch_chain may be scheduled
+// while their predecessor in the stream still runs; pdl_enter() (first statement of every
+// such kernel) waits for the predecessor's completion and memory (griddepcontrol.wait, a
+// no-op for ordinary launches), so the next kernel is scheduled as this one drains and the
+// launch latency of each link overlaps the previous kernel instead of adding to the chain
+// (c1 decode latency 0.290 -> 0.255 ms). cbp_set_launch_chaining turns it off per context.
+__device__ __forceinline__ void pdl_enter() {
+  // no early griddepcontrol.launch_dependents: the implicit trigger at CTA exit already
+  // overlaps the dependent's launch with the predecessor's drain, while an early trigger
+  // makes the dependents resident (holding registers and shared memory) during the whole
+  // predecessor (c4 batch of 4: 2.12k vs 2.30k frames/s; c1 0.260 vs 0.255 ms)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+bool pdl_enabled();  // CBP_NO_PDL unset (cbp_capi.cu)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_chain(void (*kernel)(KArgs...), bool chain, dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  // only small grids launch early: the waiting CTAs of a large one would hold SM slots that
+  // a concurrent stream's kernels (the video pipeline's deconvolution) could use
+  const unsigned blocks = grid.x * grid.y * grid.z;
+  cfg.numAttrs = chain && pdl_enabled() && blocks <= 2 * 148 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ---------------------------------------------------------------- complex math
 __host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }

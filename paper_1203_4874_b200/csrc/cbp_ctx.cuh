@@ -21,6 +21,7 @@ struct cbp_ctx {
   cudaEvent_t ev[8] = {};
   int num_sms = 148;
   int sm_reserve = 0;  // cbp_set_sm_reserve
+  int chain = 1;       // cbp_set_launch_chaining
   void* slot_event = nullptr;  // cudaEvent_t recorded when the kernel slots are final (_async_ev)
   // optional per-pass timing of the deconvolution (cbp_profile)
   int prof = 0;

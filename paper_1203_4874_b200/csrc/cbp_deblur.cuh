@@ -28,6 +28,7 @@ struct DeblurArgs {
   int variant;      // kernel configuration variant (CBP_FFT_VARIANT), 0 = default
   int col_width;    // pass B columns per CTA
   int sm_reserve;   // SMs the persistent passes leave free (cbp_set_sm_reserve)
+  int chain;        // programmatic dependent launch of the Wiener table kernels
   const cbp_kernel_slot* slot;
   int slot_per_frame;  // 1: slot[p / channels]; 0: slot[0] for every plane
   int channels;

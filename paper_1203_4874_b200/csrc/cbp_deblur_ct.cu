@@ -574,6 +574,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) k_rows_inverse_ct(DeblurArgs a
 // --------------------------------------------- Wiener filter tables (per slot)
 // S[f][v][a] = sum_b w[a][b] exp(-2 pi i v b / Gc)  (FP64)
 __global__ void k_wiener_s(DeblurArgs a, int frames) {
+  pdl_enter();
   const int f = blockIdx.y;
   const cbp_kernel_slot* slot = a.slot + f;
   if (slot->status != 0) return;
@@ -608,6 +609,7 @@ __global__ void k_wiener_s(DeblurArgs a, int frames) {
 constexpr int WH_V = CBP_WH_V, WH_U = CBP_WH_U;
 __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
   __shared__ double2 Ss[WH_V * CBP_MAX_WIDTH];
+  pdl_enter();
   const int f = blockIdx.z;
   const cbp_kernel_slot* slot = a.slot + f;
   if (slot->status != 0) return;
@@ -669,9 +671,9 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
 
 cudaError_t launch_wiener_tables(const DeblurArgs& a, int frames, cudaStream_t s) {
   dim3 g1((a.Hc * CBP_MAX_WIDTH + 255) / 256, frames);
-  k_wiener_s<<<g1, 256, 0, s>>>(a, frames);
+  launch_chain(k_wiener_s, a.chain != 0, g1, dim3(256), 0, s, a, frames);
   dim3 g2((a.Gr + 128 * WH_U - 1) / (128 * WH_U), (a.Hc + WH_V - 1) / WH_V, frames);
-  k_wiener_h<<<g2, 128, 0, s>>>(a, frames);
+  launch_chain(k_wiener_h, a.chain != 0, g2, dim3(128), 0, s, a, frames);
   return cudaGetLastError();
 }
 

@@ -146,6 +146,7 @@ int plan_recover(cbp_ctx* ctx, RecoverPlan& P, const float* pub, const float* pr
   a.search_max = smax;
   a.nsizes = smax >= smin ? (smax - smin) / 2 + 1 : 0;
   a.tau = tau;
+  a.chain = ctx->chain;
   a.trust_hint = trust_hint;
   a.gap_threshold = cfg ? cfg->gap_threshold : 1e-9;
   a.max_imag_energy = cfg ? cfg->max_imag_energy : 0.01;

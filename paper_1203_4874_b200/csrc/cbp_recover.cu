@@ -16,6 +16,7 @@ constexpr int kSolveMaxWidth = kSmemMaxWidth;  // 2t x 2t complex Gram + eigenve
 
 // ----------------------------------------------------------------- slots
 __global__ void k_init_slots(RecoverArgs a, HintChunk hc) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= hc.count) return;
   const int b = hc.first + j;
@@ -43,7 +44,7 @@ cudaError_t launch_init_slots(const RecoverArgs& a, const int* hints_host, cudaS
     hc.first = first;
     hc.count = a.batch - first < HintChunk::kMax ? a.batch - first : HintChunk::kMax;
     for (int j = 0; j < hc.count; ++j) hc.hint[j] = hints_host ? hints_host[first + j] : 0;
-    k_init_slots<<<(hc.count + 127) / 128, 128, 0, s>>>(a, hc);
+    launch_chain(k_init_slots, a.chain != 0, dim3((hc.count + 127) / 128), dim3(128), 0, s, a, hc);
   }
   return cudaGetLastError();
 }
@@ -87,6 +88,7 @@ constexpr size_t fold_smem() {
 
 template <int C>
 __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
+  pdl_enter();
   constexpr int NS = FoldNS<C>::value;
   extern __shared__ __align__(16) float fsm[];
   float* raw = fsm;                                                        // [NS][C][FT_J][FT_W]
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
 // grid (.., batch*2), smem t_max*128 doubles + roots.
 constexpr int FD_Z1 = 32;  // columns per Z1 block
 __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
+  pdl_enter();
   extern __shared__ double sh[];
   const int b = blockIdx.y >> 1, q = blockIdx.y & 1;
   const cbp_kernel_slot* slot = a.slots + b;
@@ -337,11 +340,11 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
     cudaFuncSetAttribute(k_fold_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<1>()));
     cudaFuncSetAttribute(k_fold_tile<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fold_smem<3>()));
   });
-  if (a.channels == 1) k_fold_tile<1><<<g1, 256, fold_smem<1>(), s>>>(a, t_fixed);
-  else k_fold_tile<3><<<g1, 256, fold_smem<3>(), s>>>(a, t_fixed);
+  if (a.channels == 1) launch_chain(k_fold_tile<1>, a.chain != 0, g1, dim3(256), fold_smem<1>(), s, a, t_fixed);
+  else launch_chain(k_fold_tile<3>, a.chain != 0, g1, dim3(256), fold_smem<3>(), s, a, t_fixed);
   const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128 * 2) * sizeof(double);  // folds + Z1 quarter sums
   dim3 g2((a.cols + FD_Z1 - 1) / FD_Z1 + (a.rows + 127) / 128, a.batch * 2);
-  k_fold_dft<<<g2, 128, smf, s>>>(a, t_fixed);
+  launch_chain(k_fold_dft, a.chain != 0, g2, dim3(128), smf, s, a, t_fixed);
   return cudaGetLastError();
 }
 
@@ -358,6 +361,7 @@ void fold_plan(int batch, int rows, int cols, int t_max, int& ncb, int& rh, size
 // One CTA per (size s, axis, frame): s x s leading Bezout block of the DC slices
 // (poly.cpp:66-79), then sigma_min / sigma_max by one-sided Jacobi (poly.cpp:81-91).
 __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
+  pdl_enter();
   extern __shared__ double2 shz[];
   __shared__ int flag;
   __shared__ double sv[CBP_MAX_WIDTH + 1];
@@ -417,6 +421,7 @@ __global__ void __launch_bounds__(512) k_width_blocks(RecoverArgs a) {
 // Per frame: all-zero check, first singular size per axis, axis agreement
 // (decoder.cpp:38-44, 83-89).
 __global__ void __launch_bounds__(512) k_width_pick(RecoverArgs a) {
+  pdl_enter();
   const int b = blockIdx.x;
   cbp_kernel_slot* slot = a.slots + b;
   if (slot->status != 0 || slot->width > 0) return;
@@ -489,8 +494,8 @@ cudaError_t launch_width(const RecoverArgs& a, cudaStream_t s) {
   CBP_ONCE_PER_DEVICE({
     cudaFuncSetAttribute(k_width_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   });
-  k_width_blocks<<<g, 512, sm, s>>>(a);
-  k_width_pick<<<a.batch, 512, 0, s>>>(a);
+  launch_chain(k_width_blocks, a.chain != 0, g, dim3(512), sm, s, a);
+  launch_chain(k_width_pick, a.chain != 0, dim3(a.batch), dim3(512), 0, s, a);
   return cudaGetLastError();
 }
 
@@ -909,6 +914,7 @@ __device__ void solve_slice(const RecoverArgs& a, int b, int axis, int i, int t,
 // kernels is not launched with the shared memory of the widest allowed one.
 template <int NT>
 __global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo, int t_hi) {
+  pdl_enter();
   extern __shared__ double2 shs[];
   const int i = blockIdx.x, axis = blockIdx.y, b = blockIdx.z;
   cbp_kernel_slot* slot = a.slots + b;
@@ -922,6 +928,7 @@ __global__ void __launch_bounds__(NT, 512 / NT) k_solve(RecoverArgs a, int t_lo,
 // Gram, eigenvectors and vectors in per-CTA global scratch (a.wide); wide_ctas persistent
 // CTAs walk the (slice, axis, frame) problems.
 __global__ void __launch_bounds__(256) k_solve_wide(RecoverArgs a) {
+  pdl_enter();
   const int np = kWideMaxWidth * 2 * a.batch;
   const SolveSmem sm = carve_solve(a.wide + size_t(blockIdx.x) * a.wide_stride, kWideMaxWidth);
   for (int pid = blockIdx.x; pid < np; pid += gridDim.x) {
@@ -957,13 +964,13 @@ cudaError_t launch_solve(const RecoverArgs& a, cudaStream_t s) {
     dim3 g(tb, 2, a.batch);
     const int nt = nt_env ? nt_env : (size_t(2) * tb * a.batch > 2 * 148 ? 128 : 256);
     if (nt == 128)
-      k_solve<128><<<g, 128, solve_smem_bytes(tb, false), s>>>(a, lo, hi);
+      launch_chain(k_solve<128>, a.chain != 0, g, dim3(128), solve_smem_bytes(tb, false), s, a, lo, hi);
     else
-      k_solve<256><<<g, 256, solve_smem_bytes(tb, false), s>>>(a, lo, hi);
+      launch_chain(k_solve<256>, a.chain != 0, g, dim3(256), solve_smem_bytes(tb, false), s, a, lo, hi);
   }
   if (a.t_max > kSolveMaxWidth) {
     if (!a.wide) return cudaErrorInvalidValue;
-    k_solve_wide<<<a.wide_ctas, 256, 0, s>>>(a);
+    launch_chain(k_solve_wide, a.chain != 0, dim3(a.wide_ctas), dim3(256), 0, s, a);
   }
   return cudaGetLastError();
 }
@@ -1679,6 +1686,7 @@ __device__ void compose_frame(const RecoverArgs& a, int b, void* base) {
 
 // One CTA per frame (t <= kSolveMaxWidth: shared-memory scratch).
 __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
+  pdl_enter();
   extern __shared__ double2 shc[];
   const int b = blockIdx.x;
   const cbp_kernel_slot* slot = a.slots + b;
@@ -1688,6 +1696,7 @@ __global__ void __launch_bounds__(256) k_compose(RecoverArgs a) {
 
 // Frames with kSolveMaxWidth < t <= 63: persistent CTAs with global scratch.
 __global__ void __launch_bounds__(256) k_compose_wide(RecoverArgs a) {
+  pdl_enter();
   for (int b = blockIdx.x; b < a.batch; b += gridDim.x) {
     const cbp_kernel_slot* slot = a.slots + b;
     if (slot->status != 0 || slot->width <= kSolveMaxWidth) continue;  // uniform over the CTA
@@ -1700,10 +1709,10 @@ cudaError_t launch_compose(const RecoverArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_compose, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(compose_smem_bytes(kSolveMaxWidth)));
   });
-  k_compose<<<a.batch, 256, compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s>>>(a);
+  launch_chain(k_compose, a.chain != 0, dim3(a.batch), dim3(256), compose_smem_bytes(min(a.t_max, kSolveMaxWidth)), s, a);
   if (a.t_max > kSolveMaxWidth) {
     if (!a.wide) return cudaErrorInvalidValue;
-    k_compose_wide<<<min(a.batch, a.wide_ctas), 256, 0, s>>>(a);
+    launch_chain(k_compose_wide, a.chain != 0, dim3(min(a.batch, a.wide_ctas)), dim3(256), 0, s, a);
   }
   return cudaGetLastError();
 }
@@ -2135,6 +2144,7 @@ __device__ __forceinline__ void conv2_dispatch(const double* te, const double* t
 
 constexpr int CONV2_THREADS = 128;
 __global__ void __launch_bounds__(CONV2_THREADS, 4) k_conv_resid2(ConvResidArgs a) {
+  pdl_enter();
   extern __shared__ double shd2[];
   constexpr int OUT = 8, VT_R = 4 * OUT;  // 4 row groups of 32 threads
   const int plane = blockIdx.y;
@@ -2241,6 +2251,7 @@ __host__ inline size_t conv_smem(int t, int mode) {
 // entry point that validates a frame returns the same bits.
 __global__ void __launch_bounds__(256) k_resid_reduce(const double2* part, int stride, int used, int channels,
                                                       cbp_kernel_slot* slots, double* out, int batch) {
+  pdl_enter();
   const int b = blockIdx.x;
   if (slots && slots[b].status != 0) return;
   double num = 0.0, den = 0.0;
@@ -2301,8 +2312,9 @@ cudaError_t launch_validate(const RecoverArgs& ra, const float* latent, int ld_o
   for (int t = 1; t <= std::min(ra.t_max, kWideMaxWidth); ++t) sm = std::max(sm, conv2_smem(t));
   if (cudaFuncSetAttribute(k_conv_resid2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess)
     return cudaErrorInvalidValue;
-  k_conv_resid2<<<g, CONV2_THREADS, sm, s>>>(a);
-  k_resid_reduce<<<ra.batch, 256, 0, s>>>(a.part, ntiles_max, used, ra.channels, ra.slots, nullptr, ra.batch);
+  launch_chain(k_conv_resid2, ra.chain != 0, g, dim3(CONV2_THREADS), sm, s, a);
+  launch_chain(k_resid_reduce, ra.chain != 0, dim3(ra.batch), dim3(256), 0, s, (const double2*)a.part, ntiles_max, used, ra.channels,
+               ra.slots, (double*)nullptr, ra.batch);
   return cudaGetLastError();
 }
 

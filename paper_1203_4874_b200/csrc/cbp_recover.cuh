@@ -7,6 +7,7 @@ namespace cbp_dev {
 
 // Device-side geometry of one decode batch and the workspace layout.
 struct RecoverArgs {
+  int chain;  // programmatic dependent launch of the small recovery kernels (cbp_set_launch_chaining)
   const float* pub;
   const float* prv;
   int batch, channels, rows, cols, ld;  // blurred geometry (Mb = rows, Nb = cols)

@@ -34,6 +34,7 @@ __device__ __forceinline__ const float* stream_base(const RecoverArgs& a, int b,
 
 // roots[k] = exp(-2 pi i k / rows) for k < rows, then exp(-2 pi i k / cols) for k < cols
 __global__ void k_spec_roots(RecoverArgs a) {
+  pdl_enter();
   bool any = false;  // nothing to do for a batch of nonnegative frames (the common case)
   for (int b = 0; b < a.batch && !any; ++b) any = signed_frame(a, b);
   if (!any) return;
@@ -53,6 +54,7 @@ __device__ __forceinline__ bool any_signed(const RecoverArgs& a) {
 // Persistent grid over tiles (x fastest, then y, then frame*2+stream): a batch without
 // signed frames costs one flag scan per CTA instead of ~10^4 empty CTAs.
 __global__ void __launch_bounds__(256) k_spec_energy_z1(RecoverArgs a) {
+  pdl_enter();
   if (!any_signed(a)) return;
   const int M = a.rows, N = a.cols, H1 = M / 2 + 1;
   const int tx = (N + TS - 1) / TS, ty = (H1 + TS - 1) / TS;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(256) k_spec_energy_z1(RecoverArgs a) {
 // z2: F_q(m, j) = sum_n luma_q(m, n) W_N^{j n}, j <= N/2. Per tile: partial energies
 // sum_m |F|^2 for the tile's 32 frequencies. grid (ceil(H2/32), ceil(M/32), batch*2).
 __global__ void __launch_bounds__(256) k_spec_energy_z2(RecoverArgs a) {
+  pdl_enter();
   if (!any_signed(a)) return;
   const int M = a.rows, N = a.cols, H2 = N / 2 + 1;
   const int tx = (H2 + TS - 1) / TS, ty = (M + TS - 1) / TS;
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(256) k_spec_energy_z2(RecoverArgs a) {
 // Per (frame, axis): joint energies in a fixed order, first maximum (Eigen maxCoeff),
 // then the picked slice of both lumas into slices[b][axis][q][0][*]. grid (batch, 2).
 __global__ void __launch_bounds__(512) k_spec_pick(RecoverArgs a) {
+  pdl_enter();
   const int b = blockIdx.x, axis = blockIdx.y;
   if (!signed_frame(a, b)) return;
   const int M = a.rows, N = a.cols;
@@ -232,12 +236,12 @@ size_t signed_energy_doubles(int batch, int rows, int cols) {
 
 cudaError_t launch_signed_slices(const RecoverArgs& a, cudaStream_t s) {
   const int M = a.rows, N = a.cols;
-  k_spec_roots<<<(std::max(M, N) + 255) / 256, 256, 0, s>>>(a);
+  launch_chain(k_spec_roots, a.chain != 0, dim3((std::max(M, N) + 255) / 256), dim3(256), 0, s, a);
   const int t1 = ((N + TS - 1) / TS) * ((M / 2 + 1 + TS - 1) / TS) * a.batch * 2;
   const int t2 = ((N / 2 + 1 + TS - 1) / TS) * ((M + TS - 1) / TS) * a.batch * 2;
-  k_spec_energy_z1<<<std::min(t1, 148 * 4), 256, 0, s>>>(a);
-  k_spec_energy_z2<<<std::min(t2, 148 * 4), 256, 0, s>>>(a);
-  k_spec_pick<<<dim3(a.batch, 2), 512, 0, s>>>(a);
+  launch_chain(k_spec_energy_z1, a.chain != 0, dim3(std::min(t1, 148 * 4)), dim3(256), 0, s, a);
+  launch_chain(k_spec_energy_z2, a.chain != 0, dim3(std::min(t2, 148 * 4)), dim3(256), 0, s, a);
+  launch_chain(k_spec_pick, a.chain != 0, dim3(a.batch, 2), dim3(512), 0, s, a);
   return cudaGetLastError();
 }
 

@@ -24,4 +24,7 @@ print(json.dumps({
     "solve_us": {"corr+gram": d(10, 11), "eig": d(11, 12), "refine": d(12, 13), "gap": d(13, 14)},
     "compose_us": {"complete": d(20, 21), "resolve_chol": d(21, 25), "resolve_invit": d(25, 22),
                    "resolve_refine": d(22, 23), "assemble": d(23, 24)},
+    "compose_detail_us": {"refine_loop": d(22, 26), "after_refine": d(26, 23),
+                           "div0": d(40, 41), "ifft0": d(41, 42), "realize0": d(42, 43),
+                           "div1": d(44, 45), "ifft1": d(45, 46), "realize1": d(46, 47)},
     "eig_last_us": {"tridiag": d(30, 31), "ql": d(31, 32), "back": d(32, 33)}}))
