@@ -488,7 +488,8 @@ def run_c3(args, world, rank, local):
         # one host-buffer run of e2e_steps epochs (distinct pool epochs), like the reference CLI
         # decoding a video run (tools/cbp.cpp:130-207): the pipeline streams across the epoch
         # boundaries (recovery frames at 0, 30, 60, ...) instead of refilling per epoch
-        nE = args.e2e_steps
+        # (with several ranks each keeps fewer epochs in pinned host memory: ~2.3 GB per epoch)
+        nE = max(1, args.e2e_steps // world) if world > 2 else args.e2e_steps
         hpub = torch.cat([pub[e % E].contiguous().cpu() for e in range(nE)]).pin_memory()
         hprv = torch.zeros_like(hpub).pin_memory()
         rec = np.zeros(EPOCH * nE, np.int32)
