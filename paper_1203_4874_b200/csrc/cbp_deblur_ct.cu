@@ -583,12 +583,14 @@ __global__ void k_wiener_s(DeblurArgs a, int frames) {
   if (idx >= a.Hc * t) return;
   const int v = idx / t, ai = idx - v * t;
   double re = 0.0, im = 0.0;
+  // powers of W_Gc^v by recurrence from one sincos (drift ~t ulp, far below the FP32 table)
+  const double2 wv = zroot(v, a.Gc);
+  double2 p = make_double2(1.0, 0.0);
   for (int bj = 0; bj < t; ++bj) {
     const double w = slot->weights[ai * t + bj];
-    double sn, cs;
-    sincospi(-2.0 * double((long(v) * bj) % a.Gc) / double(a.Gc), &sn, &cs);
-    re = fma(w, cs, re);
-    im = fma(w, sn, im);
+    re = fma(w, p.x, re);
+    im = fma(w, p.y, im);
+    p = zmul(p, wv);
   }
   a.S[size_t(f) * a.s_frame + idx] = make_double2(re, im);
 }
@@ -652,6 +654,7 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
     }
   }
   const double sc = 1.0 / (double(a.Gr) * double(a.Gc));
+  const double eps = slot->epsilon;
   // transposed table HT[v][slot(u)]: slot(u) = pos(u) of the column plan (a.hpos), so pass B
   // multiplies element-wise in its DIF output order
 #pragma unroll
@@ -662,7 +665,14 @@ __global__ void __launch_bounds__(128) k_wiener_h(DeblurArgs a, int frames) {
     for (int vv = 0; vv < WH_V; ++vv) {
       const int v = v0 + vv;
       if (v < a.Hc) {
-        const double g = sc / (acc[k][vv].x * acc[k][vv].x + acc[k][vv].y * acc[k][vv].y + slot->epsilon);
+        // reciprocal by MUFU seed + two Newton steps (~1 ulp; the table is stored in FP32)
+        // instead of an IEEE division per entry, which dominated the kernel's instructions
+        const double den = acc[k][vv].x * acc[k][vv].x + acc[k][vv].y * acc[k][vv].y + eps;
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+        r = fma(r, fma(-den, r, 1.0), r);
+        r = fma(r, fma(-den, r, 1.0), r);
+        const double g = sc * r;
         H[size_t(v) * a.hp] = make_float2(float(acc[k][vv].x * g), float(-acc[k][vv].y * g));
       }
     }
