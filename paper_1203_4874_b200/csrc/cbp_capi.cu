@@ -226,19 +226,19 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
   static const bool fused_off = getenv("CBP_FUSED") == nullptr;  // measured slower: opt-in experiment
   int nA = 0, nB = 0, nC = 0;
   if (!fused_off && planes > 0 && deblur_fused_shape(a, nA, nB, nC)) {
-    static const int lag_b = getenv("CBP_FUSED_LAG") ? std::max(1, atoi(getenv("CBP_FUSED_LAG"))) : 2;
-    static const int ring_env = getenv("CBP_FUSED_RING") ? atoi(getenv("CBP_FUSED_RING")) : 0;
+    static const int ring_env = getenv("CBP_FUSED_RING") ? atoi(getenv("CBP_FUSED_RING")) : 6;
     FusedCtl f{};
     f.planes = planes;
-    f.lag_b = lag_b;
-    f.lag_c = 2 * lag_b;
-    f.ring = std::min(std::max(ring_env > 0 ? ring_env : f.lag_c + 2, f.lag_c + 2), planes);
+    f.ring = std::min(std::max(ring_env, 2), planes);
     f.nA = nA, f.nB = nB, f.nC = nC;
+    f.nsm = ctx->num_sms;
     a.X = static_cast<float2*>(workspace(ctx, WS_X, plane_bytes * f.ring));
-    unsigned* ctl = static_cast<unsigned*>(workspace(ctx, WS_FUSED, sizeof(unsigned) * (3 * size_t(planes) + 1)));
+    const size_t nctl = 4 + 3 * size_t(planes);
+    unsigned* ctl = static_cast<unsigned*>(workspace(ctx, WS_FUSED, sizeof(unsigned) * (nctl + f.nsm)));
     if (!a.X || !ctl) return set_error(ctx, CBP_CUDA_ERROR, "workspace allocation failed");
     f.ticket = ctl;
-    f.done = ctl + 1;
+    f.done = ctl + 4;
+    f.sm_role = reinterpret_cast<int*>(ctl + nctl);
     a.frame0 = 0;
     a.in_vec2 = (reinterpret_cast<uintptr_t>(a.in) % 8 == 0) && a.in_ld % 2 == 0 && in_plane_stride % 2 == 0;
     a.out_vec2 = (reinterpret_cast<uintptr_t>(a.out) % 8 == 0) && a.out_ld % 2 == 0 && out_plane_stride % 2 == 0;
@@ -256,7 +256,8 @@ int deblur_run(cbp_ctx* ctx, DeblurArgs a, int planes, size_t in_plane_stride,
       ctx->prof_used += 4;
       ctx->prof_planes += planes;
     }
-    cudaMemsetAsync(ctl, 0, sizeof(unsigned) * (3 * size_t(planes) + 1), stream);
+    cudaMemsetAsync(ctl, 0, sizeof(unsigned) * nctl, stream);
+    cudaMemsetAsync(f.sm_role, 0xff, sizeof(int) * f.nsm, stream);  // -1: no role claimed
     if (ev) cudaEventRecord(ev[0], stream);
     if (launch_deblur_fused(a, f, stream)) {
       if (ev)  // one launch: the whole duration is reported as pass A, B and C as zero

@@ -65,9 +65,11 @@ bool deblur_has_ct(int Gr, int Gc, int pass);
 bool ct_radices(int n, bool column, std::vector<int>& r);
 int ct_pos(const std::vector<int>& rad, int n);
 struct FusedCtl {
-  unsigned* ticket;  // [0]: next ticket (zeroed per launch)
+  unsigned* ticket;  // [0..2]: queue heads of roles A, B, C; [3]: role counter (zeroed per launch)
   unsigned* done;    // [0, P): A tiles done per plane, [P, 2P): B strips, [2P, 3P): C tiles
-  int planes, ring, lag_b, lag_c;
+  int* sm_role;      // [nsm]: role claimed by the first CTA on each SM (-1 per launch)
+  int nsm;
+  int planes, ring;
   int nA, nB, nC;    // items per plane of each pass
 };
 

@@ -1000,43 +1000,17 @@ bool launch_deblur_pass_ct(const DeblurArgs& a, int planes, int pass, cudaStream
 
 
 // ------------------------------------------------ fused persistent deconvolution
-// One persistent launch runs passes A, B and C of a whole batch. Work items (pass A row
-// tiles, pass B column strips, pass C row tiles) are handed out from one ticket counter in
-// a fixed order of rounds: round r holds A(r), B(r - lag_b) and C(r - lag_c), where X(p) is
-// every item of that pass for plane p. An item waits for its producer plane's completion
-// counter (B(p): all A(p) tiles; C(p): all B(p) strips; A(p): all C(p - ring) tiles, whose
-// spectrum slot it reuses), and producers are always items with smaller tickets, which are
-// held by running CTAs: the minimum unfinished ticket can always progress (no deadlock,
-// whatever the residency). The half spectrum lives in a ring of `ring` plane slots
-// (ring x 8.5 MB at 1080p), so it stays L2-resident between the passes and the three
-// launch boundaries (fill and drain of 3 persistent grids per launch group) disappear.
-struct FusedItem {
-  int type, p, idx;  // type 0: A, 1: B, 2: C; -1: none
-};
-
-__device__ __forceinline__ long long fused_prefix(const FusedCtl& f, int r) {  // tickets of rounds < r
-  return (long long)f.nA * min(r, f.planes) + (long long)f.nB * min(max(r - f.lag_b, 0), f.planes) +
-         (long long)f.nC * min(max(r - f.lag_c, 0), f.planes);
-}
-__device__ __forceinline__ FusedItem fused_item(const FusedCtl& f, unsigned tk) {
-  int lo = 0, hi = f.planes + f.lag_c;  // prefix(lo) <= tk < prefix(hi)
-  if ((long long)tk >= fused_prefix(f, hi)) return {-1, 0, 0};
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (fused_prefix(f, mid) <= (long long)tk) lo = mid;
-    else hi = mid;
-  }
-  long long off = (long long)tk - fused_prefix(f, lo);
-  if (lo < f.planes) {
-    if (off < f.nA) return {0, lo, int(off)};
-    off -= f.nA;
-  }
-  if (lo - f.lag_b >= 0 && lo - f.lag_b < f.planes) {
-    if (off < f.nB) return {1, lo - f.lag_b, int(off)};
-    off -= f.nB;
-  }
-  return {2, lo - f.lag_c, int(off)};
-}
+// One persistent launch runs passes A, B and C of a whole batch, each SM in one role: the
+// first CTA to start on an SM claims a role for the SM (A, B, C in a 4:5:4 pattern, the
+// passes' relative costs), so an SM only ever runs one pass's code (one pass's instruction
+// stream stays in the SM's instruction cache; the union of the three thrashed it) and the
+// row roles keep their twiddles in shared memory. Each role takes its items (A and C: row
+// tiles, B: column strips) in plane order from its own queue; an item waits for its
+// producer plane's completion counter (B(p): all A(p) tiles; C(p): all B(p) strips; A(p):
+// all C(p - ring) tiles, whose spectrum slot it reuses). Deadlock-free while every role has
+// a running CTA (the first three SMs take A, B, C): the oldest unfinished plane-pass is
+// always ready and at the head of its queue. The half spectrum lives in a ring of `ring`
+// plane slots (ring x 8.5 MB at 1080p), so it stays L2-resident between the passes.
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -1045,77 +1019,111 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
-// the producers of item `it` have completed (and their writes are visible to the async proxy)
-__device__ __forceinline__ bool fused_ready(const FusedCtl& f, FusedItem it) {
+// the producers of plane p for a role-`role` item have completed (writes visible to TMA)
+__device__ __forceinline__ bool fused_ready(const FusedCtl& f, int role, int p) {
   bool ok = true;
-  if (it.type == 0) ok = it.p < f.ring || ld_acquire(f.done + 2 * f.planes + it.p - f.ring) >= unsigned(f.nC);
-  else if (it.type == 1) ok = ld_acquire(f.done + it.p) >= unsigned(f.nA);
-  else if (it.type == 2) ok = ld_acquire(f.done + f.planes + it.p) >= unsigned(f.nB);
+  if (role == 0) ok = p < f.ring || ld_acquire(f.done + 2 * f.planes + p - f.ring) >= unsigned(f.nC);
+  else if (role == 1) ok = ld_acquire(f.done + p) >= unsigned(f.nA);
+  else ok = ld_acquire(f.done + f.planes + p) >= unsigned(f.nB);
   if (ok) fence_proxy_async_global();
   return ok;
 }
-__device__ __forceinline__ void fused_publish(const FusedCtl& f, int type, int p) {
+__device__ __forceinline__ void fused_publish(const FusedCtl& f, int role, int p) {
   fence_proxy_async_global();
   __threadfence();
-  atomicAdd(f.done + type * f.planes + p, 1u);
+  atomicAdd(f.done + role * f.planes + p, 1u);
 }
 
 template <class PR, class PC>
 struct FusedPlan {
   static_assert(PR::NT == PC::NT, "one CTA shape for all three passes");
   static constexpr int NT = PR::NT;
-  static constexpr int L = PR::L, RPC = PR::RPC;
+  static constexpr int L = PR::L, RPC = PR::RPC, SPA = PR::SPA;
   static constexpr int G = PC::G, W = PC::W, GP = ((G + 11) / 16) * 16 + 4;
-  static constexpr int TILE_A = RPC * L, TILE_B = GP * W, TILE_C = ((L + 1) * RPC + 15) & ~15;
-  static constexpr int MAXT = TILE_A > TILE_B ? (TILE_A > TILE_C ? TILE_A : TILE_C) : (TILE_B > TILE_C ? TILE_B : TILE_C);
-  static constexpr int BUF = (MAXT + 15) & ~15;  // float2; 128-byte multiple (TMA destinations)
-  static constexpr size_t SMEM = size_t(2) * BUF * sizeof(float2) + 64;  // + 3 mbarriers, 2 item slots
+  static constexpr int TILE_A = RPC * SPA, TILE_B = GP * W, TILE_C = ((L + 1) * RPC + 15) & ~15;
+  static constexpr int BUFR = ((TILE_A > TILE_C ? TILE_A : TILE_C) + 15) & ~15;  // rows: 128-byte multiple
+  static constexpr int BUFB = (TILE_B + 15) & ~15;
+  static constexpr int TWN = L / 2 + 1 + TwUsed<L, typename PR::R>::count;  // staged row twiddles
+  static constexpr int ROWS_F2 = 2 * BUFR + TWN, COLS_F2 = 2 * BUFB;
+  static constexpr int F2 = ROWS_F2 > COLS_F2 ? ROWS_F2 : COLS_F2;
+  static constexpr size_t SMEM = size_t(F2) * sizeof(float2) + 64;  // + 2 mbarriers, role
 };
 
 template <class PR, class PC>
 __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a, FusedCtl f,
                                                                    const __grid_constant__ CUtensorMap tmap) {
   using FP = FusedPlan<PR, PC>;
-  constexpr int NT = FP::NT, L = FP::L, RPC = FP::RPC, BUF = FP::BUF;
+  constexpr int NT = FP::NT, L = FP::L, RPC = FP::RPC, SPA = FP::SPA;
   constexpr int W = FP::W, GP = FP::GP;
   using RR = typename PR::R;
   using RC = typename PC::R;
-  using FFTA = FftIP<L, RPC, L, 1, NT, false, false>;
+  using FFTA = FftIP<L, RPC, SPA, 1, NT, false, true>;
   using FFTB = FftIP<FP::G, W, GP, 1, NT, false>;
-  using FFTC = FftIP<L, RPC, 1, RPC, NT, true, false>;
+  using FFTC = FftIP<L, RPC, 1, RPC, NT, true, true>;
   constexpr int NRAD = RadixCount<RR>::value;
   extern __shared__ __align__(128) float2 smf[];
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smf + 2 * BUF);  // [0], [1]: buffers
-  int* s_item = reinterpret_cast<int*>(bar + 3);
+  // barriers and broadcast slots in dynamic shared memory: static shared variables would
+  // shift the dynamic region off the 128-byte alignment the tensor copies need
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smf + FP::F2);
+  int* s_role = reinterpret_cast<int*>(bar + 2);
+  unsigned* s_item = reinterpret_cast<unsigned*>(bar + 3);
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     mbar_init_fence();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    volatile int* slot = f.sm_role + (smid % unsigned(f.nsm));
+    const int old = atomicCAS(f.sm_role + (smid % unsigned(f.nsm)), -1, -2);
+    int role;
+    if (old == -1) {  // first CTA on this SM: A, B, C, A, B, C, A, B, C, A, B, C, B
+      const unsigned k = atomicAdd(f.ticket + 3, 1u) % 13u;
+      role = k == 12 ? 1 : int(k % 3);
+      __threadfence();
+      *slot = role;
+    } else {
+      role = old;
+      while (role < 0) role = *slot;
+    }
+    *s_role = role;
+  }
+  __syncthreads();
+  const int role = *s_role;
+  const int BUF = role == 1 ? FP::BUFB : FP::BUFR;
+  const int nper = role == 0 ? f.nA : (role == 1 ? f.nB : f.nC);
+  const unsigned total = unsigned(nper) * unsigned(f.planes);
+  // row roles: split and stage twiddles in shared memory (RTW), after the two tile buffers
+  const float2* twst = a.twst_row;
+  const float2* twp = a.tw_post;
+  if (role != 1) {
+    float2* tws = smf + 2 * FP::BUFR;
+    twst = stage_row_twiddles<PR>(a, tws);
+    twp = tws;
   }
   const unsigned row_bytes = unsigned((a.Nb + 3) & ~3) * 4u;
   auto xt = [&](int p) { return a.X + size_t(p % f.ring) * a.x_plane; };
-  auto rows_of = [&](int p) {  // latent rows written by pass C (failed frames: none)
+  auto rows_of = [&](int p) {
     const cbp_kernel_slot* sl = plane_slot(a, p);
     return sl->status == 0 ? a.Mb - sl->width + 1 : 0;
   };
-  // thread 0: start the loads of item `it` into buffer b (its producers have completed)
-  auto issue = [&](FusedItem it, int b) {
+  // thread 0: loads of item (p, idx) of this role into buffer b (its producers completed)
+  auto issue = [&](int p, int idx, int b) {
     float2* dst = smf + b * BUF;
     unsigned long long* mb = &bar[b];
     fence_proxy_async();
-    if (it.type == 0) {
-      const int r0 = it.idx * RPC;
-      const float* src = a.in + size_t(it.p) * a.in_plane + size_t(r0) * a.in_ld;
+    if (role == 0) {
+      const int r0 = idx * RPC;
+      const float* src = a.in + size_t(p) * a.in_plane + size_t(r0) * a.in_ld;
       const int nr = min(RPC, a.Mb - r0);
       mbar_expect_tx(mb, unsigned(nr) * row_bytes);
-      for (int s = 0; s < nr; ++s) bulk_g2s(dst + s * L, src + size_t(s) * a.in_ld, row_bytes, mb);
-    } else if (it.type == 1) {
-      const int v0 = it.idx * W, nc = min(W, a.Hc - v0);
-      const float2* XT = xt(it.p);
+      for (int s = 0; s < nr; ++s) bulk_g2s(dst + s * SPA, src + size_t(s) * a.in_ld, row_bytes, mb);
+    } else if (role == 1) {
+      const int v0 = idx * W, nc = min(W, a.Hc - v0);
+      const float2* XT = xt(p);
       mbar_expect_tx(mb, unsigned(nc) * unsigned(a.Mb) * 8u);
       for (int s = 0; s < nc; ++s) bulk_g2s(dst + s * GP, XT + size_t(v0 + s) * a.xp, unsigned(a.Mb) * 8u, mb);
     } else {
-      const int r0 = it.idx * RPC, slot = it.p % f.ring;
+      const int r0 = idx * RPC, slot = p % f.ring;
       const unsigned tail = unsigned(min(RPC, a.xp - r0)) * 8u;
       mbar_expect_tx(mb, unsigned(RPC) * L * 8u + tail);
       const unsigned d = smem_u32(dst), bb = smem_u32(mb);
@@ -1128,65 +1136,64 @@ __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a,
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
             ::"r"(d), "l"(tm), "r"(r0), "r"(0), "r"(0), "r"(0), "r"(slot), "r"(bb) : "memory");
-      bulk_g2s(dst + L * RPC, xt(it.p) + size_t(L) * a.xp + r0, tail, mb);
+      bulk_g2s(dst + L * RPC, xt(p) + size_t(L) * a.xp + r0, tail, mb);
     }
   };
   // thread 0 state: the plane of a pass-B strip whose bulk stores are not yet published
   int pend_b = -1;
-  auto flush_b = [&](int keep) {  // publish the pending strip once its stores completed
+  auto flush_b = [&](int keep) {
     if (pend_b < 0) return;
     if (keep) asm volatile("cp.async.bulk.wait_group 1;\n" ::: "memory");
     else bulk_wait_all();
     fused_publish(f, 1, pend_b);
     pend_b = -1;
   };
-  __syncthreads();  // barriers initialised
-  FusedItem cur{-1, 0, 0};
+  unsigned cur = 0;
   if (threadIdx.x == 0) {
-    cur = fused_item(f, atomicAdd(f.ticket, 1u));
-    if (cur.type >= 0) {
-      while (!fused_ready(f, cur)) __nanosleep(256);
-      issue(cur, 0);
+    cur = atomicAdd(f.ticket + role, 1u);
+    if (cur < total) {
+      while (!fused_ready(f, role, int(cur / nper))) __nanosleep(256);
+      issue(int(cur / nper), int(cur % nper), 0);
     }
-    s_item[0] = cur.type, s_item[1] = cur.p, s_item[2] = cur.idx;
+    *s_item = cur;
   }
   __syncthreads();
-  cur = FusedItem{s_item[0], s_item[1], s_item[2]};
+  cur = *s_item;
   unsigned ph = 0u;  // mbarrier phase bits of buffers 0, 1
-  for (int it = 0; cur.type >= 0; ++it) {
+  for (int it = 0; cur < total; ++it) {
     const int cb = it & 1;
     float2* buf = smf + cb * BUF;
-    FusedItem nxt{-1, 0, 0};
+    unsigned nxt = total;
     bool issued = false;
     if (threadIdx.x == 0) {
-      nxt = fused_item(f, atomicAdd(f.ticket, 1u));
-      if (nxt.type >= 0 && fused_ready(f, nxt)) {
+      nxt = atomicAdd(f.ticket + role, 1u);
+      if (nxt < total && fused_ready(f, role, int(nxt / nper))) {
         bulk_wait_read();  // the other buffer's bulk stores (a pass-B strip) have left shared memory
-        issue(nxt, cb ^ 1);
+        issue(int(nxt / nper), int(nxt % nper), cb ^ 1);
         issued = true;
       }
     }
     mbar_wait(&bar[cb], (ph >> cb) & 1u);  // every thread observes the tile's arrival
     ph ^= 1u << cb;
-    const int p = cur.p;
+    const int p = int(cur / nper), idx = int(cur % nper);
     int b_commit = 0;  // thread 0: this item committed a bulk-store group
-    if (cur.type == 0) {
+    if (role == 0) {
       // ---- pass A: forward row FFTs of RPC rows, r2c split into XT (see k_rows_forward_ct)
-      FFTA::template dif_masked<false>(buf, a.twst_row, a.Nb, RR{});
-      const int r0 = cur.idx * RPC;
+      FFTA::template dif_masked<false>(buf, twst, a.Nb, RR{});
+      const int r0 = idx * RPC;
       float2* XT = xt(p) + r0;
       const int nrows = min(RPC, a.Mb - r0);
       constexpr int NPAIR = L / 2 + 1, HALF = RPC / 2;
 #pragma unroll 1
-      for (int idx = threadIdx.x; idx < NPAIR * HALF; idx += NT) {
-        const int k = idx / HALF, j = idx - k * HALF;
+      for (int q = threadIdx.x; q < NPAIR * HALF; q += NT) {
+        const int k = q / HALF, j = q - k * HALF;
         if (2 * j >= nrows) continue;
         const int pk = Pos<RR>::get(k), pc = Pos<RR>::get(k == 0 ? 0 : L - k);
-        const float2 w = __ldg(&a.tw_post[k]);
+        const float2 w = twp[k];
         float2 xk[2], xc[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const float2* z = buf + (2 * j + h) * L;
+          const float2* z = buf + (2 * j + h) * SPA;
           const float2 zk = z[pk], zc = cconj(z[pc]);
           const float2 e = cscale(cadd(zk, zc), 0.5f);
           const float2 d = csub(zk, zc);
@@ -1204,9 +1211,9 @@ __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a,
           if (L - k != k) dc[0] = xc[0];
         }
       }
-    } else if (cur.type == 1) {
+    } else if (role == 1) {
       // ---- pass B: column DIF, fused filter stage (H from L2), DIT (see k_cols_filter_bulk)
-      const int v0 = cur.idx * W, nc = min(W, a.Hc - v0);
+      const int v0 = idx * W, nc = min(W, a.Hc - v0);
       const int fs = deblur_slot_index(a, p);
       const cbp_kernel_slot* slot = a.slot + fs;
       if (slot->status == 0) {  // uniform over the CTA
@@ -1217,25 +1224,25 @@ __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a,
         if (threadIdx.x == 0) {
           const int M = a.Mb - t + 1;  // even: Mb even, t odd
           float2* XT = xt(p);
-          for (int s = 0; s < nc; ++s) bulk_s2g(XT + size_t(v0 + s) * a.xp, buf + s * GP, unsigned(M) * 8u);
+          for (int s2 = 0; s2 < nc; ++s2) bulk_s2g(XT + size_t(v0 + s2) * a.xp, buf + s2 * GP, unsigned(M) * 8u);
           bulk_commit();
           b_commit = 1;
         }
       }
     } else {
       // ---- pass C: c2r split, inverse row DIT, crop (see k_rows_inverse_ct)
-      const int r0 = cur.idx * RPC;
+      const int r0 = idx * RPC;
       const int M = rows_of(p);
       const int nrows = min(RPC, M - r0);
       if (nrows > 0) {
         constexpr int NP = L / 2 + 1, HALF = RPC / 2;
 #pragma unroll 1
-        for (int idx = threadIdx.x; idx < NP * HALF; idx += NT) {
-          const int k = idx / HALF, j = idx - k * HALF;
+        for (int q = threadIdx.x; q < NP * HALF; q += NT) {
+          const int k = q / HALF, j = q - k * HALF;
           float4* pa = reinterpret_cast<float4*>(buf + Pos<RR>::get(k) * RPC + 2 * j);
           float4* pb = reinterpret_cast<float4*>(buf + (k == 0 ? L : Pos<RR>::get(L - k)) * RPC + 2 * j);
           const float4 A4 = *pa, B4 = *pb;
-          const float2 w = cconj(__ldg(&a.tw_post[k]));
+          const float2 w = cconj(twp[k]);
           const float2 wm = make_float2(-w.x, w.y);
           float2 r1[2], r2[2];
 #pragma unroll
@@ -1253,56 +1260,50 @@ __global__ void __launch_bounds__(PR::NT, PR::MINB) k_deblur_fused(DeblurArgs a,
           if (k != 0 && 2 * k != L) *pb = make_float4(r2[0].x, r2[0].y, r2[1].x, r2[1].y);
         }
         __syncthreads();
-        FFTC::template dit<true>(buf, a.twst_row, RR{});
+        FFTC::template dit<true>(buf, twst, RR{});
         const int N = a.Nb - (a.Mb - M);
         float* dst = a.out + size_t(p) * a.out_plane + size_t(r0) * a.out_ld;
         if (a.out_vec2 && N % 2 == 0) {
-          const int h = N / 2;
-          for (int n = threadIdx.x; n < h; n += NT) {
-#pragma unroll
-            for (int s2 = 0; s2 < RPC; s2 += 2) {
-              const float4 z = reinterpret_cast<const float4*>(buf + n * RPC)[s2 / 2];
-              if (s2 < nrows) __stcs(reinterpret_cast<float2*>(dst + size_t(s2) * a.out_ld) + n, make_float2(z.x, z.y));
-              if (s2 + 1 < nrows)
-                __stcs(reinterpret_cast<float2*>(dst + size_t(s2 + 1) * a.out_ld) + n, make_float2(z.z, z.w));
-            }
+          constexpr int CH = RPC / 2;
+          const int nf = (N / 2) * CH;
+          for (int q = threadIdx.x; q < nf; q += NT) {
+            const int n = q / CH, s2 = 2 * (q - n * CH);
+            const float4 z = reinterpret_cast<const float4*>(buf)[q];
+            if (s2 < nrows) __stcs(reinterpret_cast<float2*>(dst + size_t(s2) * a.out_ld) + n, make_float2(z.x, z.y));
+            if (s2 + 1 < nrows)
+              __stcs(reinterpret_cast<float2*>(dst + size_t(s2 + 1) * a.out_ld) + n, make_float2(z.z, z.w));
           }
         } else {
-          for (int s = 0; s < nrows; ++s)
+          for (int s2 = 0; s2 < nrows; ++s2)
             for (int n = threadIdx.x; n < N; n += NT) {
-              const float2 z = buf[(n >> 1) * RPC + s];
-              __stcs(dst + size_t(s) * a.out_ld + n, (n & 1) ? z.y : z.x);
+              const float2 z = buf[(n >> 1) * RPC + s2];
+              __stcs(dst + size_t(s2) * a.out_ld + n, (n & 1) ? z.y : z.x);
             }
         }
       }
     }
-    fence_proxy_async();  // shared-memory reads/writes of this item before the buffer's next bulk fill
+    fence_proxy_async();  // shared-memory accesses of this item before the buffer's next bulk fill
     __syncthreads();      // all threads' stores of this item issued
     if (threadIdx.x == 0) {
-      if (cur.type == 1) {
+      if (role == 1) {
         flush_b(b_commit);  // the previous strip's stores (this strip's own group may still run)
-        pend_b = p;         // published once its stores completed
+        pend_b = p;
       } else {
-        flush_b(0);
-        fused_publish(f, cur.type, p);
+        fused_publish(f, role, p);
       }
-      if (nxt.type >= 0 && !issued) {
+      if (nxt < total && !issued) {
         flush_b(0);  // never wait while holding unpublished work
-        while (!fused_ready(f, nxt)) __nanosleep(128);
+        while (!fused_ready(f, role, int(nxt / nper))) __nanosleep(128);
         bulk_wait_read();
-        issue(nxt, cb ^ 1);
+        issue(int(nxt / nper), int(nxt % nper), cb ^ 1);
       }
-      s_item[0] = nxt.type, s_item[1] = nxt.p, s_item[2] = nxt.idx;
+      *s_item = nxt;
     }
     __syncthreads();
-    cur = FusedItem{s_item[0], s_item[1], s_item[2]};
+    cur = *s_item;
   }
   if (threadIdx.x == 0) flush_b(0);
 }
-
-// Tensor map of pass C over the spectrum ring (plane coordinate = ring slot).
-template <class P>
-bool rows_inverse_tmap(const DeblurArgs& a, int planes, CUtensorMap* map);
 
 template <class PR, class PC>
 bool launch_fused_impl(const DeblurArgs& a, const FusedCtl& f, cudaStream_t s) {
@@ -1319,8 +1320,7 @@ bool launch_fused_impl(const DeblurArgs& a, const FusedCtl& f, cudaStream_t s) {
   });
   CUtensorMap map;
   if (!rows_inverse_tmap<PR>(a, f.ring, &map)) return false;
-  const long long total = (long long)(f.nA + f.nB + f.nC) * f.planes;
-  const int grid = persistent_grid(c.per_sm, c.sms, a.sm_reserve, int(std::min<long long>(total, 1 << 30)));
+  const int grid = persistent_grid(c.per_sm, c.sms, a.sm_reserve, 1 << 30);
   k_deblur_fused<PR, PC><<<grid, FP::NT, FP::SMEM, s>>>(a, f, map);
   return true;
 }
