@@ -248,12 +248,18 @@ __global__ void __launch_bounds__(256) k_fold_tile(RecoverArgs a, int t_fixed) {
 // Sum the partials in a fixed order (Z1: row blocks of column n; Z2: column strips of row
 // m), then the t x t DFT epilogue: slice_i[x] = sum_r W(i, r) fold[r][x],
 // W(i, r) = exp(-2 pi i ((i r) mod t) / t) (fft.cpp:203-212). One launch for both axes:
-// blocks [0, ceil(cols/32)) do Z1, the rest Z2 (128 columns / rows per block). A Z1 block
-// owns 32 columns; its 4 warps sum interleaved quarters of the row blocks (loads batched 4
-// deep) and warp 0 adds the four quarter sums in a fixed order: the Z1 fold is a long sum
-// (~75 row blocks at 1080p) that one thread per column left latency-bound.
+// blocks [0, nb1) do Z1, the rest Z2 (128 rows per block). When the Z1 fold is a long sum
+// (>= 16 row blocks, e.g. ~75 for one 1080p frame; one thread per column left it
+// latency-bound) a Z1 block owns 32 columns and its 4 warps sum interleaved quarters of the
+// row blocks (loads batched 4 deep), warp 0 adding the quarters in a fixed order; short
+// sums (large batches) keep 128 columns per block.
 // grid (.., batch*2), smem t_max*128 doubles + roots.
-constexpr int FD_Z1 = 32;  // columns per Z1 block
+// Z1 row-block sums split over S warps-groups when the sum is long (>= 16 row blocks:
+// small batches of large frames); S = 1 (128 columns per block) otherwise
+__host__ __device__ __forceinline__ int fold_dft_split(const RecoverArgs& a) {
+  const int rh = a.fold_rh > 0 ? a.fold_rh : 1;
+  return (a.rows + rh - 1) / rh >= 16 ? 4 : 1;
+}
 __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
   pdl_enter();
   extern __shared__ double sh[];
@@ -266,27 +272,28 @@ __global__ void __launch_bounds__(128) k_fold_dft(RecoverArgs a, int t_fixed) {
   double* fold = sh + 2 * a.t_max;
   for (int i = threadIdx.x; i < t; i += blockDim.x) root[i] = zroot(i, t);
   __syncthreads();
-  const int nb1 = (a.cols + FD_Z1 - 1) / FD_Z1;
+  const int S = fold_dft_split(a), cpb = 128 / S;  // Z1 columns per block
+  const int nb1 = (a.cols + cpb - 1) / cpb;
   const bool z1 = int(blockIdx.x) < nb1;
   if (z1) {
-    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;  // 4 quarter sums per column
-    const int x = blockIdx.x * FD_Z1 + lane;
+    const int col = threadIdx.x % cpb, g = threadIdx.x / cpb;  // S partial sums per column
+    const int x = blockIdx.x * cpb + col;
     const int RB = fold_rows(t, a.fold_rh);
     const int nrb = (a.rows + RB - 1) / RB;
     const double* part = a.part + (size_t(b) * 2 + q) * a.part_stride + x;
-    double* quarter = fold + t * blockDim.x;  // [r][g][lane]
+    double* quarter = S > 1 ? fold + t * blockDim.x : fold;  // [r][g][col] (S = 1: the fold itself)
     if (x < a.cols)
       for (int r = 0; r < t; ++r) {
         double acc = 0.0;
 #pragma unroll 4
-        for (int rb = g; rb < nrb; rb += 4) acc += part[(size_t(rb) * t + r) * a.cols];
-        quarter[(r * 4 + g) * 32 + lane] = acc;
+        for (int rb = g; rb < nrb; rb += S) acc += part[(size_t(rb) * t + r) * a.cols];
+        quarter[(r * S + g) * cpb + col] = acc;
       }
     __syncthreads();
     if (g != 0 || x >= a.cols) return;
     for (int r = 0; r < t; ++r) {
-      const double* qv = quarter + r * 4 * 32 + lane;
-      fold[r * blockDim.x + threadIdx.x] = (qv[0] + qv[32]) + (qv[64] + qv[96]);
+      const double* qv = quarter + r * S * cpb + col;
+      fold[r * blockDim.x + threadIdx.x] = S == 4 ? (qv[0] + qv[cpb]) + (qv[2 * cpb] + qv[3 * cpb]) : qv[0];
     }
     double2* out = a.slices + slice_offset(a, b, 0, q, 0) + x;
     for (int i = 0; i < t; ++i) {
@@ -342,8 +349,9 @@ cudaError_t launch_fold(const RecoverArgs& a, int t_fixed, cudaStream_t s) {
   });
   if (a.channels == 1) launch_chain(k_fold_tile<1>, a.chain != 0, g1, dim3(256), fold_smem<1>(), s, a, t_fixed);
   else launch_chain(k_fold_tile<3>, a.chain != 0, g1, dim3(256), fold_smem<3>(), s, a, t_fixed);
-  const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128 * 2) * sizeof(double);  // folds + Z1 quarter sums
-  dim3 g2((a.cols + FD_Z1 - 1) / FD_Z1 + (a.rows + 127) / 128, a.batch * 2);
+  // folds (+ the Z1 partial sums when they are split)
+  const size_t smf = (2 * a.t_max + size_t(a.t_max) * 128 * (fold_dft_split(a) > 1 ? 2 : 1)) * sizeof(double);
+  dim3 g2((a.cols + 128 / fold_dft_split(a) - 1) / (128 / fold_dft_split(a)) + (a.rows + 127) / 128, a.batch * 2);
   launch_chain(k_fold_dft, a.chain != 0, g2, dim3(128), smf, s, a, t_fixed);
   return cudaGetLastError();
 }
