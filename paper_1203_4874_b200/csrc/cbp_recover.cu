@@ -2178,26 +2178,39 @@ __global__ void __launch_bounds__(CONV2_THREADS, 4) k_conv_resid2(ConvResidArgs 
   }
   const float* X = a.X + size_t(plane) * a.x_plane;
   const float* Y = a.Y + size_t(plane) * a.y_plane;
-  #ifndef CBP_CONV2_LB
-#define CBP_CONV2_LB 8
+  {
+    // tile fill by rows: warp w takes rows w, w + NW, ...; lane l reads tile columns l + 32c
+    // (coalesced 128-byte row segments, no index division), RB rows of loads in flight per
+    // batch. Tile column lj = l + 32c lands at (lj >> 1) = (l >> 1) + 16c of te (even l) or to.
+#ifndef CBP_CONV2_RB
+#define CBP_CONV2_RB 1
 #endif
-  constexpr int LB = CBP_CONV2_LB;
-  for (int base = threadIdx.x; base < th * tw; base += LB * blockDim.x) {
-    float xv[LB];
+    constexpr int NW = CONV2_THREADS / 32, RB = CBP_CONV2_RB, NCH = (VT_C + kWideMaxWidth - 1 + 31) / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gi0 = i0 - tp + 1, gj0 = j0 - t + 1;
+    for (int lr = warp; lr < th; lr += NW * RB) {
+      float xv[RB][NCH];
 #pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int idx = base + u * blockDim.x;
-      const int li = idx / tw, lj = idx - li * tw;
-      const int gi = i0 - tp + 1 + li, gj = j0 - t + 1 + lj;
-      const bool in = idx < th * tw && gi >= 0 && gi < xr && gj >= 0 && gj < xc;
-      xv[u] = in ? __ldg(X + size_t(gi) * a.xld + gj) : 0.f;
-    }
+      for (int r = 0; r < RB; ++r) {
+        const int gi = gi0 + lr + NW * r;
+        const bool rin = lr + NW * r < th && gi >= 0 && gi < xr;
+        const float* row = X + size_t(rin ? gi : 0) * a.xld;
 #pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int idx = base + u * blockDim.x;
-      if (idx < th * tw) {
-        const int li = idx / tw, lj = idx - li * tw;
-        ((lj & 1) ? to : te)[li * twh + (lj >> 1)] = double(xv[u]);
+        for (int c = 0; c < NCH; ++c) {
+          const int lj = lane + 32 * c, gj = gj0 + lj;
+          xv[r][c] = 0.f;
+          if (32 * c < tw && rin && lj < tw && gj >= 0 && gj < xc) xv[r][c] = __ldg(row + gj);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int li = lr + NW * r;
+        if (li < th) {
+          double* dst = ((lane & 1) ? to : te) + li * twh + (lane >> 1);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+            if (lane + 32 * c < tw) dst[16 * c] = double(xv[r][c]);
+        }
       }
     }
   }
