@@ -505,8 +505,8 @@ def run_c3(args, world, rank, local):
         barrier(world)
         e2e_s = max_over_ranks(t1 - t0, world)
         frame_bytes = CH * Mb * Nb * 4
-        # D2H: the first Mb - tmin + 1 rows of each plane, tmin = search_min (9)
-        crop_bytes = CH * (Mb - 9 + 1) * Nb * 4
+        # D2H: one block per frame ending at row Mb - tmin of the last plane, tmin = search_min (9)
+        crop_bytes = ((CH - 1) * Mb + (Mb - 9 + 1)) * Nb * 4
         e2e = {"value": EPOCH * nE * world / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * crop_bytes,
                "steps": nE, "host_memory": "pinned",

@@ -19,6 +19,8 @@ for e in range(NE):
     hpub[EPOCH * e:EPOCH * (e + 1)].copy_(p.cpu())
     hprv[EPOCH * e].copy_(q[0].cpu())
     rec[EPOCH * e] = 1
+if os.environ.get("E2E_ONE_RECOVERY"):  # A/B: only the run's first frame recovers (no recovery stalls)
+    rec[EPOCH:] = 0
 hout = torch.empty_like(hpub).pin_memory()
 cfg = api.make_cfg(9, 25, 1e-6, validate=True)
 api.decode_run_host(hpub[:EPOCH], hprv[:EPOCH], rec[:EPOCH], cfg, out=hout[:EPOCH])
