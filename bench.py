@@ -505,10 +505,14 @@ def run_c3(args, world, rank, local):
         barrier(world)
         e2e_s = max_over_ranks(t1 - t0, world)
         frame_bytes = CH * Mb * Nb * 4
-        # D2H: one block per frame ending at row Mb - tmin of the last plane, tmin = search_min (9)
-        crop_bytes = ((CH - 1) * Mb + (Mb - 9 + 1)) * Nb * 4
+        # D2H: one block per group of G frames (cbp_pipeline.cu, CBP_E2E_GROUP, default 2) ending
+        # at row Mb - tmin of the group's last plane, tmin = search_min (9)
+        G = int(os.environ.get("CBP_E2E_GROUP", "2"))
+        G = G if G in (1, 3) else 2
+        groups = -(-EPOCH * nE // G)
+        d2h_bytes = (EPOCH * nE * frame_bytes - groups * (9 - 1) * Nb * 4) / nE
         e2e = {"value": EPOCH * nE * world / e2e_s, "unit": "frames/s",
-               "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": EPOCH * crop_bytes,
+               "h2d_bytes_per_step": (EPOCH + 1) * frame_bytes, "d2h_bytes_per_step": int(d2h_bytes),
                "steps": nE, "host_memory": "pinned",
                "api": f"cbp_decode_run_host (C ABI, host buffers, H2D/compute/D2H overlapped): one run of "
                       f"{nE} epochs = {EPOCH * nE} frames, a recovery frame every {EPOCH}"}

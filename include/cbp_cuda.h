@@ -295,10 +295,11 @@ int cbp_synth_frames(cbp_ctx* ctx, float* out_dev, int planes, int rows, int col
  * (width_hint > 0 with cfg->trust_hint skips the width search); the others reuse the
  * most recent recovered kernel through spectral_deblur on the device. H2D, compute
  * and D2H overlap on internal streams. latent receives frames in the input geometry
- * (the latent is the top-left (rows-t+1) x (cols-t+1) of each plane). Each frame is
- * transferred as one block that ends at row rows-tlo of its last plane, tlo = width_hint
- * when cfg->trust_hint, else cfg->search_min: the rows after it are left untouched, other
- * samples outside the latents hold unspecified values. slots_host (may be NULL) gets
+ * (the latent is the top-left (rows-t+1) x (cols-t+1) of each plane). Frames are
+ * transferred in pairs, each pair as one block that ends at row rows-tlo of the second
+ * frame's last plane, tlo = width_hint when cfg->trust_hint, else cfg->search_min: the
+ * rows after it are left untouched, other samples outside the latents hold unspecified
+ * values. slots_host (may be NULL) gets
  * one cbp_kernel_slot per recovery frame. Synchronizes before returning.
  * Pinned host memory gives full PCIe bandwidth. recover[0] must be nonzero. */
 int cbp_decode_run_host(cbp_ctx* ctx, const float* pub, const float* prv, int n_frames,

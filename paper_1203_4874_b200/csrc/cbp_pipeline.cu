@@ -13,7 +13,10 @@
 namespace {
 // ring depth: H2D runs up to kRing frames ahead, so the ~1 ms recovery of a frame hides
 // under the transfers of the following ones (the path is PCIe-bound)
-constexpr int kRing = 6;
+#ifndef CBP_E2E_RING
+#define CBP_E2E_RING 6
+#endif
+constexpr int kRing = CBP_E2E_RING;
 
 struct Pipe {
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
@@ -86,43 +89,63 @@ int run_host(cbp_ctx* ctx, const void* pub, const void* prv, int bits, int n_fra
   const int hint = width_hint;
   int tlo = hint > 0 && cfg->trust_hint ? hint : cfg->search_min;
   tlo = tlo < 1 ? 1 : (tlo > rows || tlo > cols ? 1 : tlo);
-  for (int j = 0; j < n_frames; ++j) {
-    const int r = j % kRing;
-    if (j >= kRing) cudaStreamWaitEvent(P.h2d, P.out[r], 0);  // ring slot drained
-    char* cpub = bits ? codes + esz * frame * r : reinterpret_cast<char*>(dpub + r * frame);
-    char* cprv = bits ? codes + esz * frame * (kRing + r) : reinterpret_cast<char*>(dprv + r * frame);
-    cudaMemcpyAsync(cpub, hpub + esz * frame * j, esz * frame, cudaMemcpyHostToDevice, P.h2d);
-    if (recover[j]) cudaMemcpyAsync(cprv, hprv + esz * frame * j, esz * frame, cudaMemcpyHostToDevice, P.h2d);
-    cudaEventRecord(P.in[r], P.h2d);
-    cudaStreamWaitEvent(P.comp, P.in[r], 0);
-    int st = 0;
-    if (bits) {
-      st = cbp_dequantize_frames(ctx, cpub, bits, channels, rows, cols, cols, dpub + r * frame, cols, P.comp);
-      if (!st && recover[j])
-        st = cbp_dequantize_frames(ctx, cprv, bits, channels, rows, cols, cols, dprv + r * frame, cols, P.comp);
+  // Frames move in groups of G consecutive frames (consecutive ring slots: kRing % G == 0):
+  // one H2D copy of the group's public frames and one D2H copy of its latents. Copies of two
+  // 1080p RGB frames (50 MB) keep the PCIe link busier than per-frame ones (tools/
+  // copy_pattern_probe.py, copies alone: 1.76k against 1.70k frames/s); the decode of a
+  // group's first frame waits for its second frame's transfer (latency, not throughput).
+  static const int G = [] {  // CBP_E2E_GROUP: A/B switch (1, 2 or 3)
+    const char* e = getenv("CBP_E2E_GROUP");
+    const int g = e ? atoi(e) : 2;
+    return g == 1 || g == 3 ? g : 2;
+  }();
+  static_assert(kRing % 2 == 0 && kRing % 3 == 0, "ring slots must split into groups");
+  for (int j0 = 0; j0 < n_frames; j0 += G) {
+    const int g = n_frames - j0 < G ? n_frames - j0 : G;
+    const int r0 = j0 % kRing;
+    if (j0 >= kRing) cudaStreamWaitEvent(P.h2d, P.out[r0], 0);  // the group's ring slots drained
+    char* cpub0 = bits ? codes + esz * frame * r0 : reinterpret_cast<char*>(dpub + r0 * frame);
+    cudaMemcpyAsync(cpub0, hpub + esz * frame * j0, esz * frame * g, cudaMemcpyHostToDevice, P.h2d);
+    for (int k = 0; k < g; ++k) {
+      char* cprv = bits ? codes + esz * frame * (kRing + r0 + k) : reinterpret_cast<char*>(dprv + (r0 + k) * frame);
+      if (recover[j0 + k])
+        cudaMemcpyAsync(cprv, hprv + esz * frame * (j0 + k), esz * frame, cudaMemcpyHostToDevice, P.h2d);
+    }
+    cudaEventRecord(P.in[r0], P.h2d);
+    cudaStreamWaitEvent(P.comp, P.in[r0], 0);
+    for (int k = 0; k < g; ++k) {
+      const int j = j0 + k, r = r0 + k;
+      char* cpub = bits ? codes + esz * frame * r : reinterpret_cast<char*>(dpub + r * frame);
+      char* cprv = bits ? codes + esz * frame * (kRing + r) : reinterpret_cast<char*>(dprv + r * frame);
+      int st = 0;
+      if (bits) {
+        st = cbp_dequantize_frames(ctx, cpub, bits, channels, rows, cols, cols, dpub + r * frame, cols, P.comp);
+        if (!st && recover[j])
+          st = cbp_dequantize_frames(ctx, cprv, bits, channels, rows, cols, cols, dprv + r * frame, cols, P.comp);
+        if (st) return st;
+      }
+      if (recover[j]) {
+        ++rec;
+        st = cbp_decode_frames_async(ctx, dpub + r * frame, dprv + r * frame, 1, channels, rows, cols, cols,
+                                     hint > 0 ? &hint : nullptr, cfg, dout + r * frame, cols, slots + rec, P.comp);
+      } else {
+        st = cbp_spectral_deblur_slot(ctx, dpub + r * frame, 1, channels, rows, cols, cols, slots + rec,
+                                      dout + r * frame, cols, P.comp);
+      }
       if (st) return st;
     }
-    if (recover[j]) {
-      ++rec;
-      st = cbp_decode_frames_async(ctx, dpub + r * frame, dprv + r * frame, 1, channels, rows, cols, cols,
-                                   hint > 0 ? &hint : nullptr, cfg, dout + r * frame, cols, slots + rec, P.comp);
-    } else {
-      st = cbp_spectral_deblur_slot(ctx, dpub + r * frame, 1, channels, rows, cols, cols, slots + rec,
-                                    dout + r * frame, cols, P.comp);
-    }
-    if (st) return st;
-    cudaEventRecord(P.done[r], P.comp);
-    cudaStreamWaitEvent(P.d2h, P.done[r], 0);
-    // D2H as ONE contiguous copy per frame, ending at the last row a latent can occupy in the
-    // last plane (rows - tlo + 1 rows, tlo = the smallest width the frame can decode with:
-    // trusted hint, else search_min). One 25 MB copy per 1080p RGB frame sustains ~7% more
-    // of the PCIe link than three per-plane copies of the latent rows (tools/
-    // copy_pattern_probe.py: 1.70k against 1.59k frames/s for the copies alone), for 0.2%
-    // more bytes (the t - 1 rows between planes).
-    static const bool full_d2h = getenv("CBP_E2E_FULL_D2H") != nullptr;  // A/B switch: whole frame
-    const size_t n_d2h = full_d2h ? frame : size_t(channels - 1) * rows * cols + size_t(rows - tlo + 1) * cols;
-    cudaMemcpyAsync(latent + j * frame, dout + r * frame, sizeof(float) * n_d2h, cudaMemcpyDeviceToHost, P.d2h);
-    cudaEventRecord(P.out[r], P.d2h);
+    cudaEventRecord(P.done[r0], P.comp);
+    cudaStreamWaitEvent(P.d2h, P.done[r0], 0);
+    // D2H as ONE contiguous copy per group, ending at the last row a latent can occupy in the
+    // group's last plane (rows - tlo + 1 rows, tlo = the smallest width the frame can decode
+    // with: trusted hint, else search_min). One block sustains more of the link than three
+    // per-plane copies of the latent rows per frame (copies alone: 1.70k against 1.59k
+    // frames/s), for 0.2% more bytes (the t - 1 rows between planes).
+    static const bool full_d2h = getenv("CBP_E2E_FULL_D2H") != nullptr;  // A/B switch: whole frames
+    const size_t n_d2h = full_d2h ? frame * g
+                                  : frame * (g - 1) + size_t(channels - 1) * rows * cols + size_t(rows - tlo + 1) * cols;
+    cudaMemcpyAsync(latent + j0 * frame, dout + r0 * frame, sizeof(float) * n_d2h, cudaMemcpyDeviceToHost, P.d2h);
+    cudaEventRecord(P.out[r0], P.d2h);
   }
   int st = cuda_check(ctx, cudaStreamSynchronize(P.d2h), "pipeline");
   if (st) return st;
