@@ -497,7 +497,9 @@ def run_c3(args, world, rank, local):
             hprv[EPOCH * e].copy_(prv[e % E, 0].cpu())
             rec[EPOCH * e] = 1
         hout = torch.empty_like(hpub).pin_memory()
-        api.decode_run_host(hpub[:EPOCH], hprv[:EPOCH], rec[:EPOCH], cfg, out=hout[:EPOCH], device=local)  # warm-up
+        # warm-up: the whole run once, so every pinned page has been mapped for DMA before the
+        # timed run (a first pass over fresh pinned buffers measured ~3% slower)
+        api.decode_run_host(hpub, hprv, rec, cfg, out=hout, device=local)
         barrier(world)
         t0 = time.perf_counter()
         _, sl = api.decode_run_host(hpub, hprv, rec, cfg, out=hout, device=local)
