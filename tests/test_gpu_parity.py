@@ -280,6 +280,37 @@ def test_split_decode_equals_decode(oracle, api, geom):
     assert torch.equal(out[..., : rows, : cols], ref[..., : rows, : cols])
 
 
+@pytest.mark.parametrize("rec", [[1], [1, 0, 0, 0, 0, 1, 1], [1, 1, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0]])
+def test_host_pipeline_pairs(oracle, api, rec):
+    """cbp_decode_run_host moves frames in pairs (one H2D and one D2H copy per two frames,
+    ring of 6 device slots): a single frame, an odd run with recovery frames in the second
+    slot of a pair and at the end, and a run longer than the ring all give, frame by frame,
+    the latents of the device path (decode_frame for recovery frames, spectral_deblur with
+    the latest recovered kernel otherwise)."""
+    pairs = [oracle.generate_coprime_pair(5, 31), oracle.generate_coprime_pair(5, 32)]
+    n = len(rec)
+    which, cur = [], -1
+    for r in rec:
+        cur = (cur + 1) % 2 if r else cur
+        which.append(cur)
+    frames = [oracle.encode_frame(oracle.random_frame(40, 52, 3, 70 + i), pairs[which[i]].k1, pairs[which[i]].k2)
+              for i in range(n)]
+    pub = torch.from_numpy(np.stack([f[0] for f in frames]).astype(np.float32)).pin_memory()
+    prv = torch.from_numpy(np.stack([f[1] for f in frames]).astype(np.float32)).pin_memory()
+    cfg = api.make_cfg(3, 9)
+    out, slots = api.decode_run_host(pub, prv, rec, cfg)
+    assert len(slots) == sum(rec) and all(s.status == 0 and s.width == 5 for s in slots)
+    k = -1
+    for i in range(n):
+        if rec[i]:
+            k += 1
+            ref = api.decode_frame(pub[i], prv[i], cfg=cfg).latent.cpu()
+        else:
+            w = np.array(slots[k].weights[:25]).reshape(5, 5)
+            ref = api.spectral_deblur(pub[i:i + 1].cuda(), w, slots[k].epsilon)[0].cpu()
+        assert torch.equal(out[i, :, :40, :52], ref), i
+
+
 def test_host_pipeline_equals_device_path(oracle, api):
     pair = oracle.generate_coprime_pair(5, 31)
     frames = [oracle.encode_frame(oracle.random_frame(60, 70, 1, 40 + i), pair.k1, pair.k2) for i in range(5)]
