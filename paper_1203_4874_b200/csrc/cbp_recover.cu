@@ -578,26 +578,74 @@ __device__ double apply_A(const double2* p, int lp, const double2* q, int lq, in
   return tot;
 }
 
-// g = A^H r (length 2t) into smem.
+// g = A^H r (length 2t) into smem: g[j] = sum_m conj(p[m]) r[m + j], g[t + j] = -sum_m
+// conj(q[m]) r[m + j], j < t. Long slices: threads stride over m (coalesced) and keep AH_JB
+// lags of both sums in registers, so one load of p[m] and q[m] serves AH_JB lags (a warp per
+// lag walking m serially left the refinement latency-bound at 1080p / 4K); partials are
+// reduced in a fixed order. Short slices keep a warp per lag (the register reduction costs
+// more than it saves there).
+#ifndef CBP_AH_JB
+#define CBP_AH_JB 8
+#endif
 __device__ void apply_AH(const double2* p, int lp, const double2* q, int lq, int t, const double2* r,
                          double2* g) {
+  constexpr int JB = CBP_AH_JB;
+  __shared__ double2 part[8][2 * JB];  // [warp][lag of p | lag of q]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < 2 * t; j += nw) {
-    const bool isq = j >= t;
-    const int sh = isq ? j - t : j;
-    const double2* v = isq ? q : p;
-    const int len = isq ? lq : lp;
-    double re = 0.0, im = 0.0;
-    for (int m = lane; m < len; m += 32) {
-      const double2 c = zcmul(v[m], r[m + sh]);
-      re += c.x;
-      im += c.y;
+  const int len = max(lp, lq);
+  if (len < 1024) {  // short slices (c1: 256 samples): a warp per lag, no register reduction
+    for (int j = warp; j < 2 * t; j += nw) {
+      const bool isq = j >= t;
+      const int sh = isq ? j - t : j;
+      const double2* v = isq ? q : p;
+      const int lv = isq ? lq : lp;
+      double re = 0.0, im = 0.0;
+      for (int m = lane; m < lv; m += 32) {
+        const double2 c = zcmul(v[m], r[m + sh]);
+        re += c.x;
+        im += c.y;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) g[j] = isq ? make_double2(-re, -im) : make_double2(re, im);
     }
-    re = warp_sum(re);
-    im = warp_sum(im);
-    if (lane == 0) g[j] = isq ? make_double2(-re, -im) : make_double2(re, im);
+    __syncthreads();
+    return;
   }
-  __syncthreads();
+  for (int j0 = 0; j0 < t; j0 += JB) {
+    double2 ap[JB], aq[JB];
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) ap[jj] = aq[jj] = make_double2(0.0, 0.0);
+    for (int m = threadIdx.x; m < len; m += blockDim.x) {
+      const double2 pm = ld_or0(p, m, lp), qm = ld_or0(q, m, lq);
+#pragma unroll
+      for (int jj = 0; jj < JB; ++jj) {
+        if (j0 + jj < t) {
+          const double2 rv = r[m + j0 + jj];
+          const double2 u = zcmul(pm, rv), v = zcmul(qm, rv);
+          ap[jj].x += u.x, ap[jj].y += u.y;
+          aq[jj].x += v.x, aq[jj].y += v.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+      ap[jj] = make_double2(warp_sum(ap[jj].x), warp_sum(ap[jj].y));
+      aq[jj] = make_double2(warp_sum(aq[jj].x), warp_sum(aq[jj].y));
+      if (lane == 0) part[warp][jj] = ap[jj], part[warp][JB + jj] = aq[jj];
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * JB) {
+      const int jj = threadIdx.x % JB;
+      const bool isq = threadIdx.x >= JB;
+      if (j0 + jj < t) {
+        double sx = 0.0, sy = 0.0;
+        for (int w = 0; w < nw; ++w) sx += part[w][threadIdx.x].x, sy += part[w][threadIdx.x].y;
+        g[(isq ? t : 0) + j0 + jj] = isq ? make_double2(-sx, -sy) : make_double2(sx, sy);
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // normalize_phase (poly.cpp:18-23): the first entry of largest modulus made real positive.
